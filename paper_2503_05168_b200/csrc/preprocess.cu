@@ -1,0 +1,343 @@
+// Hybrid preprocessing on sm_100a: device-side cluster-table lookup (K0) and
+// the fused per-splat preprocess kernel (K1).
+//
+// K1 replaces plan_frame's per-splat loop (render.py:94-126): Gaussian3D
+// rotation normalisation (model.py:122), project_detailed
+// (preprocess.py:89-146: near cull, EWA Jacobian, 0.3 low-pass, determinant
+// test, conic), sh_to_color (model.py:264-305), effective_radius_sq
+// (preprocess.py:68-71) and the bin_tiles extent box (preprocess.py:159-189).
+// All of it runs in fp64 in the reference's operation order; this file is
+// compiled with --fmad=false so no FMA contraction changes a rounding.  The
+// kernel is HBM-bound: 240 B of scene in (float4 planes, coalesced) and
+// ~140 B of records out per splat.
+#include <math.h>
+
+#include "common.cuh"
+
+namespace seele {
+
+namespace {
+
+__constant__ double kSH_C0 = 0.28209479177387814;
+__constant__ double kSH_C1 = 0.4886025119029199;
+__constant__ double kSH_C2[5] = {1.0925484305920792, -1.0925484305920792, 0.31539156525252005,
+                                 -1.0925484305920792, 0.5462742152960396};
+__constant__ double kSH_C3[7] = {-0.5900435899266435, 2.890611442640554, -0.4570457994644658,
+                                 0.3731763325901154, -0.4570457994644658, 1.445305721320277,
+                                 -0.5900435899266435};
+
+__device__ __forceinline__ void quat_to_mat(double w, double x, double y, double z, double r[9]) {
+    // model.py:83-93
+    r[0] = 1 - 2 * (y * y + z * z);
+    r[1] = 2 * (x * y - w * z);
+    r[2] = 2 * (x * z + w * y);
+    r[3] = 2 * (x * y + w * z);
+    r[4] = 1 - 2 * (x * x + z * z);
+    r[5] = 2 * (y * z - w * x);
+    r[6] = 2 * (x * z - w * y);
+    r[7] = 2 * (y * z + w * x);
+    r[8] = 1 - 2 * (x * x + y * y);
+}
+
+// sh_to_color for one channel (model.py:276-305), then +0.5 and clamp at 0.
+// `s(k)` yields coefficient k of the channel (loaded on demand: each is used once).
+template <typename Coef>
+__device__ __forceinline__ double sh_channel(Coef s, double x, double y, double z, int degree) {
+    double c = kSH_C0 * s(0);
+    if (degree >= 1) c = c - kSH_C1 * y * s(1) + kSH_C1 * z * s(2) - kSH_C1 * x * s(3);
+    if (degree >= 2) {
+        double xx = x * x, yy = y * y, zz = z * z, xy = x * y, yz = y * z, xz = x * z;
+        c = c + kSH_C2[0] * xy * s(4) + kSH_C2[1] * yz * s(5) + kSH_C2[2] * (2.0 * zz - xx - yy) * s(6) +
+            kSH_C2[3] * xz * s(7) + kSH_C2[4] * (xx - yy) * s(8);
+        if (degree >= 3) {
+            c = c + kSH_C3[0] * y * (3.0 * xx - yy) * s(9) + kSH_C3[1] * xy * z * s(10) +
+                kSH_C3[2] * y * (4.0 * zz - xx - yy) * s(11) +
+                kSH_C3[3] * z * (2.0 * zz - 3.0 * xx - 3.0 * yy) * s(12) +
+                kSH_C3[4] * x * (4.0 * zz - xx - yy) * s(13) + kSH_C3[5] * z * (xx - yy) * s(14) +
+                kSH_C3[6] * x * (xx - 3.0 * yy) * s(15);
+        }
+    }
+    c = c + 0.5;
+    return c > 0.0 ? c : 0.0;
+}
+
+// _axis_range (preprocess.py:149-156): inclusive [first, last]; first > last = none.
+__device__ __forceinline__ void axis_range(double lo, double hi, int n_tiles, int &first, int &last) {
+    double f = floor(lo / kTile);
+    if (f * kTile == lo) f -= 1.0;
+    double l = floor(hi / kTile);
+    f = f < 0.0 ? 0.0 : f;
+    l = l > (double)(n_tiles - 1) ? (double)(n_tiles - 1) : l;
+    if (!(f <= l)) {
+        first = 1;
+        last = 0;
+    } else {
+        first = (int)f;
+        last = (int)l;
+    }
+}
+
+struct Splat {
+    double p[3], s[3], q[4], o;
+    float shf[48];  // planes layout: SH stays fp32 (exact) until use
+};
+
+__device__ __forceinline__ double sigmoid_clip(double x) {
+    // io.py:33-34 _decode_opacity = clip(sigmoid(x), 1e-12, 1 - 1e-12); sigmoid model.py:44-54
+    double v;
+    if (x >= 0.0) {
+        v = 1.0 / (1.0 + exp(-x));
+    } else {
+        double e = exp(x);
+        v = e / (1.0 + e);
+    }
+    v = v < 1e-12 ? 1e-12 : v;
+    v = v > 1.0 - 1e-12 ? 1.0 - 1e-12 : v;
+    return v;
+}
+
+__device__ __forceinline__ void normalize4(double q[4]) {
+    double nrm = sqrt(q[0] * q[0] + q[1] * q[1] + q[2] * q[2] + q[3] * q[3]);
+    q[0] = q[0] / nrm;
+    q[1] = q[1] / nrm;
+    q[2] = q[2] / nrm;
+    q[3] = q[3] / nrm;
+}
+
+template <int LAYOUT>
+__device__ __forceinline__ void load_splat(const SceneK &sc, long long i, int sh_planes, Splat &g) {
+    if (LAYOUT == SEELE_LAYOUT_PLANES) {
+        const long long st = sc.plane_stride;
+        float4 p0 = __ldg(sc.planes + 0 * st + i);
+        float4 p1 = __ldg(sc.planes + 1 * st + i);
+        float4 p2 = __ldg(sc.planes + 2 * st + i);
+        g.p[0] = p0.x; g.p[1] = p0.y; g.p[2] = p0.z;
+        g.o = sigmoid_clip((double)p0.w);
+        g.s[0] = p1.x; g.s[1] = p1.y; g.s[2] = p1.z;
+        g.q[0] = p2.x; g.q[1] = p2.y; g.q[2] = p2.z; g.q[3] = p2.w;
+        normalize4(g.q);  // container decode (io.py:226-229)
+        #pragma unroll
+        for (int ch = 0; ch < 3; ch++) {
+            #pragma unroll
+            for (int k = 0; k < 4; k++) {
+                float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+                if (k < sh_planes) v = __ldg(sc.planes + (3 + 4 * ch + k) * st + i);
+                g.shf[16 * ch + 4 * k + 0] = v.x;
+                g.shf[16 * ch + 4 * k + 1] = v.y;
+                g.shf[16 * ch + 4 * k + 2] = v.z;
+                g.shf[16 * ch + 4 * k + 3] = v.w;
+            }
+        }
+    } else {
+        for (int k = 0; k < 3; k++) {
+            g.p[k] = sc.pos[3 * i + k];
+            g.s[k] = sc.log_scale[3 * i + k];
+        }
+        for (int k = 0; k < 4; k++) g.q[k] = sc.rot[4 * i + k];
+        g.o = sc.opac[i];
+    }
+    normalize4(g.q);  // Gaussian3D.__post_init__ (model.py:122, 76-80)
+}
+
+__device__ __forceinline__ void warp_count_add(int64_t *dst, int pred) {
+    unsigned b = __ballot_sync(0xffffffffu, pred);
+    if ((threadIdx.x & 31) == 0 && b) atomicAdd((unsigned long long *)dst, (unsigned long long)__popc(b));
+}
+
+template <int LAYOUT>
+__global__ void __launch_bounds__(256) k_preprocess(SceneK sc, const int64_t *__restrict__ ranges,
+                                                    int n_ranges, CamK cam, CfgK cfg, Workspace ws,
+                                                    int64_t *stats) {
+    __shared__ long long s_start[SEELE_MAX_RANGES], s_prefix[SEELE_MAX_RANGES + 1];
+    if (threadIdx.x == 0) {
+        long long acc = 0;
+        for (int r = 0; r < n_ranges; r++) {
+            s_start[r] = ranges[2 * r];
+            s_prefix[r] = acc;
+            acc += ranges[2 * r + 1];
+        }
+        s_prefix[n_ranges] = acc;
+        if (blockIdx.x == 0) {
+            ws.counters[CNT_WS] = (uint32_t)acc;
+            stats[SEELE_STAT_WORKING_SET] = acc;
+        }
+    }
+    __syncthreads();
+    const long long n_ws = s_prefix[n_ranges];
+    const int sh_planes = cfg.sh_degree >= 3 ? 4 : (cfg.sh_degree == 2 ? 3 : 1);
+    const long long stride = (long long)gridDim.x * blockDim.x;
+    const long long n_iter = (n_ws + stride - 1) / stride;  // uniform trip count for the warp votes
+    for (long long it = 0; it < n_iter; it++) {
+        const long long p = it * stride + (long long)blockIdx.x * blockDim.x + threadIdx.x;
+        const bool active = p < n_ws;
+        int status = 3;  // 3 = inactive lane
+        uint32_t n_tiles = 0;
+        if (active) {
+            int r = 0;
+            while (r + 1 < n_ranges && s_prefix[r + 1] <= p) r++;
+            const long long i = s_start[r] + (p - s_prefix[r]);
+            Splat g;
+            load_splat<LAYOUT>(sc, i, sh_planes, g);
+            double d[3] = {g.p[0] - cam.pos[0], g.p[1] - cam.pos[1], g.p[2] - cam.pos[2]};
+            double t[3];
+            for (int k = 0; k < 3; k++) t[k] = cam.w2v[3 * k] * d[0] + cam.w2v[3 * k + 1] * d[1] + cam.w2v[3 * k + 2] * d[2];
+            const double z = t[2];
+            short4 rect = make_short4(1, 0, 1, 0);
+            if (z <= cam.near_clip) {
+                status = 1;  // "near" (preprocess.py:101-103)
+            } else {
+                const double m0 = cam.fx * t[0] / z + cam.cx;  // preprocess.py:107
+                const double m1 = cam.fy * t[1] / z + cam.cy;
+                const double j00 = cam.fx / z, j02 = -cam.fx * t[0] / (z * z);
+                const double j11 = cam.fy / z, j12 = -cam.fy * t[1] / (z * z);
+                double jw[6];
+                for (int c = 0; c < 3; c++) {
+                    jw[c] = j00 * cam.w2v[c] + 0.0 * cam.w2v[3 + c] + j02 * cam.w2v[6 + c];
+                    jw[3 + c] = 0.0 * cam.w2v[c] + j11 * cam.w2v[3 + c] + j12 * cam.w2v[6 + c];
+                }
+                double rg[9];
+                quat_to_mat(g.q[0], g.q[1], g.q[2], g.q[3], rg);
+                const double es[3] = {exp(g.s[0]), exp(g.s[1]), exp(g.s[2])};
+                double m[9], cv[9], cov[9];
+                for (int a = 0; a < 3; a++)
+                    for (int b = 0; b < 3; b++) m[3 * a + b] = rg[3 * a + b] * es[b];
+                for (int a = 0; a < 3; a++)
+                    for (int b = 0; b < 3; b++)
+                        cv[3 * a + b] = m[3 * a] * m[3 * b] + m[3 * a + 1] * m[3 * b + 1] + m[3 * a + 2] * m[3 * b + 2];
+                for (int a = 0; a < 3; a++)
+                    for (int b = 0; b < 3; b++) cov[3 * a + b] = 0.5 * (cv[3 * a + b] + cv[3 * b + a]);
+                double tmp[6], c2[4];
+                for (int a = 0; a < 2; a++)
+                    for (int c = 0; c < 3; c++)
+                        tmp[3 * a + c] = jw[3 * a] * cov[c] + jw[3 * a + 1] * cov[3 + c] + jw[3 * a + 2] * cov[6 + c];
+                for (int a = 0; a < 2; a++)
+                    for (int c = 0; c < 2; c++)
+                        c2[2 * a + c] = tmp[3 * a] * jw[3 * c] + tmp[3 * a + 1] * jw[3 * c + 1] + tmp[3 * a + 2] * jw[3 * c + 2];
+                c2[0] += 0.3;  // COV2D_LOWPASS (preprocess.py:24, 117)
+                c2[3] += 0.3;
+                const double s00 = 0.5 * (c2[0] + c2[0]), s01 = 0.5 * (c2[1] + c2[2]);
+                const double s10 = 0.5 * (c2[2] + c2[1]), s11 = 0.5 * (c2[3] + c2[3]);
+                const double det = s00 * s11 - s01 * s10;
+                if (!isfinite(det) || det <= 1e-12) {
+                    status = 2;  // "degenerate" (preprocess.py:122-124)
+                } else {
+                    status = 0;
+                    const double ca = s11 / det, cb = -s01 / det, cc = s00 / det;
+                    const double nrm = sqrt(d[0] * d[0] + d[1] * d[1] + d[2] * d[2]);
+                    const double vx = d[0] / nrm, vy = d[1] / nrm, vz = d[2] / nrm;
+                    float4 col;
+                    if (LAYOUT == SEELE_LAYOUT_PLANES) {
+                        col.x = (float)sh_channel([&](int k) { return (double)g.shf[k]; }, vx, vy, vz, cfg.sh_degree);
+                        col.y = (float)sh_channel([&](int k) { return (double)g.shf[16 + k]; }, vx, vy, vz, cfg.sh_degree);
+                        col.z = (float)sh_channel([&](int k) { return (double)g.shf[32 + k]; }, vx, vy, vz, cfg.sh_degree);
+                    } else {
+                        const double *shp = sc.sh + 48 * i;
+                        col.x = (float)sh_channel([&](int k) { return shp[k]; }, vx, vy, vz, cfg.sh_degree);
+                        col.y = (float)sh_channel([&](int k) { return shp[16 + k]; }, vx, vy, vz, cfg.sh_degree);
+                        col.z = (float)sh_channel([&](int k) { return shp[32 + k]; }, vx, vy, vz, cfg.sh_degree);
+                    }
+                    col.w = 0.f;
+                    double r2 = 9.0;  // MAX_RADIUS_SQ
+                    if (cfg.opacity_aware) {
+                        r2 = 2.0 * log(g.o / cfg.alpha_theta);
+                        r2 = r2 > 9.0 ? 9.0 : r2;
+                        r2 = r2 < 0.0 ? 0.0 : r2;
+                    }
+                    if (r2 > 0.0) {
+                        const double detp = ca * cc - cb * cb;
+                        const double hx = sqrt(r2 * (cc / detp)), hy = sqrt(r2 * (ca / detp));
+                        int x0, x1, y0, y1;
+                        axis_range(m0 - hx, m0 + hx, cam.tiles_x, x0, x1);
+                        axis_range(m1 - hy, m1 + hy, cam.tiles_y, y0, y1);
+                        if (x0 <= x1 && y0 <= y1) {
+                            rect = make_short4((short)x0, (short)x1, (short)y0, (short)y1);
+                            n_tiles = (uint32_t)(x1 - x0 + 1) * (uint32_t)(y1 - y0 + 1);
+                        }
+                    }
+                    ws.depth[p] = z;
+                    ws.mean[p] = make_double2(m0, m1);
+                    ws.conic_op[p] = make_double4(ca, cb, cc, g.o);
+                    ws.color[p] = col;
+                    // FAST raster alpha-test bracket (raster.cu): alpha >= theta  <=>  q <= q_th =
+                    // 2 ln(o / theta) (rasterize.py:146-151, 209).  The kernel rounds its fp64 q to
+                    // fp32 (rel. 2^-24) and its fp64 q differs from numpy's by <= 1e-15 kappa,
+                    // kappa = 2 (a + c) / lambda_min bounding the term cancellation.
+                    const double qth = 2.0 * log(g.o / cfg.alpha_theta);
+                    const double tr = ca + cc, disc = sqrt(0.25 * (ca - cc) * (ca - cc) + cb * cb);
+                    const double lmin = fmax(0.5 * tr - disc, 1e-300);
+                    const double slack = 1.3e-7 + 1e-15 * (2.0 * tr / lmin);
+                    float q_lo = -INFINITY, q_hi = -INFINITY;
+                    if (qth >= 0.0) {
+                        q_lo = __double2float_rd(qth * (1.0 - slack) - 1e-30);
+                        q_hi = slack < 0.5 ? __double2float_ru(qth * (1.0 + slack) + 1e-30) : INFINITY;
+                    }
+                    ws.fast[p] = make_float4(q_lo, q_hi, (float)g.o, 0.f);
+                }
+            }
+            ws.status[p] = (uint8_t)status;
+            ws.rect[p] = rect;
+            ws.tiles[p] = n_tiles;
+        }
+        warp_count_add(stats + SEELE_STAT_CULLED_NEAR, status == 1);
+        warp_count_add(stats + SEELE_STAT_DROPPED_DEGENERATE, status == 2);
+        warp_count_add(stats + SEELE_STAT_PROJECTED, status == 0);
+        warp_count_add(stats + SEELE_STAT_BINNED, n_tiles > 0);
+    }
+}
+
+// K0: select_clusters (residency.py:38-54) with pose_feature (compiler.py:113-121).
+__global__ void k_select(CamK cam, const double *__restrict__ centroids, int n, int m, double beta,
+                         double3 mean3, double scale, const int64_t *__restrict__ chunks,
+                         int32_t *out_ids, int64_t *ranges_out) {
+    __shared__ double d2[1024];
+    double f[6];
+    f[0] = (cam.pos[0] - mean3.x) / scale;
+    f[1] = (cam.pos[1] - mean3.y) / scale;
+    f[2] = (cam.pos[2] - mean3.z) / scale;
+    // CameraPose.forward = R_cw[:, 2] (model.py:174-176) = row 2 of world_to_view
+    f[3] = beta * cam.w2v[6];
+    f[4] = beta * cam.w2v[7];
+    f[5] = beta * cam.w2v[8];
+    for (int c = threadIdx.x; c < n; c += blockDim.x) {
+        double s = 0.0;
+        for (int k = 0; k < 6; k++) {
+            double v = centroids[6 * c + k] - f[k];
+            s = s + v * v;
+        }
+        d2[c] = s;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        ranges_out[0] = chunks[0];
+        ranges_out[1] = chunks[1];
+        unsigned long long used[16] = {0};
+        for (int s = 0; s <= m; s++) {
+            int best = -1;
+            for (int c = 0; c < n; c++) {
+                if ((used[c >> 6] >> (c & 63)) & 1ull) continue;
+                if (best < 0 || d2[c] < d2[best]) best = c;  // np.lexsort((arange, d2)): ties -> smaller id
+            }
+            used[best >> 6] |= 1ull << (best & 63);
+            out_ids[s] = best;
+            ranges_out[2 * (s + 1)] = chunks[2 * (best + 1)];
+            ranges_out[2 * (s + 1) + 1] = chunks[2 * (best + 1) + 1];
+        }
+    }
+}
+
+}  // namespace
+
+void launch_preprocess(const SceneK &s, const int64_t *ranges, int n_ranges, const CamK &cam,
+                       const CfgK &cfg, const Workspace &ws, int64_t *stats, int grid, cudaStream_t st) {
+    if (s.layout == SEELE_LAYOUT_PLANES)
+        k_preprocess<SEELE_LAYOUT_PLANES><<<grid, 256, 0, st>>>(s, ranges, n_ranges, cam, cfg, ws, stats);
+    else
+        k_preprocess<SEELE_LAYOUT_F64><<<grid, 256, 0, st>>>(s, ranges, n_ranges, cam, cfg, ws, stats);
+}
+
+void launch_select(const CamK &cam, const double *centroids, int n, int m, double beta, const double *mean3,
+                   double scale, const int64_t *chunks, int32_t *out_ids, int64_t *ranges_out, cudaStream_t st) {
+    k_select<<<1, 128, 0, st>>>(cam, centroids, n, m, beta, make_double3(mean3[0], mean3[1], mean3[2]), scale, chunks, out_ids, ranges_out);
+}
+
+}  // namespace seele
