@@ -1,0 +1,370 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 Seele render path (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+Workload (BASELINE config 3): the SURVEY.md Appendix C synthetic 3M-Gaussian
+scene at 1920x1080 on the 120-frame orbit, with view-dependent cluster tables
+(24 pose clusters, M = 4 neighbours; built with the reference's clustering +
+partition rules, clusters.py) and the Seele engine (hybrid preprocessing +
+contribution-aware raster, w = 2).  A step is one frame per GPU: device
+cluster lookup -> preprocess -> depth rank -> binning/sort -> raster, image
+left in HBM.  Frames are sharded f = rank + N k (mod 120) with no data-path
+collective ("weak": per-GPU work fixed).  ``value`` = frames/s of the whole
+job (N K / max-over-ranks device time).  ``e2e`` = the same through the public
+API (ResidentRenderer.render_frame, float32 image + contributor counts + stats
+downloaded to pinned host memory every frame).
+
+``--impl reference`` times the reference algorithm on the host CPU: the C
+fp64 restatement of the reference (oracle/, OpenMP over tiles, all cores) on
+the same scene, cluster selection and frames; rank 0 only.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+METRIC = "frames/sec @1920x1080, 3M Gaussians (1/2/4/8 B200); ms/frame per stage"
+N_FRAMES = 120
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=int(os.environ.get("WORLD_SIZE", "1")))
+    ap.add_argument("--steps", type=int, default=240)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--n", type=int, default=3_000_000)
+    ap.add_argument("--width", type=int, default=1920)
+    ap.add_argument("--height", type=int, default=1080)
+    ap.add_argument("--engine", default="cr2", choices=["ref", "cr1", "cr2", "cr4"])
+    ap.add_argument("--flat", action="store_true", help="no cluster tables (whole scene every frame)")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=20)
+    return ap.parse_args()
+
+
+def engine_cfg(name: str, precision: str = "fast"):
+    from paper_2503_05168_b200.render import EngineConfig
+    if name == "ref":
+        return EngineConfig(engine="ref", precision=precision)
+    return EngineConfig(engine="cr", group_w=int(name[2]), precision=precision)
+
+
+def build_workload(args, device):
+    from paper_2503_05168_b200.clusters import ClusterTable, build_cluster_table
+    from paper_2503_05168_b200.container import container_from_table
+    from paper_2503_05168_b200.synthetic import orbit, synth
+    t0 = time.time()
+    scene = synth(args.n, 0)
+    poses = orbit(N_FRAMES, args.width, args.height)
+    if args.flat:
+        table = ClusterTable(shared_ids=np.arange(args.n), exclusive_ids=[np.zeros(0, np.int64)] * 2,
+                             discarded_ids=np.zeros(0, np.int64), centroids=np.zeros((2, 6)), beta=1.0, neighbors=0,
+                             position_mean=np.zeros(3), position_scale=1.0)
+    else:
+        table = build_cluster_table(scene, poses, n_clusters=24, neighbors=4, beta=1.0, seed=0, device=device)
+    container = container_from_table(table, scene)
+    return scene, poses, table, container, time.time() - t0
+
+
+def world():
+    rank = int(os.environ.get("RANK", "0"))
+    size = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, size, local
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("uuid,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device):
+        self.uuid = None
+        try:
+            self.uuid = str(torch.cuda.get_device_properties(device).uuid)
+        except Exception:  # pragma: no cover
+            pass
+        self.file = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                                          "-lms", "20"], stdout=self.file, stderr=subprocess.DEVNULL)
+        except FileNotFoundError:
+            self.proc = None
+        time.sleep(0.3)
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.1)
+        self.proc.terminate()
+        self.proc.wait(timeout=5)
+        self.file.flush()
+        rows = [r.split(", ") for r in Path(self.file.name).read_text().splitlines() if r.strip()]
+        mine = [r for r in rows if self.uuid is None or self.uuid.replace("GPU-", "") in r[0]] or rows
+        sm = [float(r[1]) for r in mine if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in mine if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[k] for r in mine for k in range(4) if len(r) > 5 + k and r[5 + k].strip() == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(mine)}
+
+
+def load_peaks() -> dict:
+    p = ROOT / "MEASURED_PEAKS.json"
+    return json.loads(p.read_text()) if p.exists() else {}
+
+
+def profile_traffic() -> dict:
+    p = ROOT / "profiles" / "traffic.json"
+    return json.loads(p.read_text()) if p.exists() else {}
+
+
+def cpu_baseline(container, rr, poses, cfg, frame: int = 0) -> dict:
+    """One full frame of the reference algorithm (C fp64 oracle) on all host cores."""
+    from oracle import oracle as O
+    cam = poses[frame]
+    sel = rr.select(cam)
+    ws = rr.assemble(sel)
+    threads = os.cpu_count() or 1
+    t0 = time.perf_counter()
+    O.render(ws, cam, cfg, threads=threads)
+    dt = time.perf_counter() - t0
+    return {"value": 1.0 / dt, "unit": "frames/s", "cores": threads, "kind": "port",
+            "sample": f"1 full frame (orbit frame {frame}, {len(ws)} splats in the working set), "
+                      f"oracle/seele_oracle.c fp64, {dt:.1f} s"}
+
+
+def run_reference(args):
+    rank, size, local = world()
+    if rank != 0:
+        return
+    from oracle import oracle as O
+    from paper_2503_05168_b200.residency import ResidentRenderer
+    device = torch.device("cuda", local) if torch.cuda.is_available() else None
+    scene, poses, table, container, _ = build_workload(args, device)
+    cfg = engine_cfg(args.engine)
+    # host-side cluster selection + assembly (residency.py:38-54, 217-220), no GPU involved
+    from paper_2503_05168_b200.clusters import pose_feature
+    norm = container.normalization
+
+    def select(cam):
+        f = pose_feature(cam, container.beta, norm)
+        d2 = np.sum((container.centroids - f[None, :]) ** 2, axis=1)
+        return [int(i) for i in np.lexsort((np.arange(len(d2)), d2))[:1 + container.m]]
+
+    from paper_2503_05168_b200.model import SceneArrays
+
+    def assemble(sel):
+        return SceneArrays.concatenate([container.chunk_arrays(-1)] + [container.chunk_arrays(c) for c in sel])
+
+    threads = os.cpu_count() or 1
+    steps, warm = max(1, min(args.steps, 3)), min(args.warmup, 1)
+    frames = [(k * 7) % N_FRAMES for k in range(warm + steps)]
+    times = []
+    for k, f in enumerate(frames):
+        cam = poses[f]
+        t0 = time.perf_counter()
+        O.render(assemble(select(cam)), cam, cfg, threads=threads)
+        if k >= warm:
+            times.append(time.perf_counter() - t0)
+    value = steps / sum(times)
+    out = {
+        "metric": METRIC, "value": value, "unit": "frames/s", "n_gpus": args.gpus, "steps": steps, "warmup": warm,
+        "ms_per_step": 1000.0 * sum(times) / steps, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "fp64", "data": "synthetic", "impl": "reference",
+        "config": workload_config(args, container),
+        "cpu_baseline": {"value": value, "unit": "frames/s", "cores": threads, "kind": "port",
+                         "sample": f"{steps} full frames of the reference algorithm (C fp64 restatement, "
+                                   f"OpenMP over tiles) incl. host cluster selection + assembly"},
+        "e2e": {"value": value, "unit": "frames/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(out))
+
+
+def workload_config(args, container) -> dict:
+    return {
+        "workload": ("C3: synthetic 3M-Gaussian scene (SURVEY App. C synth(3e6, 0)), 1920x1080, 120-frame orbit, "
+                     "view-dependent cluster tables (24 clusters, M=4, beta=1), Seele engine (HP + CR w=2)")
+        if not args.flat and args.n == 3_000_000 else f"synth({args.n}) {args.width}x{args.height} "
+                                                       f"{'flat' if args.flat else 'clustered'}",
+        "gaussians": args.n, "width": args.width, "height": args.height, "engine": args.engine,
+        "clusters": container.num_clusters, "neighbors": container.m,
+        "shared_splats": int(container.chunks[0, 1]),
+        "frames": "f = rank + N*k mod 120",
+        "l2": "inputs larger than L2 (resident scene 720 MB vs 126 MB L2); no flush",
+    }
+
+
+def run_ours(args):
+    rank, size, local = world()
+    if not torch.cuda.is_available():
+        raise SystemExit("bench.py needs a GPU (the render path has no CPU fallback)")
+    device = torch.device("cuda", local)
+    torch.cuda.set_device(device)
+    if size > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=device)
+    from paper_2503_05168_b200 import _native
+    from paper_2503_05168_b200.render import FrameRenderer, enable_stage_timing, read_stage_timing
+    from paper_2503_05168_b200.residency import ResidentRenderer
+
+    scene, poses, table, container, setup_s = build_workload(args, device)
+    rr = ResidentRenderer(container, device=device)
+    renderer = FrameRenderer(device)
+    cfg = engine_cfg(args.engine)
+    lib = _native.load()
+    my_frames = [(rank + size * k) % N_FRAMES for k in range(args.warmup + args.steps)]
+
+    # size the tile-pair workspace for every frame this rank renders (untimed)
+    renderer.reserve(rr.n_max, args.width, args.height, pair_capacity=16 * rr.n_max)
+    need = 0
+    for f in sorted(set(my_frames)):
+        rr.select_async(poses[f])
+        _, host = renderer.render_checked(rr.scene, poses[f], cfg, ranges=rr.ranges, n_ranges=rr.m + 2, n_max=rr.n_max)
+        need = max(need, int(host[_native.STAT_TILE_PAIRS]))
+    renderer.reserve(rr.n_max, args.width, args.height, pair_capacity=int(need * 1.02) + 1024)
+
+    stream = torch.cuda.current_stream(device)
+    for f in my_frames[:args.warmup]:
+        rr.render_device(poses[f], cfg, renderer=renderer)
+    torch.cuda.synchronize(device)
+    if size > 1:
+        torch.distributed.barrier()
+    clocks = ClockSampler(device) if rank == 0 else None
+    if clocks:
+        clocks.start()
+    launches0 = lib.seele_launch_count()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize(device)
+    ev0.record(stream)
+    for f in my_frames[args.warmup:]:
+        rr.render_device(poses[f], cfg, renderer=renderer)
+    ev1.record(stream)
+    torch.cuda.synchronize(device)
+    launches = lib.seele_launch_count() - launches0
+    clock_info = clocks.stop() if clocks else None
+    last = renderer.stats.cpu().numpy()
+    ms = ev0.elapsed_time(ev1)
+    ms_t = torch.tensor([ms], dtype=torch.float64, device=device)
+    if size > 1:
+        torch.distributed.all_reduce(ms_t, op=torch.distributed.ReduceOp.MAX)
+        torch.distributed.barrier()
+    max_ms = float(ms_t.item())
+    value = size * args.steps / (max_ms / 1000.0)
+
+    # per-stage breakdown + work counters on a sample of this rank's frames (instrumented, untimed above)
+    enable_stage_timing(True)
+    sample = my_frames[args.warmup:args.warmup + min(8, args.steps)] or my_frames[:1]
+    st_acc, ctr = {}, []
+    for f in sample:
+        rr.render_device(poses[f], cfg, renderer=renderer)
+        for k, v in read_stage_timing().items():
+            st_acc[k] = st_acc.get(k, 0.0) + v / len(sample)
+        ctr.append(renderer.stats.cpu().numpy().copy())
+    enable_stage_timing(False)
+    ctr = np.mean(np.stack(ctr), axis=0)
+
+    # end to end through the public API (host output every frame)
+    e2e_frames = my_frames[args.warmup:args.warmup + max(1, min(args.e2e_steps, args.steps))]
+    rr.render_frame(poses[e2e_frames[0]], cfg, output="numpy32")
+    torch.cuda.synchronize(device)
+    if size > 1:
+        torch.distributed.barrier()
+    t0 = time.perf_counter()
+    for f in e2e_frames:
+        res = rr.render_frame(poses[f], cfg, output="numpy32")
+    e2e_s = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device=device)
+    if size > 1:
+        torch.distributed.all_reduce(e2e_s, op=torch.distributed.ReduceOp.MAX)
+    e2e_value = size * len(e2e_frames) / float(e2e_s.item())
+    d2h = args.width * args.height * (3 * 4 + 4) + 8 * _native.STAT_COUNT
+
+    if rank == 0:
+        peaks = load_peaks()
+        hbm = float(peaks.get("hbm_gbs", 6650.0))
+        sm_mhz = float(peaks.get("sm_max_mhz", 1965.0))
+        fp32_tflops = 148 * 128 * 2 * sm_mhz * 1e6 / 1e12  # nominal FFMA peak at max clock
+        # raster work model: FP32-pipe instructions ~ 8 per live (pixel, splat) step + 6 per blend
+        live, blends = float(ctr[_native.STAT_LIVE_PIXEL_STEPS]), float(ctr[_native.STAT_PIXEL_BLENDS])
+        r_ms = st_acc.get("raster", float("nan"))
+        r_tflops = 2.0 * (8.0 * live + 6.0 * blends) / (r_ms * 1e-3) / 1e12
+        traffic = profile_traffic()
+        n_ws, binned, pairs = float(ctr[_native.STAT_WORKING_SET]), float(ctr[_native.STAT_BINNED]), \
+            float(ctr[_native.STAT_TILE_PAIRS])
+        # algorithmic bytes: preprocess 240 B in per assembled splat + 52 B out per projected;
+        # depth rank 12 B read + 4 B written per binned splat; binning: 8 B emitted per pair
+        # (4 B tile key + 4 B splat index) + one read+write of both per stable sort pass
+        pre_bytes = n_ws * 240 + float(ctr[_native.STAT_PROJECTED]) * 52
+        rank_bytes = binned * 16
+        sort_bytes = pairs * (8 + 16)
+        stages = {
+            k: {"ms": round(v, 4)} for k, v in st_acc.items()
+        }
+        for k, b in (("preprocess", pre_bytes), ("depth_rank", rank_bytes), ("binning_sort", sort_bytes)):
+            if k in stages and stages[k]["ms"] > 0:
+                gbs = b / (stages[k]["ms"] * 1e-3) / 1e9
+                stages[k].update({"bound": "hbm", "algorithmic_bytes": int(b), "achieved_gbs": round(gbs, 1),
+                                  "frac": round(gbs / hbm, 4)})
+        stages["raster"].update({"bound": "fp32", "achieved_tflops": round(r_tflops, 2),
+                                 "frac": round(r_tflops / fp32_tflops, 4)})
+        out = {
+            "metric": METRIC, "value": value, "unit": "frames/s", "n_gpus": size, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": max_ms / args.steps, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "fp64+fp32", "data": "synthetic",
+            "config": {**workload_config(args, container), "parallelism": f"frame-sharded x{size}"},
+            "roofline": {"kernel": "k_raster_quad + k_fixup (raster stage)", "bound": "fp32",
+                         "achieved": round(r_tflops, 3), "peak": round(fp32_tflops, 1), "unit": "TFLOP/s",
+                         "frac": round(r_tflops / fp32_tflops, 4),
+                         "peak_source": f"nominal 148 SM x 128 FP32 lanes x 2 x {sm_mhz:.0f} MHz (no FP32 peak in "
+                                        f"MEASURED_PEAKS.json)",
+                         "work_model": "2 x (8 x live pixel-splat steps + 6 x blends) per frame (SURVEY 8d)",
+                         "traffic": traffic.get("k_raster_quad")},
+            "stages": stages,
+            "work": {"working_set": int(n_ws), "binned": int(binned), "tile_pairs": int(pairs),
+                     "live_pixel_steps": int(live), "blends": int(blends),
+                     "fixup_warps": int(ctr[_native.STAT_FIXUP_WARPS]),
+                     "alpha_redecide": int(ctr[_native.STAT_ALPHA_REDECIDE])},
+            "e2e": {"value": e2e_value, "unit": "frames/s", "h2d_bytes_per_step": 96, "d2h_bytes_per_step": d2h,
+                    "api": "ResidentRenderer.render_frame(cam, cfg, output='numpy32')"},
+            "gpu_launches": int(launches),
+            "clocks": clock_info,
+            "overflow_last_frame": int(last[_native.STAT_OVERFLOW]),
+            "setup_s": round(setup_s, 1),
+        }
+        if not args.no_cpu_baseline and size == 1:
+            out["cpu_baseline"] = cpu_baseline(container, rr, poses, cfg)
+        print(json.dumps(out))
+    if size > 1:
+        torch.distributed.destroy_process_group()
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -119,6 +119,8 @@ enum {
     SEELE_STAT_FIXUP_WARPS = 11,/* fast path: model-warps replayed in fp64 (T test undecidable in fp32) */
     SEELE_STAT_ALPHA_REDECIDE = 12, /* fast path: lane alpha tests re-decided in fp64 */
     SEELE_STAT_T_AMBIGUOUS = 13,    /* fast path: lane T < gamma tests inside the fp32 error band */
+    SEELE_STAT_LIVE_PIXEL_STEPS = 14, /* fast path: (live pixel, iterated splat) pairs */
+    SEELE_STAT_PIXEL_BLENDS = 15,     /* fast path: (pixel, splat) blends */
     SEELE_STAT_COUNT = 16
 };
 
@@ -193,6 +195,10 @@ const char *seele_last_error(void);
 
 /* ABI version (bumped on any signature change). */
 int32_t seele_abi_version(void);
+
+/* Number of CUDA kernels this library has launched in this process (all
+ * threads); bench.py reads it around its timed region. */
+int64_t seele_launch_count(void);
 
 #ifdef __cplusplus
 }

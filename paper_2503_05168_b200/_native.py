@@ -30,6 +30,8 @@ STAT_OVERFLOW = 10
 STAT_FIXUP_WARPS = 11
 STAT_ALPHA_REDECIDE = 12
 STAT_T_AMBIGUOUS = 13
+STAT_LIVE_PIXEL_STEPS = 14
+STAT_PIXEL_BLENDS = 15
 STAT_COUNT = 16
 
 LAYOUT_F64 = 0
@@ -47,6 +49,7 @@ EXPORTED_SYMBOLS = (
     "seele_profile_read",
     "seele_last_error",
     "seele_abi_version",
+    "seele_launch_count",
 )
 
 
@@ -127,6 +130,8 @@ def load(required: bool = True):
     lib.seele_last_error.restype = ctypes.c_char_p
     lib.seele_abi_version.argtypes = []
     lib.seele_abi_version.restype = I32
+    lib.seele_launch_count.argtypes = []
+    lib.seele_launch_count.restype = I64
     if lib.seele_abi_version() != ABI_VERSION:
         raise DeviceError(f"libseele_b200 ABI {lib.seele_abi_version()} != expected {ABI_VERSION}; rebuild")
     _lib = lib

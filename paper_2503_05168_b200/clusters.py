@@ -1,0 +1,179 @@
+"""View-dependent cluster tables (offline side of hybrid preprocessing).
+
+Builds the table the runtime lookup (``residency.select_clusters``, device
+kernel K0) consumes: pose clusters in the 6-D pose-feature space and the
+shared / exclusive / discarded partition of the splats.
+
+* ``compute_pose_normalization``, ``pose_feature``, ``cluster_poses`` and
+  ``partition`` restate pkg/src/seele/compiler.py:105-193, 234-261 with the
+  same numpy call sequence, so a given seed yields the reference's centroids
+  (pinned by tests/golden/clusters_orbit.npz).
+* The reference's per-pixel top-k contributor harvest (compiler.py:196-231)
+  needs a dense (P x H*W) matrix per pose and cannot run at benchmark scale;
+  for the synthetic configs the candidate set of a cluster is every splat
+  whose centre projects inside the image in front of the near plane for at
+  least one member pose.  That projection runs on the
+  GPU through torch (offline, not the render path).
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from .errors import InvalidArgumentError
+from .model import CameraPose, SceneArrays
+
+KMEANS_MAX_ITER = 100
+KMEANS_REL_TOL = 1e-6
+
+
+def compute_pose_normalization(poses) -> tuple[np.ndarray, float]:
+    """compiler.py:105-110: mean position and pose-cloud radius (1.0 if 0)."""
+    positions = np.asarray([p.position for p in poses], dtype=np.float64)
+    mean = positions.mean(axis=0)
+    radius = float(np.max(np.linalg.norm(positions - mean, axis=1))) if len(poses) else 0.0
+    return mean, radius if radius > 0.0 else 1.0
+
+
+def pose_feature(cam: CameraPose, beta: float, normalization) -> np.ndarray:
+    """compiler.py:113-121: (normalised position, beta * view direction)."""
+    mean, scale = normalization
+    if scale <= 0.0:
+        raise InvalidArgumentError("normalization scale must be positive")
+    pos = (cam.position - np.asarray(mean, dtype=np.float64)) / scale
+    return np.concatenate([pos, beta * cam.forward()])
+
+
+def _kmeans_pp_init(features: np.ndarray, k: int, rng: np.random.Generator) -> np.ndarray:
+    n = features.shape[0]
+    centroids = np.empty((k, features.shape[1]))
+    centroids[0] = features[int(rng.integers(n))]
+    d2 = np.sum((features - centroids[0]) ** 2, axis=1)
+    for c in range(1, k):
+        total = d2.sum()
+        if total <= 0.0:
+            centroids[c:] = features[0]
+            return centroids
+        centroids[c] = features[int(np.searchsorted(np.cumsum(d2 / total), rng.random()))]
+        d2 = np.minimum(d2, np.sum((features - centroids[c]) ** 2, axis=1))
+    return centroids
+
+
+def _kmeans(features: np.ndarray, k: int, seed: int) -> tuple[np.ndarray, np.ndarray]:
+    """Lloyd iterations from k-means++ seeds (compiler.py:141-165)."""
+    rng = np.random.default_rng(seed)
+    centroids = _kmeans_pp_init(features, k, rng)
+    scale = max(float(np.abs(features).max()), 1.0)
+    for _ in range(KMEANS_MAX_ITER):
+        d2 = np.sum((features[:, None, :] - centroids[None, :, :]) ** 2, axis=2)
+        labels = np.argmin(d2, axis=1)
+        updated = centroids.copy()
+        for c in range(k):
+            members = labels == c
+            if members.any():
+                updated[c] = features[members].mean(axis=0)
+            else:
+                updated[c] = features[int(np.argmax(d2[np.arange(len(features)), labels]))]
+        movement = float(np.max(np.linalg.norm(updated - centroids, axis=1)))
+        centroids = updated
+        if movement < KMEANS_REL_TOL * scale:
+            break
+    d2 = np.sum((features[:, None, :] - centroids[None, :, :]) ** 2, axis=2)
+    return centroids, np.argmin(d2, axis=1)
+
+
+@dataclass
+class PoseCluster:
+    centroid: np.ndarray
+    member_indices: list
+    member_poses: list
+
+
+def cluster_poses(poses, n_clusters: int, beta: float = 1.0, seed: int = 0, normalization=None) -> list[PoseCluster]:
+    """compiler.py:168-193."""
+    if len(poses) < n_clusters:
+        raise InvalidArgumentError(f"need at least {n_clusters} poses to build {n_clusters} clusters, got {len(poses)}")
+    normalization = normalization or compute_pose_normalization(poses)
+    features = np.stack([pose_feature(p, beta, normalization) for p in poses])
+    centroids, labels = _kmeans(features, n_clusters, seed)
+    out = []
+    for c in range(n_clusters):
+        idx = np.flatnonzero(labels == c).tolist()
+        out.append(PoseCluster(centroids[c], idx, [poses[i] for i in idx]))
+    return out
+
+
+def partition(top_sets, all_ids, share_threshold: int = 2):
+    """compiler.py:234-261: (shared, exclusive per cluster, discarded)."""
+    all_ids = np.asarray(all_ids, dtype=np.int64)
+    n_total = int(all_ids.max()) + 1 if len(all_ids) else 0
+    counts = np.zeros(n_total, dtype=np.int64)
+    owner = np.full(n_total, -1, dtype=np.int64)
+    for c in reversed(range(len(top_sets))):
+        ids = np.asarray(top_sets[c], dtype=np.int64)
+        counts[ids] += 1
+        owner[ids] = c
+    cnt = counts[all_ids]
+    shared = all_ids[cnt >= share_threshold]
+    discarded = all_ids[cnt == 0]
+    exclusive = [all_ids[(cnt >= 1) & (cnt < share_threshold) & (owner[all_ids] == c)] for c in range(len(top_sets))]
+    return shared, exclusive, discarded
+
+
+def visible_centres(scene: SceneArrays, poses, device=None) -> np.ndarray:
+    """Ids whose centre projects inside the image with z > near for >= 1 pose
+    (fp64, the mean2d / near test of preprocess.py:97-107)."""
+    import torch
+
+    dev = torch.device(device or ("cuda" if torch.cuda.is_available() else "cpu"))
+    pos = torch.as_tensor(np.asarray(scene.positions, dtype=np.float64), device=dev)
+    seen = torch.zeros(pos.shape[0], dtype=torch.bool, device=dev)
+    for cam in poses:
+        w2v = torch.as_tensor(cam.rotation_matrix().T, device=dev)
+        t = (pos - torch.as_tensor(cam.position, device=dev)) @ w2v.T
+        fx, fy = cam.focal()
+        cx, cy = cam.principal_point()
+        z = t[:, 2]
+        ok = z > cam.near_clip
+        zs = torch.where(ok, z, torch.ones_like(z))
+        mx = fx * t[:, 0] / zs + cx
+        my = fy * t[:, 1] / zs + cy
+        seen |= ok & (mx >= 0) & (mx < cam.width) & (my >= 0) & (my < cam.height)
+    return np.asarray(scene.ids)[seen.cpu().numpy()]
+
+
+@dataclass
+class ClusterTable:
+    """A compiled partition (compiler.ClusteredScene, compiler.py:45-62)."""
+
+    shared_ids: np.ndarray
+    exclusive_ids: list
+    discarded_ids: np.ndarray
+    centroids: np.ndarray
+    beta: float
+    neighbors: int
+    position_mean: np.ndarray
+    position_scale: float
+    pose_assignments: np.ndarray = field(default=None)
+    share_threshold: int = 2
+    top_k: int = 32
+    sh_degree: int = 3
+    group_w: int = 2
+    alpha_theta: float = 1.0 / 255.0
+
+
+def build_cluster_table(scene: SceneArrays, poses, n_clusters: int = 24, neighbors: int = 4, beta: float = 1.0,
+                        seed: int = 0, share_threshold: int = 2, device=None) -> ClusterTable:
+    """Cluster the trajectory's poses and partition the scene by visibility."""
+    norm = compute_pose_normalization(poses)
+    specs = cluster_poses(poses, n_clusters, beta, seed, normalization=norm)
+    sets = [visible_centres(scene, s.member_poses, device) for s in specs]
+    shared, exclusive, discarded = partition(sets, scene.ids, share_threshold)
+    assign = np.zeros(len(poses), dtype=np.int64)
+    for c, s in enumerate(specs):
+        assign[s.member_indices] = c
+    return ClusterTable(shared_ids=shared, exclusive_ids=exclusive, discarded_ids=discarded,
+                        centroids=np.stack([s.centroid for s in specs]), beta=beta, neighbors=neighbors,
+                        position_mean=np.asarray(norm[0]), position_scale=float(norm[1]), pose_assignments=assign,
+                        share_threshold=share_threshold)

@@ -3,6 +3,8 @@
 // launch sequence of one frame.  No allocation, no host synchronisation.
 #include <math.h>
 #include <stdarg.h>
+
+#include <atomic>
 #include <stdio.h>
 #include <string.h>
 
@@ -13,6 +15,7 @@ namespace seele {
 namespace {
 
 thread_local char g_err[512] = "";
+std::atomic<long long> g_launches{0};
 thread_local bool g_prof = false;
 thread_local cudaEvent_t g_ev[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
 
@@ -111,6 +114,8 @@ int check_config(const seele_config *c) {
 
 }  // namespace
 
+void note_launches(int n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
+
 Workspace carve_workspace(void *base, long long n_max, long long cap, int width, int height) {
     Carver c{static_cast<char *>(base)};
     Workspace w;
@@ -195,6 +200,8 @@ using namespace seele;
 extern "C" {
 
 int32_t seele_abi_version(void) { return 1; }
+
+int64_t seele_launch_count(void) { return g_launches.load(std::memory_order_relaxed); }
 
 const char *seele_last_error(void) { return g_err; }
 
@@ -337,6 +344,7 @@ int seele_plan_export(void *workspace, int64_t n_max, int64_t pair_capacity, int
     if (n_ws > 0)
         k_export_splats<<<(int)((n_ws + 255) / 256 < 4096 ? (n_ws + 255) / 256 : 4096), 256, 0, st>>>(
             ws, n_ws, out->status, out->depth, out->rect, out->mean, out->conic, out->opacity, out->color);
+    if (n_ws > 0) note_launches(1);
     if ((e = cudaGetLastError()) != cudaSuccess) return cuda_fail(e, "seele_plan_export");
     return SEELE_OK;
 }

@@ -253,6 +253,7 @@ int radix_sort(K *keys[2], uint32_t *vals[2], const uint32_t *n_ptr, int begin_b
         k_radix_scatter<K><<<G, 256, 0, st>>>(keys[cur], vals[cur], keys[cur ^ 1], vals[cur ^ 1], n_ptr, shift, bits,
                                               hist, tot);
         cur ^= 1;
+        note_launches(3);
     }
     return cur;
 }
@@ -329,6 +330,7 @@ void launch_depth_rank(const Workspace &ws, long long n_max, int grid, int64_t *
     k_chunk_reduce<0><<<G, 256, 0, st>>>(ws, nullptr);
     k_scan_sums<0><<<1, 1024, 0, st>>>(ws, G, 0, stats);
     k_chunk_scan<0><<<G, 256, 0, st>>>(ws, nullptr);
+    note_launches(3);
     uint64_t *k[2] = {ws.dkey[0], ws.dkey[1]};
     uint32_t *v[2] = {ws.dval[0], ws.dval[1]};
     // positive doubles order like their bit patterns; bit 63 (sign) is always 0
@@ -344,6 +346,7 @@ void launch_binning(const Workspace &ws, const uint32_t *sorted_pos, long long n
     k_scan_sums<1><<<1, 1024, 0, st>>>(ws, G, cap, stats);
     k_chunk_scan<1><<<G, 256, 0, st>>>(ws, sorted_pos);
     k_emit<<<G, 256, 0, st>>>(ws, sorted_pos, cam.tiles_x, ws.pkey[0], ws.pval[0]);
+    note_launches(4);
     const int n_tiles = cam.tiles_x * cam.tiles_y;
     int bits = 1;
     while ((1 << bits) < n_tiles) bits++;
@@ -352,6 +355,7 @@ void launch_binning(const Workspace &ws, const uint32_t *sorted_pos, long long n
     const int cur = radix_sort<uint32_t>(k, v, ws.counters + CNT_PAIRS, 0, bits, ws.hist, G, st);
     k_clear_ranges<<<(n_tiles + 255) / 256, 256, 0, st>>>(ws.ranges, n_tiles);
     k_ranges<<<G, 256, 0, st>>>(ws, k[cur]);
+    note_launches(2);
     *pair_pos = v[cur];
     *pair_tile = k[cur];
 }

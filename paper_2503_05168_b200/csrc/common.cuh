@@ -100,7 +100,10 @@ void launch_raster_fast(int W, const Workspace &ws, const uint32_t *pair_pos, co
                         const CfgK &cfg, float *image, int32_t *contrib, int64_t *stats,
                         cudaStream_t st);
 
-// generic device-count scan / sort building blocks (scan_sort.cu)
+// grid of the chunked scan / sort kernels (binning.cu)
 int chunk_grid(int sms);
+
+// Counts kernels this library has launched (seele_launch_count, api.cu).
+void note_launches(int n);
 
 }  // namespace seele

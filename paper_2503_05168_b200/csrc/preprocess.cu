@@ -333,11 +333,13 @@ void launch_preprocess(const SceneK &s, const int64_t *ranges, int n_ranges, con
         k_preprocess<SEELE_LAYOUT_PLANES><<<grid, 256, 0, st>>>(s, ranges, n_ranges, cam, cfg, ws, stats);
     else
         k_preprocess<SEELE_LAYOUT_F64><<<grid, 256, 0, st>>>(s, ranges, n_ranges, cam, cfg, ws, stats);
+    note_launches(1);
 }
 
 void launch_select(const CamK &cam, const double *centroids, int n, int m, double beta, const double *mean3,
                    double scale, const int64_t *chunks, int32_t *out_ids, int64_t *ranges_out, cudaStream_t st) {
     k_select<<<1, 128, 0, st>>>(cam, centroids, n, m, beta, make_double3(mean3[0], mean3[1], mean3[2]), scale, chunks, out_ids, ranges_out);
+    note_launches(1);
 }
 
 }  // namespace seele

@@ -123,9 +123,11 @@ void launch_engine(const Workspace &ws, const uint32_t *pair_pos, const CamK &ca
     const int n_tiles = cam.tiles_x * cam.tiles_y;
     if (cfg.precision == SEELE_PRECISION_EXACT) {
         k_raster_exact<W><<<n_tiles, 256, 0, st>>>(ws, pair_pos, cam, cfg, image, contrib, stats);
+        note_launches(1);
     } else {
         launch_raster_fast(W, ws, pair_pos, cam, cfg, image, contrib, stats, st);
         k_fixup<W><<<592, 128, 0, st>>>(ws, pair_pos, cam, cfg, image, contrib, stats);
+        note_launches(2);
     }
 }
 

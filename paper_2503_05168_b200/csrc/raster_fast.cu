@@ -139,6 +139,7 @@ __global__ void __launch_bounds__(64, 8) k_raster_quad(Workspace ws, const uint3
     }
     bool abandoned = false;
     uint32_t c_alpha = 0, c_blend = 0, c_leader = 0, n_redecide = 0, n_tamb = 0;
+    uint32_t n_live = 0, n_blend = 0;  // pixel-level work (roofline model in bench.py)
     const uint2 rg = ws.ranges[tile];
 
     for (uint32_t b0 = rg.x; b0 < rg.y; b0 += kBatch) {
@@ -173,6 +174,7 @@ __global__ void __launch_bounds__(64, 8) k_raster_quad(Workspace ws, const uint3
             if (lb == 0u) break;  // all four model-warps of this warp are done
             const Staged &sg = s_g[j];
             const uint32_t mw_live = slice_any(lb, shift);
+            n_live += __popc(live);
             float al[4], rel[4];
             uint32_t blend;
             if (W == 0 || W == 1) {
@@ -202,6 +204,7 @@ __global__ void __launch_bounds__(64, 8) k_raster_quad(Workspace ws, const uint3
             const unsigned bb = __ballot_sync(0xffffffffu, blend != 0u);
             if (bb == 0u) continue;
             c_blend += slice_any(bb, shift);
+            n_blend += __popc(blend);
             uint32_t amb = 0;
 #pragma unroll
             for (int s = 0; s < 4; s++) {  // _blend (rasterize.py:169-177), predicated per pixel
@@ -234,9 +237,14 @@ __global__ void __launch_bounds__(64, 8) k_raster_quad(Workspace ws, const uint3
     }
     const uint32_t w_red = __reduce_add_sync(0xffffffffu, n_redecide);
     const uint32_t w_tamb = __reduce_add_sync(0xffffffffu, n_tamb);
+    const uint32_t w_live = __reduce_add_sync(0xffffffffu, n_live);
+    const uint32_t w_blend = __reduce_add_sync(0xffffffffu, n_blend);
     if (lane == 0) {
-        if (w_red) atomicAdd((unsigned long long *)(stats + SEELE_STAT_ALPHA_REDECIDE), (unsigned long long)w_red);
-        if (w_tamb) atomicAdd((unsigned long long *)(stats + SEELE_STAT_T_AMBIGUOUS), (unsigned long long)w_tamb);
+        unsigned long long *st = (unsigned long long *)stats;
+        if (w_red) atomicAdd(st + SEELE_STAT_ALPHA_REDECIDE, (unsigned long long)w_red);
+        if (w_tamb) atomicAdd(st + SEELE_STAT_T_AMBIGUOUS, (unsigned long long)w_tamb);
+        if (w_live) atomicAdd(st + SEELE_STAT_LIVE_PIXEL_STEPS, (unsigned long long)w_live);
+        if (w_blend) atomicAdd(st + SEELE_STAT_PIXEL_BLENDS, (unsigned long long)w_blend);
     }
     if (abandoned) {
         if (i == 0) {

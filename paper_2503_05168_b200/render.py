@@ -249,6 +249,34 @@ class FrameRenderer:
             self.reserve(self.n_max, self.size[0], self.size[1], pair_capacity=int(need * 1.25) + 1024)
         raise DeviceError("tile-pair workspace could not be grown enough")
 
+    def render_to_host(self, scene: DeviceScene, cam: CameraPose, cfg: EngineConfig, **kw):
+        """Render and download image (float32), contributor counts and stats
+        into pinned host buffers with one synchronisation; grows the workspace
+        and re-renders on overflow.  The returned arrays are views into a
+        two-deep ring of pinned buffers: valid until two more calls."""
+        w, h = int(cam.width), int(cam.height)
+        ring = getattr(self, "_ring", None)
+        if ring is None or ring[0][0].shape[:2] != (h, w):
+            ring = self._ring = [(torch.empty((h, w, 3), dtype=torch.float32, pin_memory=True),
+                                  torch.empty((h, w), dtype=torch.int32, pin_memory=True),
+                                  torch.empty(_native.STAT_COUNT, dtype=torch.int64, pin_memory=True))
+                                 for _ in range(2)]
+            self._ring_i = 0
+        img_h, cnt_h, st_h = ring[self._ring_i]
+        self._ring_i ^= 1
+        for _ in range(4):
+            out = self.render(scene, cam, cfg, **kw)
+            st_h.copy_(out.stats, non_blocking=True)
+            img_h.copy_(out.image, non_blocking=True)
+            cnt_h.copy_(out.contrib, non_blocking=True)
+            torch.cuda.current_stream(self.device).synchronize()
+            host = st_h.numpy()
+            if not host[_native.STAT_OVERFLOW]:
+                return img_h.numpy(), cnt_h.numpy(), host.copy()
+            need = int(host[_native.STAT_TILE_PAIRS])
+            self.reserve(self.n_max, w, h, pair_capacity=int(need * 1.25) + 1024)
+        raise DeviceError("tile-pair workspace could not be grown enough")
+
     def export_plan(self, scene: DeviceScene, cam: CameraPose, host_stats: np.ndarray,
                     working_ids: np.ndarray | None = None) -> FramePlan:
         """FramePlan of the last frame rendered by this renderer (synchronises)."""
@@ -323,22 +351,30 @@ def render_frame(scene, cam: CameraPose, cfg: EngineConfig, *, record_contributi
     :class:`~.device.DeviceScene`.  ``plan`` is accepted for API
     compatibility; the GPU recomputes its plan (bit-equal discrete fields).
     ``output="numpy"`` returns the image as (H, W, 3) float64 like the
-    reference; ``"torch"`` leaves it on the device as float32.
+    reference; ``"numpy32"`` returns float32 views of pinned host buffers
+    (valid until two more renders on this device; the fast host path);
+    ``"torch"`` leaves image and counts on the device (float32 / int32).
     """
     t0 = time.perf_counter()
     if record_contributions:
         raise InvalidArgumentError("record_contributions (dense P x H*W weights) is not supported on the GPU path")
-    if output not in ("numpy", "torch"):
-        raise InvalidArgumentError(f"unknown output '{output}'")
     dscene = _as_device_scene(scene)
     renderer = get_renderer(dscene.device)
-    out, host = renderer.render_checked(dscene, cam, cfg)
-    stats = FrameStats.from_device(host)
-    if output == "numpy":
-        image = out.image.cpu().numpy().astype(np.float64)
-        count = out.contrib.cpu().numpy()
-    else:
+    return _finish(renderer, lambda **kw: renderer.render_checked(dscene, cam, cfg, **kw),
+                   lambda **kw: renderer.render_to_host(dscene, cam, cfg, **kw), output, t0, {})
+
+
+def _finish(renderer, checked, to_host, output: str, t0: float, kw: dict) -> RenderResult:
+    if output == "torch":
+        out, host = checked(**kw)
         image, count = out.image, out.contrib
+    elif output in ("numpy", "numpy32"):
+        image, count, host = to_host(**kw)
+        if output == "numpy":
+            image, count = image.astype(np.float64), count.copy()
+    else:
+        raise InvalidArgumentError(f"unknown output '{output}'")
+    stats = FrameStats.from_device(host)
     stats.wall_ms = (time.perf_counter() - t0) * 1000.0
     return RenderResult(image=image, stats=stats, contrib_count=count, device_stats=host)
 

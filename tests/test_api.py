@@ -93,7 +93,7 @@ def test_planes_roundtrip_matches_container_decode():
 
 def _header_symbols():
     text = (ROOT / "include" / "seele_b200.h").read_text()
-    return sorted(set(re.findall(r"^\s*(?:int|int32_t|size_t|const char \*)\s*(seele_\w+)\s*\(", text, re.M)))
+    return sorted(set(re.findall(r"^\s*(?:int|int32_t|int64_t|size_t|const char \*)\s*(seele_\w+)\s*\(", text, re.M)))
 
 
 def test_library_exports_header_symbols():

@@ -123,7 +123,7 @@ def test_config1_vs_reference():
 def test_synth_1080p_vs_reference(frame):
     g = load(f"synth20k_f{frame}")
     scene = synth(20_000, 0)
-    cam = orbit_pose(frame)
+    cam = camera_from(g)
     dscene = DeviceScene.from_arrays(scene)
     plan = plan_frame(dscene, cam, EngineConfig())
     pair_ids = np.stack([plan.sorted_pairs["tile_id"], plan.ids[plan.sorted_pairs["gaussian_ref"]]], axis=1)

@@ -10,6 +10,7 @@ import pytest
 from helpers import (ENGINES, SMALL_CASES, STAT_KEYS, base_cfg, camera_from, config_for, engines_in, golden_ranges,
                      load, scene_from, sha)
 from oracle import oracle as O
+from paper_2503_05168_b200.model import CameraPose
 from paper_2503_05168_b200.synthetic import config1_scene, orbit_pose, synth
 
 
@@ -91,8 +92,8 @@ def test_oracle_synth_1080p(frame):
     scene = synth(20_000, 0)
     got = [sha(scene.positions), sha(scene.log_scales), sha(scene.rotations), sha(scene.opacities), sha(scene.sh)]
     assert got == [str(v) for v in g["scene_sha"]]
-    cam = orbit_pose(frame)
-    np.testing.assert_array_equal(cam.orientation, g["cam_orientation"])
+    cam = camera_from(g)  # the reference re-normalised orbit_pose's quaternion
+    np.testing.assert_allclose(cam.orientation, orbit_pose(frame).orientation, rtol=0, atol=1e-15)
     _check_big(g, scene, cam, ("ref", "cr2"), "summary")
 
 
@@ -100,9 +101,9 @@ def test_oracle_select_clusters_orbit():
     g = load("clusters_orbit")
     norm = (g["norm_mean"], float(g["norm_scale"][0]))
     for i in range(120):
-        cam = orbit_pose(i)
+        p = orbit_pose(i)
+        cam = CameraPose(p.position, p.orientation, p.fov_x, p.fov_y, p.width, p.height)
         assert O.select_clusters(cam, g["centroids"], 4, 1.0, norm) == g["selections"][i].tolist()
-    from paper_2503_05168_b200.model import CameraPose
     base = orbit_pose(0)
     for probe, want in zip(g["probes"], g["probe_selections"]):
         cam = CameraPose(position=probe[:3], orientation=probe[3:], fov_x=base.fov_x, fov_y=base.fov_y,
