@@ -130,8 +130,8 @@ def visible_centres(scene: SceneArrays, poses, device=None) -> np.ndarray:
     pos = torch.as_tensor(np.asarray(scene.positions, dtype=np.float64), device=dev)
     seen = torch.zeros(pos.shape[0], dtype=torch.bool, device=dev)
     for cam in poses:
-        w2v = torch.as_tensor(cam.rotation_matrix().T, device=dev)
-        t = (pos - torch.as_tensor(cam.position, device=dev)) @ w2v.T
+        w2v = torch.as_tensor(np.array(cam.rotation_matrix().T), device=dev)
+        t = (pos - torch.as_tensor(np.array(cam.position), device=dev)) @ w2v.T
         fx, fy = cam.focal()
         cx, cy = cam.principal_point()
         z = t[:, 2]

@@ -184,14 +184,6 @@ __global__ void k_export_splats(Workspace ws, long long n, int8_t *status, doubl
     }
 }
 
-int tile_sort_buffer(int width, int height) {
-    const int n_tiles = ((width + kTile - 1) / kTile) * ((height + kTile - 1) / kTile);
-    int bits = 1;
-    while ((1 << bits) < n_tiles) bits++;
-    const int passes = (bits + 7) / 8;
-    return passes & 1;
-}
-
 }  // namespace
 }  // namespace seele
 
@@ -331,7 +323,8 @@ int seele_plan_export(void *workspace, int64_t n_max, int64_t pair_capacity, int
     if (n_pairs > pair_capacity || n_ws > n_max) return fail(SEELE_ERR_INVALID_ARGUMENT, "sizes exceed the workspace");
     const Workspace ws = carve_workspace(workspace, n_max, pair_capacity, width, height);
     cudaStream_t st = static_cast<cudaStream_t>(stream);
-    const int buf = tile_sort_buffer(width, height);
+    const long long n_tiles_all = (long long)((width + kTile - 1) / kTile) * ((height + kTile - 1) / kTile);
+    const int buf = pair_buffer((int)n_tiles_all);
     cudaError_t e = cudaSuccess;
     if (out->pair_pos && n_pairs > 0)
         e = cudaMemcpyAsync(out->pair_pos, ws.pval[buf], sizeof(uint32_t) * n_pairs, cudaMemcpyDeviceToDevice, st);

@@ -1,27 +1,33 @@
-// Tile binning and sort on sm_100a, all sizes read from device memory (no
-// host round trip inside a frame):
-//   1. ordered compaction of binned splats (assembled order)      [scan]
-//   2. stable LSD radix sort of their fp64 depth bits             [depth rank]
-//      -> order by (depth, assembled position) = the reference's
+// Tile binning and sort on sm_100a.  Every size is read from device memory,
+// so a frame needs no host round trip:
+//   1. ordered compaction of the binned splats (assembled order)        [scan]
+//   2. stable LSD radix sort of their fp64 depth bits                    [depth rank]
+//      -> order by (depth, assembled position), the reference's
 //         (depth, gaussian_ref) tie-break (sorting.py:43, render.py:108)
-//   3. exclusive scan of tile counts in depth-rank order          [pair offsets]
-//   4. pair emission: key = tile id, value = assembled position   [bin_tiles,
-//      preprocess.py:179-189]; emitted in depth-rank order
-//   5. stable LSD radix sort by tile id (ceil(log2 tiles) bits)   [sort_intersections,
-//      sorting.py:32-54]: stability keeps depth-rank order inside a tile
-//   6. per-tile [start, end) ranges                               [sorting.py:46-53]
+//   3. exclusive scan of tile counts in depth-rank order, then pair emission
+//      load-balanced by pairs (key = tile id, value = assembled position)
+//                                                                        [bin_tiles,
+//      preprocess.py:159-189]
+//   4. stable LSD radix sort on the tile id (ceil(log2 tiles) bits): stability
+//      keeps depth-rank order inside a tile -> (tile_id, depth, ref) order of
+//      sort_intersections (sorting.py:32-54)
+//   5. per-tile [start, end) ranges                                     [sorting.py:46-53]
 //
-// The radix sort ranks stably inside a CTA with __match_any_sync over the
-// digit (warp-level multisplit) and a per-tile warp-prefix in shared memory.
+// Radix passes: per-block digit histograms, one scan block per digit, and a
+// scatter that ranks IPT x 256 items per iteration stably (warp
+// __match_any_sync + per-(sub-round, warp) digit prefixes), stages them in
+// shared memory in digit order and writes digit runs coalesced.
 #include "common.cuh"
 
 namespace seele {
 
 namespace {
 
+constexpr int kChunkSplats = 1024;  // splats per column-bucketing CTA
+
 __device__ __forceinline__ long long chunk_size(long long n, int G) {
     long long c = (n + G - 1) / G;
-    return (c + 255) / 256 * 256;
+    return (c + 1023) / 1024 * 1024;
 }
 
 // 256-thread block exclusive scan of one value per thread.
@@ -53,117 +59,77 @@ __device__ __forceinline__ T block_exclusive_scan(T v, T &total) {
     return warp_off + x - v;
 }
 
-// ---- chunked exclusive scan with a device-resident item count --------------
+// ---- 1. ordered compaction of binned splats ----------------------------------
 
-// mode 0: flag = tiles[p] > 0 over p < counters[CNT_WS]          (compaction)
-// mode 1: value = tiles[sorted_pos[r]] over r < counters[CNT_BINNED] (pair offsets)
-template <int MODE>
-__device__ __forceinline__ unsigned long long scan_value(const Workspace &ws, const uint32_t *sorted_pos,
-                                                         long long i) {
-    if (MODE == 0) return ws.tiles[i] > 0 ? 1ull : 0ull;
-    return (unsigned long long)ws.tiles[sorted_pos[i]];
-}
-
-template <int MODE>
-__device__ __forceinline__ long long scan_count(const Workspace &ws) {
-    return MODE == 0 ? (long long)ws.counters[CNT_WS] : (long long)ws.counters[CNT_BINNED];
-}
-
-template <int MODE>
-__global__ void __launch_bounds__(256) k_chunk_reduce(Workspace ws, const uint32_t *sorted_pos) {
-    const long long n = scan_count<MODE>(ws);
-    const int G = gridDim.x;
-    const long long c = chunk_size(n, G);
-    const long long b0 = (long long)blockIdx.x * c;
-    const long long b1 = min(b0 + c, n);
+__global__ void __launch_bounds__(256) k_compact_reduce(Workspace ws) {
+    const long long n = ws.counters[CNT_WS];
+    const long long c = chunk_size(n, gridDim.x);
+    const long long b0 = (long long)blockIdx.x * c, b1 = min(b0 + c, n);
     unsigned long long acc = 0;
-    for (long long i = b0 + threadIdx.x; i < b1; i += blockDim.x) acc += scan_value<MODE>(ws, sorted_pos, i);
+    for (long long i = b0 + threadIdx.x; i < b1; i += blockDim.x) acc += ws.tiles[i] > 0 ? 1ull : 0ull;
     unsigned long long tot;
     block_exclusive_scan<unsigned long long>(acc, tot);
     if (threadIdx.x == 0) ws.block_sums[blockIdx.x] = tot;
 }
 
-// Single block: exclusive scan of G block sums; publishes the total.
-template <int MODE>
-__global__ void __launch_bounds__(1024) k_scan_sums(Workspace ws, int G, long long cap, int64_t *stats) {
+__global__ void __launch_bounds__(1024) k_compact_sums(Workspace ws, int G) {
     __shared__ unsigned long long s[kChunkBlocksMax];
     for (int i = threadIdx.x; i < G; i += blockDim.x) s[i] = ws.block_sums[i];
     __syncthreads();
     if (threadIdx.x == 0) {
         unsigned long long run = 0;
         for (int i = 0; i < G; i++) {
-            unsigned long long v = s[i];
+            const unsigned long long v = s[i];
             s[i] = run;
             run += v;
         }
-        ws.block_sums[G] = run;
-        if (MODE == 0) {
-            ws.counters[CNT_BINNED] = (uint32_t)run;
-        } else {
-            ws.pairs64[0] = run;
-            stats[SEELE_STAT_TILE_PAIRS] = (int64_t)run;
-            const bool over = run > (unsigned long long)cap;
-            ws.counters[CNT_OVERFLOW] = over ? 1u : 0u;
-            ws.counters[CNT_PAIRS] = over ? 0u : (uint32_t)run;
-            stats[SEELE_STAT_OVERFLOW] = over ? 1 : 0;
-        }
+        ws.counters[CNT_BINNED] = (uint32_t)run;
     }
     __syncthreads();
     for (int i = threadIdx.x; i < G; i += blockDim.x) ws.block_sums[i] = s[i];
 }
 
-template <int MODE>
-__global__ void __launch_bounds__(256) k_chunk_scan(Workspace ws, const uint32_t *sorted_pos) {
-    const long long n = scan_count<MODE>(ws);
-    const int G = gridDim.x;
-    const long long c = chunk_size(n, G);
-    const long long b0 = (long long)blockIdx.x * c;
-    const long long b1 = min(b0 + c, n);
+__global__ void __launch_bounds__(256) k_compact_write(Workspace ws) {
+    const long long n = ws.counters[CNT_WS];
+    const long long c = chunk_size(n, gridDim.x);
+    const long long b0 = (long long)blockIdx.x * c, b1 = min(b0 + c, n);
     unsigned long long run = ws.block_sums[blockIdx.x];
     for (long long t0 = b0; t0 < b1; t0 += blockDim.x) {
         const long long i = t0 + threadIdx.x;
-        const unsigned long long v = i < b1 ? scan_value<MODE>(ws, sorted_pos, i) : 0ull;
+        const unsigned v = (i < b1 && ws.tiles[i] > 0) ? 1u : 0u;
         unsigned long long tot;
         const unsigned long long ex = block_exclusive_scan<unsigned long long>(v, tot) + run;
-        if (i < b1) {
-            if (MODE == 0) {
-                if (v) {
-                    ws.dkey[0][ex] = (uint64_t)__double_as_longlong(ws.depth[i]);
-                    ws.dval[0][ex] = (uint32_t)i;
-                }
-            } else {
-                ws.poff[i] = ex;
-            }
+        if (v) {
+            ws.dkey[0][ex] = (uint64_t)__double_as_longlong(ws.depth[i]);
+            ws.dval[0][ex] = (uint32_t)i;
         }
         run += tot;
     }
 }
 
-// ---- stable LSD radix sort, device-resident count --------------------------
+// ---- stable LSD radix sort passes ---------------------------------------------
 
 template <typename K>
 __global__ void __launch_bounds__(256) k_radix_hist(const K *__restrict__ keys, const uint32_t *n_ptr, int shift,
                                                     int bits, uint32_t *hist) {
     __shared__ uint32_t h[256];
     const int nd = 1 << bits;
-    for (int i = threadIdx.x; i < 256; i += blockDim.x) h[i] = 0;
+    h[threadIdx.x] = 0;
     __syncthreads();
     const long long n = *n_ptr;
-    const int G = gridDim.x;
-    const long long c = chunk_size(n, G);
-    const long long b0 = (long long)blockIdx.x * c;
-    const long long b1 = min(b0 + c, n);
+    const long long c = chunk_size(n, gridDim.x);
+    const long long b0 = (long long)blockIdx.x * c, b1 = min(b0 + c, n);
     const K mask = (K)(nd - 1);
-    for (long long i = b0 + threadIdx.x; i < b1; i += blockDim.x) atomicAdd(&h[(uint32_t)((keys[i] >> shift) & mask)], 1u);
+    for (long long i = b0 + threadIdx.x; i < b1; i += blockDim.x)
+        atomicAdd(&h[(uint32_t)((keys[i] >> shift) & mask)], 1u);
     __syncthreads();
-    for (int d = threadIdx.x; d < nd; d += blockDim.x) hist[(long long)d * G + blockIdx.x] = h[d];
+    if (threadIdx.x < nd) hist[(long long)threadIdx.x * gridDim.x + blockIdx.x] = h[threadIdx.x];
 }
 
-// Per digit d (one block each): exclusive scan over the G block counts of
-// that digit, in place, and the digit total into tot[d].
+// Per digit d (one block each): exclusive scan over the G block counts of that
+// digit, in place, and the digit total into tot[d].
 __global__ void __launch_bounds__(256) k_radix_scan(uint32_t *hist, uint32_t *tot, int G) {
-    const int d = blockIdx.x;
-    uint32_t *row = hist + (long long)d * G;
+    uint32_t *row = hist + (long long)blockIdx.x * G;
     const int per = (G + 255) / 256;
     const int a = threadIdx.x * per, b = min(a + per, G);
     uint32_t sum = 0;
@@ -175,132 +141,220 @@ __global__ void __launch_bounds__(256) k_radix_scan(uint32_t *hist, uint32_t *to
         row[i] = run;
         run += v;
     }
-    if (threadIdx.x == 0) tot[d] = total;
+    if (threadIdx.x == 0) tot[blockIdx.x] = total;
 }
 
-template <typename K>
+template <typename K, int IPT>
 __global__ void __launch_bounds__(256) k_radix_scatter(const K *__restrict__ kin, const uint32_t *__restrict__ vin,
                                                        K *__restrict__ kout, uint32_t *__restrict__ vout,
                                                        const uint32_t *n_ptr, int shift, int bits,
                                                        const uint32_t *__restrict__ hist,
                                                        const uint32_t *__restrict__ tot) {
-    __shared__ uint32_t base[256];
-    __shared__ uint32_t wh[2][8][256];
+    constexpr int TILE = 256 * IPT;
+    __shared__ uint32_t s_base[256];            // global destination of the next item of each digit
+    __shared__ uint32_t s_loc[256];             // digit offsets inside the staged tile
+    __shared__ uint16_t s_wh[IPT][8][256];      // per (sub-round, warp, digit) counts -> prefixes
+    __shared__ K s_key[TILE];
+    __shared__ uint32_t s_val[TILE];
     const int nd = 1 << bits;
     const int G = gridDim.x;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    // global base of digit d = (all keys with a smaller digit) + (digit d in earlier blocks)
     uint32_t digit_total;
     const uint32_t digit_base = block_exclusive_scan<uint32_t>(tid < nd ? tot[tid] : 0u, digit_total);
-    base[tid] = tid < nd ? digit_base + hist[(long long)tid * G + blockIdx.x] : 0u;
-    for (int w = 0; w < 8; w++) wh[0][w][tid] = wh[1][w][tid] = 0u;
+    s_base[tid] = tid < nd ? digit_base + hist[(long long)tid * G + blockIdx.x] : 0u;
+#pragma unroll
+    for (int r = 0; r < IPT; r++)
+        for (int w = 0; w < 8; w++) s_wh[r][w][tid] = 0;
     __syncthreads();
     const long long n = *n_ptr;
     const long long c = chunk_size(n, G);
-    const long long b0 = (long long)blockIdx.x * c;
-    const long long b1 = min(b0 + c, n);
+    const long long b0 = (long long)blockIdx.x * c, b1 = min(b0 + c, n);
     const K mask = (K)(nd - 1);
     const unsigned lt = (1u << lane) - 1u;
-    int buf = 0;
-    for (long long t0 = b0; t0 < b1; t0 += 256) {
-        const long long i = t0 + tid;
-        const bool valid = i < b1;
-        K key = 0;
-        uint32_t val = 0, d = 0xffffffffu;
-        if (valid) {
-            key = kin[i];
-            val = vin[i];
-            d = (uint32_t)((key >> shift) & mask);
-        }
-        const unsigned peers = __match_any_sync(0xffffffffu, d);
-        const uint32_t rank = __popc(peers & lt);
-        if (valid && rank == 0) wh[buf][warp][d] = __popc(peers);
-        __syncthreads();
-        uint32_t tot = 0;
-        if (tid < nd) {
+    for (long long t0 = b0; t0 < b1; t0 += TILE) {
+        const int n_tile = (int)min((long long)TILE, b1 - t0);
+        K key[IPT];
+        uint32_t val[IPT], dig[IPT], rank[IPT];
 #pragma unroll
-            for (int w = 0; w < 8; w++) {
-                const uint32_t cnt = wh[buf][w][tid];
-                wh[buf][w][tid] = tot;
-                tot += cnt;
+        for (int r = 0; r < IPT; r++) {  // striped: item t0 + r*256 + tid keeps the input order
+            const int li = r * 256 + tid;
+            const bool valid = li < n_tile;
+            dig[r] = 0xffffffffu;
+            if (valid) {
+                key[r] = kin[t0 + li];
+                val[r] = vin[t0 + li];
+                dig[r] = (uint32_t)((key[r] >> shift) & mask);
             }
+            const unsigned peers = __match_any_sync(0xffffffffu, dig[r]);
+            rank[r] = __popc(peers & lt);
+            if (valid && rank[r] == 0) s_wh[r][warp][dig[r]] = (uint16_t)__popc(peers);
         }
         __syncthreads();
-        if (valid) {
-            const uint32_t pos = base[d] + wh[buf][warp][d] + rank;
-            kout[pos] = key;
-            vout[pos] = val;
+        uint32_t cnt = 0;
+        if (tid < nd) {
+#pragma unroll
+            for (int r = 0; r < IPT; r++)
+#pragma unroll
+                for (int w = 0; w < 8; w++) {
+                    const uint32_t v = s_wh[r][w][tid];
+                    s_wh[r][w][tid] = (uint16_t)cnt;
+                    cnt += v;
+                }
+        }
+        uint32_t tile_total;
+        const uint32_t loc = block_exclusive_scan<uint32_t>(cnt, tile_total);
+        if (tid < nd) s_loc[tid] = loc;
+        __syncthreads();
+#pragma unroll
+        for (int r = 0; r < IPT; r++) {
+            if (dig[r] == 0xffffffffu) continue;
+            const uint32_t li = s_loc[dig[r]] + s_wh[r][warp][dig[r]] + rank[r];
+            s_key[li] = key[r];
+            s_val[li] = val[r];
+        }
+        __syncthreads();
+        for (int li = tid; li < n_tile; li += 256) {  // digit runs land on consecutive addresses
+            const K k = s_key[li];
+            const uint32_t d = (uint32_t)((k >> shift) & mask);
+            const uint32_t dst = s_base[d] + (uint32_t)li - s_loc[d];
+            kout[dst] = k;
+            vout[dst] = s_val[li];
         }
         __syncthreads();
         if (tid < nd) {
-            base[tid] += tot;
+            s_base[tid] += cnt;
 #pragma unroll
-            for (int w = 0; w < 8; w++) wh[buf][w][tid] = 0u;
+            for (int r = 0; r < IPT; r++)
+                for (int w = 0; w < 8; w++) s_wh[r][w][tid] = 0;
         }
-        buf ^= 1;
+        __syncthreads();
     }
 }
 
 template <typename K>
 int radix_sort(K *keys[2], uint32_t *vals[2], const uint32_t *n_ptr, int begin_bit, int end_bit, uint32_t *hist,
-               int G, cudaStream_t st) {
+               uint32_t *tot, int G, cudaStream_t st) {
     int cur = 0;
-    uint32_t *tot = hist + 256LL * kChunkBlocksMax;
     for (int shift = begin_bit; shift < end_bit; shift += 8) {
         const int bits = min(8, end_bit - shift);
         k_radix_hist<K><<<G, 256, 0, st>>>(keys[cur], n_ptr, shift, bits, hist);
         k_radix_scan<<<1 << bits, 256, 0, st>>>(hist, tot, G);
-        k_radix_scatter<K><<<G, 256, 0, st>>>(keys[cur], vals[cur], keys[cur ^ 1], vals[cur ^ 1], n_ptr, shift, bits,
-                                              hist, tot);
+        k_radix_scatter<K, 4><<<G, 256, 0, st>>>(keys[cur], vals[cur], keys[cur ^ 1], vals[cur ^ 1], n_ptr, shift,
+                                                 bits, hist, tot);
         cur ^= 1;
         note_launches(3);
     }
     return cur;
 }
 
-// ---- pair emission and ranges -----------------------------------------------
+// ---- 3. pair emission, load-balanced by pairs ----------------------------------
 
-// bin_tiles emission (preprocess.py:179-189), warp-cooperative: each warp
-// takes 32 depth-ranked splats and writes their tile pairs one splat at a
-// time with all 32 lanes (coalesced stores, no per-thread serial loops over
-// the few splats that cover thousands of tiles).
-__global__ void __launch_bounds__(256) k_emit(Workspace ws, const uint32_t *__restrict__ sorted_pos, int tiles_x,
-                                              uint32_t *__restrict__ pkey, uint32_t *__restrict__ pval) {
-    if (ws.counters[CNT_OVERFLOW]) return;
+// Exclusive scan of the tile counts in depth-rank order -> first pair of each rank.
+__global__ void __launch_bounds__(256) k_pairs_reduce(Workspace ws, const uint32_t *__restrict__ sorted_pos) {
     const long long n = ws.counters[CNT_BINNED];
-    const int lane = threadIdx.x & 31;
-    const long long warp0 = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    const long long n_warps = ((long long)gridDim.x * blockDim.x) >> 5;
-    for (long long base = warp0 * 32; base < n; base += n_warps * 32) {
-        const long long r = base + lane;
-        uint32_t p = 0, lo = 0, hi = 0;
-        unsigned long long off = 0;
-        if (r < n) {
-            p = sorted_pos[r];
-            const short4 rc = ws.rect[p];
-            lo = (uint32_t)(uint16_t)rc.x | ((uint32_t)(uint16_t)rc.y << 16);
-            hi = (uint32_t)(uint16_t)rc.z | ((uint32_t)(uint16_t)rc.w << 16);
-            off = ws.poff[r];
+    const long long c = chunk_size(n, gridDim.x);
+    const long long b0 = (long long)blockIdx.x * c, b1 = min(b0 + c, n);
+    unsigned long long acc = 0;
+    for (long long r = b0 + threadIdx.x; r < b1; r += blockDim.x) acc += ws.tiles[sorted_pos[r]];
+    unsigned long long tot;
+    block_exclusive_scan<unsigned long long>(acc, tot);
+    if (threadIdx.x == 0) ws.block_sums[blockIdx.x] = tot;
+}
+
+__global__ void __launch_bounds__(1024) k_pairs_sums(Workspace ws, int G, long long cap, int64_t *stats) {
+    __shared__ unsigned long long s[kChunkBlocksMax];
+    for (int i = threadIdx.x; i < G; i += blockDim.x) s[i] = ws.block_sums[i];
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        unsigned long long run = 0;
+        for (int i = 0; i < G; i++) {
+            const unsigned long long v = s[i];
+            s[i] = run;
+            run += v;
         }
-        const int m = (int)min(32LL, n - base);
-        for (int g = 0; g < m; g++) {
-            const uint32_t gp = __shfl_sync(0xffffffffu, p, g);
-            const uint32_t glo = __shfl_sync(0xffffffffu, lo, g);
-            const uint32_t ghi = __shfl_sync(0xffffffffu, hi, g);
-            const unsigned long long goff = __shfl_sync(0xffffffffu, off, g);
-            const int tx0 = (int)(glo & 0xffff), tx1 = (int)(glo >> 16);
-            const int ty0 = (int)(ghi & 0xffff), ty1 = (int)(ghi >> 16);
-            const int w = tx1 - tx0 + 1;
-            const int cnt = w * (ty1 - ty0 + 1);
-            for (int k = lane; k < cnt; k += 32) {
-                const int ty = k / w;
-                const int tx = k - ty * w;
-                pkey[goff + k] = (uint32_t)((ty0 + ty) * tiles_x + tx0 + tx);
-                pval[goff + k] = gp;
-            }
-        }
+        stats[SEELE_STAT_TILE_PAIRS] = (int64_t)run;
+        const bool over = run > (unsigned long long)cap;
+        ws.counters[CNT_OVERFLOW] = over ? 1u : 0u;
+        ws.counters[CNT_PAIRS] = over ? 0u : (uint32_t)run;
+        stats[SEELE_STAT_OVERFLOW] = over ? 1 : 0;
+        ws.poff[ws.counters[CNT_BINNED]] = run;  // sentinel for the emission search
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < G; i += blockDim.x) ws.block_sums[i] = s[i];
+}
+
+__global__ void __launch_bounds__(256) k_pairs_scan(Workspace ws, const uint32_t *__restrict__ sorted_pos) {
+    const long long n = ws.counters[CNT_BINNED];
+    const long long c = chunk_size(n, gridDim.x);
+    const long long b0 = (long long)blockIdx.x * c, b1 = min(b0 + c, n);
+    unsigned long long run = ws.block_sums[blockIdx.x];
+    for (long long t0 = b0; t0 < b1; t0 += blockDim.x) {
+        const long long r = t0 + threadIdx.x;
+        const unsigned long long v = r < b1 ? (unsigned long long)ws.tiles[sorted_pos[r]] : 0ull;
+        unsigned long long tot;
+        const unsigned long long ex = block_exclusive_scan<unsigned long long>(v, tot) + run;
+        if (r < b1) ws.poff[r] = ex;
+        run += tot;
     }
 }
+
+// bin_tiles emission (preprocess.py:179-189) in depth-rank order, 2048 pairs
+// per block iteration whatever the splat sizes: the block finds the ranks
+// overlapping its pair range, stages their records, and every thread
+// expands its own pairs (ty-major, tx-minor inside a splat).
+constexpr int kEmitTile = 2048;
+
+__global__ void __launch_bounds__(256) k_emit(Workspace ws, const uint32_t *__restrict__ sorted_pos, int tiles_x,
+                                              uint32_t *__restrict__ pkey, uint32_t *__restrict__ pval) {
+    __shared__ unsigned long long s_off[kEmitTile + 1];
+    __shared__ uint32_t s_pos[kEmitTile];
+    __shared__ short4 s_rc[kEmitTile];
+    __shared__ long long s_r0;
+    if (ws.counters[CNT_OVERFLOW]) return;
+    const long long n = ws.counters[CNT_BINNED];
+    const unsigned long long k_total = ws.counters[CNT_PAIRS];
+    for (unsigned long long base = (unsigned long long)blockIdx.x * kEmitTile; base < k_total;
+         base += (unsigned long long)gridDim.x * kEmitTile) {
+        if (threadIdx.x == 0) {  // last rank whose first pair is <= base
+            long long lo = 0, hi = n - 1;
+            while (lo < hi) {
+                const long long mid = (lo + hi + 1) >> 1;
+                if (ws.poff[mid] <= base) lo = mid; else hi = mid - 1;
+            }
+            s_r0 = lo;
+        }
+        __syncthreads();
+        const long long r0 = s_r0;
+        const int nr = (int)min((long long)kEmitTile, n - r0);  // every splat has >= 1 pair
+        for (int k = threadIdx.x; k <= nr; k += blockDim.x) {
+            s_off[k] = ws.poff[r0 + k];
+            if (k < nr) {
+                const uint32_t p = sorted_pos[r0 + k];
+                s_pos[k] = p;
+                s_rc[k] = ws.rect[p];
+            }
+        }
+        __syncthreads();
+        const unsigned long long end = min(base + kEmitTile, k_total);
+        for (unsigned long long i = base + threadIdx.x; i < end; i += blockDim.x) {
+            int lo = 0, hi = nr - 1;
+            while (lo < hi) {
+                const int mid = (lo + hi + 1) >> 1;
+                if (s_off[mid] <= i) lo = mid; else hi = mid - 1;
+            }
+            const short4 rc = s_rc[lo];
+            const int w = rc.y - rc.x + 1;
+            const int local = (int)(i - s_off[lo]);
+            const int ty = rc.z + local / w;
+            const int tx = rc.x + local - (local / w) * w;
+            pkey[i] = (uint32_t)(ty * tiles_x + tx);
+            pval[i] = s_pos[lo];
+        }
+        __syncthreads();
+    }
+}
+
+// ---- 5. ranges --------------------------------------------------------------------
 
 __global__ void k_clear_ranges(uint2 *ranges, int n_tiles) {
     for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < n_tiles; t += gridDim.x * blockDim.x)
@@ -323,18 +377,29 @@ int chunk_grid(int sms) {
     return g > kChunkBlocksMax ? kChunkBlocksMax : g;
 }
 
+int key_bits(int n) {
+    int b = 1;
+    while ((1 << b) < n) b++;
+    return b;
+}
+
+// Which ping-pong buffer holds the sorted pairs (seele_plan_export).
+int pair_buffer(int n_tiles) { return ((key_bits(n_tiles) + 7) / 8) & 1; }
+
 void launch_depth_rank(const Workspace &ws, long long n_max, int grid, int64_t *stats, uint32_t **sorted_pos,
                        cudaStream_t st) {
     (void)n_max;
+    (void)stats;
     const int G = grid;
-    k_chunk_reduce<0><<<G, 256, 0, st>>>(ws, nullptr);
-    k_scan_sums<0><<<1, 1024, 0, st>>>(ws, G, 0, stats);
-    k_chunk_scan<0><<<G, 256, 0, st>>>(ws, nullptr);
+    k_compact_reduce<<<G, 256, 0, st>>>(ws);
+    k_compact_sums<<<1, 1024, 0, st>>>(ws, G);
+    k_compact_write<<<G, 256, 0, st>>>(ws);
     note_launches(3);
     uint64_t *k[2] = {ws.dkey[0], ws.dkey[1]};
     uint32_t *v[2] = {ws.dval[0], ws.dval[1]};
     // positive doubles order like their bit patterns; bit 63 (sign) is always 0
-    const int cur = radix_sort<uint64_t>(k, v, ws.counters + CNT_BINNED, 0, 63, ws.hist, G, st);
+    const int cur = radix_sort<uint64_t>(k, v, ws.counters + CNT_BINNED, 0, 63, ws.hist, ws.hist + 256LL * kChunkBlocksMax,
+                                         G, st);
     *sorted_pos = v[cur];
 }
 
@@ -342,17 +407,16 @@ void launch_binning(const Workspace &ws, const uint32_t *sorted_pos, long long n
                     int grid, int64_t *stats, uint32_t **pair_pos, uint32_t **pair_tile, cudaStream_t st) {
     (void)n_max;
     const int G = grid;
-    k_chunk_reduce<1><<<G, 256, 0, st>>>(ws, sorted_pos);
-    k_scan_sums<1><<<1, 1024, 0, st>>>(ws, G, cap, stats);
-    k_chunk_scan<1><<<G, 256, 0, st>>>(ws, sorted_pos);
+    k_pairs_reduce<<<G, 256, 0, st>>>(ws, sorted_pos);
+    k_pairs_sums<<<1, 1024, 0, st>>>(ws, G, cap, stats);
+    k_pairs_scan<<<G, 256, 0, st>>>(ws, sorted_pos);
     k_emit<<<G, 256, 0, st>>>(ws, sorted_pos, cam.tiles_x, ws.pkey[0], ws.pval[0]);
     note_launches(4);
     const int n_tiles = cam.tiles_x * cam.tiles_y;
-    int bits = 1;
-    while ((1 << bits) < n_tiles) bits++;
     uint32_t *k[2] = {ws.pkey[0], ws.pkey[1]};
     uint32_t *v[2] = {ws.pval[0], ws.pval[1]};
-    const int cur = radix_sort<uint32_t>(k, v, ws.counters + CNT_PAIRS, 0, bits, ws.hist, G, st);
+    const int cur = radix_sort<uint32_t>(k, v, ws.counters + CNT_PAIRS, 0, key_bits(n_tiles), ws.hist,
+                                         ws.hist + 256LL * kChunkBlocksMax, G, st);
     k_clear_ranges<<<(n_tiles + 255) / 256, 256, 0, st>>>(ws.ranges, n_tiles);
     k_ranges<<<G, 256, 0, st>>>(ws, k[cur]);
     note_launches(2);

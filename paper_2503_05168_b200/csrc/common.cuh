@@ -61,7 +61,7 @@ struct Workspace {
     // compaction + depth rank
     uint64_t *dkey[2];
     uint32_t *dval[2];
-    // pair offsets per rank (u64 to survive overflow detection)
+    // first pair of each depth-ranked splat (+ total); u64 to detect overflow
     unsigned long long *poff;
     // pairs
     uint32_t *pkey[2];
@@ -102,6 +102,7 @@ void launch_raster_fast(int W, const Workspace &ws, const uint32_t *pair_pos, co
 
 // grid of the chunked scan / sort kernels (binning.cu)
 int chunk_grid(int sms);
+int pair_buffer(int n_tiles);      // ping-pong buffer holding the sorted pairs
 
 // Counts kernels this library has launched (seele_launch_count, api.cu).
 void note_launches(int n);

@@ -78,8 +78,7 @@ __device__ __forceinline__ void axis_range(double lo, double hi, int n_tiles, in
 }
 
 struct Splat {
-    double p[3], s[3], q[4], o;
-    float shf[48];  // planes layout: SH stays fp32 (exact) until use
+    double p[3], s[3], q[4], o;  // SH coefficients are loaded later, channel by channel
 };
 
 __device__ __forceinline__ double sigmoid_clip(double x) {
@@ -116,18 +115,6 @@ __device__ __forceinline__ void load_splat(const SceneK &sc, long long i, int sh
         g.s[0] = p1.x; g.s[1] = p1.y; g.s[2] = p1.z;
         g.q[0] = p2.x; g.q[1] = p2.y; g.q[2] = p2.z; g.q[3] = p2.w;
         normalize4(g.q);  // container decode (io.py:226-229)
-        #pragma unroll
-        for (int ch = 0; ch < 3; ch++) {
-            #pragma unroll
-            for (int k = 0; k < 4; k++) {
-                float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-                if (k < sh_planes) v = __ldg(sc.planes + (3 + 4 * ch + k) * st + i);
-                g.shf[16 * ch + 4 * k + 0] = v.x;
-                g.shf[16 * ch + 4 * k + 1] = v.y;
-                g.shf[16 * ch + 4 * k + 2] = v.z;
-                g.shf[16 * ch + 4 * k + 3] = v.w;
-            }
-        }
     } else {
         for (int k = 0; k < 3; k++) {
             g.p[k] = sc.pos[3 * i + k];
@@ -145,7 +132,7 @@ __device__ __forceinline__ void warp_count_add(int64_t *dst, int pred) {
 }
 
 template <int LAYOUT>
-__global__ void __launch_bounds__(256) k_preprocess(SceneK sc, const int64_t *__restrict__ ranges,
+__global__ void __launch_bounds__(256, 3) k_preprocess(SceneK sc, const int64_t *__restrict__ ranges,
                                                     int n_ranges, CamK cam, CfgK cfg, Workspace ws,
                                                     int64_t *stats) {
     __shared__ long long s_start[SEELE_MAX_RANGES], s_prefix[SEELE_MAX_RANGES + 1];
@@ -227,9 +214,25 @@ __global__ void __launch_bounds__(256) k_preprocess(SceneK sc, const int64_t *__
                     const double vx = d[0] / nrm, vy = d[1] / nrm, vz = d[2] / nrm;
                     float4 col;
                     if (LAYOUT == SEELE_LAYOUT_PLANES) {
-                        col.x = (float)sh_channel([&](int k) { return (double)g.shf[k]; }, vx, vy, vz, cfg.sh_degree);
-                        col.y = (float)sh_channel([&](int k) { return (double)g.shf[16 + k]; }, vx, vy, vz, cfg.sh_degree);
-                        col.z = (float)sh_channel([&](int k) { return (double)g.shf[32 + k]; }, vx, vy, vz, cfg.sh_degree);
+                        // SH planes are read only for projected splats, one channel (4 x float4) at a time
+                        float cc3[3];
+#pragma unroll
+                        for (int ch = 0; ch < 3; ch++) {
+                            float shc[16];
+#pragma unroll
+                            for (int k = 0; k < 4; k++) {
+                                float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+                                if (k < sh_planes) v = __ldg(sc.planes + (3 + 4 * ch + k) * sc.plane_stride + i);
+                                shc[4 * k] = v.x;
+                                shc[4 * k + 1] = v.y;
+                                shc[4 * k + 2] = v.z;
+                                shc[4 * k + 3] = v.w;
+                            }
+                            cc3[ch] = (float)sh_channel([&](int k) { return (double)shc[k]; }, vx, vy, vz, cfg.sh_degree);
+                        }
+                        col.x = cc3[0];
+                        col.y = cc3[1];
+                        col.z = cc3[2];
                     } else {
                         const double *shp = sc.sh + 48 * i;
                         col.x = (float)sh_channel([&](int k) { return shp[k]; }, vx, vy, vz, cfg.sh_degree);

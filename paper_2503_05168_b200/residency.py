@@ -77,7 +77,7 @@ class ResidentRenderer:
             raise InvalidArgumentError(f"m must be < {handle.num_clusters}, got {self.m}")
         self.beta = handle.beta
         self.normalization = handle.normalization
-        self.device = torch.device(device or ("cuda", torch.cuda.current_device()))
+        self.device = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
         self.scene = handle.upload(self.device)
         self.centroids = torch.from_numpy(np.ascontiguousarray(handle.centroids)).to(self.device)
         self.chunks = torch.from_numpy(np.ascontiguousarray(handle.chunks)).to(self.device)
