@@ -134,6 +134,7 @@ Workspace carve_workspace(void *base, long long n_max, long long cap, int width,
     w.dval[0] = c.take<uint32_t>(n);
     w.dval[1] = c.take<uint32_t>(n);
     w.poff = c.take<unsigned long long>(n + 1);
+    w.tile_r0 = c.take<uint32_t>(cap / 2048 + 2);
     w.pkey[0] = c.take<uint32_t>(cap);
     w.pkey[1] = c.take<uint32_t>(cap);
     w.pval[0] = c.take<uint32_t>(cap);

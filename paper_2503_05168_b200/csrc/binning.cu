@@ -23,8 +23,6 @@ namespace seele {
 
 namespace {
 
-constexpr int kChunkSplats = 1024;  // splats per column-bucketing CTA
-
 __device__ __forceinline__ long long chunk_size(long long n, int G) {
     long long c = (n + G - 1) / G;
     return (c + 1023) / 1024 * 1024;
@@ -298,34 +296,36 @@ __global__ void __launch_bounds__(256) k_pairs_scan(Workspace ws, const uint32_t
     }
 }
 
-// bin_tiles emission (preprocess.py:179-189) in depth-rank order, 2048 pairs
-// per block iteration whatever the splat sizes: the block finds the ranks
-// overlapping its pair range, stages their records, and every thread
-// expands its own pairs (ty-major, tx-minor inside a splat).
+// bin_tiles emission (preprocess.py:179-189) in depth-rank order, balanced by
+// pairs: pair tile t = [t * kEmitTile, (t + 1) * kEmitTile) starts inside rank
+// tile_r0[t] (found per rank by k_emit_starts, no search).  A block stages
+// the ranks overlapping its tile, and each thread expands 8 consecutive pairs
+// (ty-major, tx-minor inside a splat) with one search and a walk.
 constexpr int kEmitTile = 2048;
+constexpr int kEmitPerThread = kEmitTile / 256;
+
+__global__ void __launch_bounds__(256) k_emit_starts(Workspace ws) {
+    const long long n = ws.counters[CNT_BINNED];
+    for (long long r = (long long)blockIdx.x * blockDim.x + threadIdx.x; r < n; r += (long long)gridDim.x * blockDim.x) {
+        const unsigned long long a = ws.poff[r], b = ws.poff[r + 1];
+        for (unsigned long long t = (a + kEmitTile - 1) / kEmitTile; t * kEmitTile < b; t++) ws.tile_r0[t] = (uint32_t)r;
+    }
+}
 
 __global__ void __launch_bounds__(256) k_emit(Workspace ws, const uint32_t *__restrict__ sorted_pos, int tiles_x,
                                               uint32_t *__restrict__ pkey, uint32_t *__restrict__ pval) {
-    __shared__ unsigned long long s_off[kEmitTile + 1];
-    __shared__ uint32_t s_pos[kEmitTile];
-    __shared__ short4 s_rc[kEmitTile];
-    __shared__ long long s_r0;
+    __shared__ unsigned long long s_off[kEmitTile + 2];
+    __shared__ uint32_t s_pos[kEmitTile + 1];
+    __shared__ short4 s_rc[kEmitTile + 1];
     if (ws.counters[CNT_OVERFLOW]) return;
     const long long n = ws.counters[CNT_BINNED];
     const unsigned long long k_total = ws.counters[CNT_PAIRS];
-    for (unsigned long long base = (unsigned long long)blockIdx.x * kEmitTile; base < k_total;
-         base += (unsigned long long)gridDim.x * kEmitTile) {
-        if (threadIdx.x == 0) {  // last rank whose first pair is <= base
-            long long lo = 0, hi = n - 1;
-            while (lo < hi) {
-                const long long mid = (lo + hi + 1) >> 1;
-                if (ws.poff[mid] <= base) lo = mid; else hi = mid - 1;
-            }
-            s_r0 = lo;
-        }
-        __syncthreads();
-        const long long r0 = s_r0;
-        const int nr = (int)min((long long)kEmitTile, n - r0);  // every splat has >= 1 pair
+    const unsigned long long n_tiles = (k_total + kEmitTile - 1) / kEmitTile;
+    for (unsigned long long t = blockIdx.x; t < n_tiles; t += gridDim.x) {
+        const unsigned long long base = t * kEmitTile, end = min(base + kEmitTile, k_total);
+        const long long r0 = ws.tile_r0[t];
+        const long long r1 = t + 1 < n_tiles ? (long long)ws.tile_r0[t + 1] : n - 1;  // last rank overlapping
+        const int nr = (int)(r1 - r0 + 1);
         for (int k = threadIdx.x; k <= nr; k += blockDim.x) {
             s_off[k] = ws.poff[r0 + k];
             if (k < nr) {
@@ -335,20 +335,38 @@ __global__ void __launch_bounds__(256) k_emit(Workspace ws, const uint32_t *__re
             }
         }
         __syncthreads();
-        const unsigned long long end = min(base + kEmitTile, k_total);
-        for (unsigned long long i = base + threadIdx.x; i < end; i += blockDim.x) {
-            int lo = 0, hi = nr - 1;
+        const unsigned long long i0 = base + (unsigned long long)threadIdx.x * kEmitPerThread;
+        if (i0 < end) {
+            int lo = 0, hi = nr - 1;  // rank holding pair i0
             while (lo < hi) {
                 const int mid = (lo + hi + 1) >> 1;
-                if (s_off[mid] <= i) lo = mid; else hi = mid - 1;
+                if (s_off[mid] <= i0) lo = mid; else hi = mid - 1;
             }
-            const short4 rc = s_rc[lo];
-            const int w = rc.y - rc.x + 1;
-            const int local = (int)(i - s_off[lo]);
-            const int ty = rc.z + local / w;
-            const int tx = rc.x + local - (local / w) * w;
-            pkey[i] = (uint32_t)(ty * tiles_x + tx);
-            pval[i] = s_pos[lo];
+            short4 rc = s_rc[lo];
+            int w = rc.y - rc.x + 1;
+            const int local = (int)(i0 - s_off[lo]);
+            int ty = rc.z + local / w;
+            int tx = rc.x + local % w;
+            unsigned long long next = s_off[lo + 1];
+            uint32_t p = s_pos[lo];
+            const unsigned long long stop = min(i0 + kEmitPerThread, end);
+            for (unsigned long long i = i0; i < stop; i++) {
+                if (i == next) {  // next splat
+                    lo++;
+                    rc = s_rc[lo];
+                    w = rc.y - rc.x + 1;
+                    ty = rc.z;
+                    tx = rc.x;
+                    next = s_off[lo + 1];
+                    p = s_pos[lo];
+                }
+                pkey[i] = (uint32_t)(ty * tiles_x + tx);
+                pval[i] = p;
+                if (++tx > rc.y) {
+                    tx = rc.x;
+                    ty++;
+                }
+            }
         }
         __syncthreads();
     }
@@ -388,7 +406,6 @@ int pair_buffer(int n_tiles) { return ((key_bits(n_tiles) + 7) / 8) & 1; }
 
 void launch_depth_rank(const Workspace &ws, long long n_max, int grid, int64_t *stats, uint32_t **sorted_pos,
                        cudaStream_t st) {
-    (void)n_max;
     (void)stats;
     const int G = grid;
     k_compact_reduce<<<G, 256, 0, st>>>(ws);
@@ -398,8 +415,10 @@ void launch_depth_rank(const Workspace &ws, long long n_max, int grid, int64_t *
     uint64_t *k[2] = {ws.dkey[0], ws.dkey[1]};
     uint32_t *v[2] = {ws.dval[0], ws.dval[1]};
     // positive doubles order like their bit patterns; bit 63 (sign) is always 0
+    (void)n_max;
+    const int Gd = G;
     const int cur = radix_sort<uint64_t>(k, v, ws.counters + CNT_BINNED, 0, 63, ws.hist, ws.hist + 256LL * kChunkBlocksMax,
-                                         G, st);
+                                         Gd, st);
     *sorted_pos = v[cur];
 }
 
@@ -410,8 +429,9 @@ void launch_binning(const Workspace &ws, const uint32_t *sorted_pos, long long n
     k_pairs_reduce<<<G, 256, 0, st>>>(ws, sorted_pos);
     k_pairs_sums<<<1, 1024, 0, st>>>(ws, G, cap, stats);
     k_pairs_scan<<<G, 256, 0, st>>>(ws, sorted_pos);
+    k_emit_starts<<<G, 256, 0, st>>>(ws);
     k_emit<<<G, 256, 0, st>>>(ws, sorted_pos, cam.tiles_x, ws.pkey[0], ws.pval[0]);
-    note_launches(4);
+    note_launches(5);
     const int n_tiles = cam.tiles_x * cam.tiles_y;
     uint32_t *k[2] = {ws.pkey[0], ws.pkey[1]};
     uint32_t *v[2] = {ws.pval[0], ws.pval[1]};

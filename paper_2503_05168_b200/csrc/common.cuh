@@ -63,6 +63,7 @@ struct Workspace {
     uint32_t *dval[2];
     // first pair of each depth-ranked splat (+ total); u64 to detect overflow
     unsigned long long *poff;
+    uint32_t *tile_r0;   // first rank of each 2048-pair emission tile
     // pairs
     uint32_t *pkey[2];
     uint32_t *pval[2];

@@ -274,7 +274,7 @@ __global__ void __launch_bounds__(256, 3) k_preprocess(SceneK sc, const int64_t 
                         q_lo = __double2float_rd(qth * (1.0 - slack) - 1e-30);
                         q_hi = slack < 0.5 ? __double2float_ru(qth * (1.0 + slack) + 1e-30) : INFINITY;
                     }
-                    ws.fast[p] = make_float4(q_lo, q_hi, (float)g.o, 0.f);
+                    ws.fast[p] = make_float4(q_lo, q_hi, (float)g.o, (float)(1.0 - g.o));
                 }
             }
             ws.status[p] = (uint8_t)status;

@@ -25,9 +25,12 @@
 //    q_lo blends, q32 > q_hi skips, in between the pixel is re-decided with the
 //    reference's own fp64 formula (alpha64).
 //  * transmittance: alpha32 = min(o32 ex2.approx(-q32 log2(e)/2), 0.99) has
-//    |alpha32 - alpha| <= alpha (3.8e-7 + 6e-8 q).  Each pixel carries an
-//    absolute bound D >= |T32 - T|:  D' = D (1 - alpha32) + T alpha rel +
-//    1.2e-7 T' (fp32 roundings of 1 - alpha and of the product).  T < gamma
+//    |alpha32 - alpha| <= alpha (3.8e-7 + 6e-8 q); for alpha > 0.5 the factor
+//    1 - alpha is rebuilt as (1 - o) + o (1 - e^{-q/2}) (polynomial, ~5e-7
+//    relative) instead of losing a factor alpha / (1 - alpha).  Each pixel
+//    carries T as the fp64 product of its factors (no rounding drift) and an
+//    absolute bound D >= |T64 - T|:  D' = D (1 - alpha) + T ef, ef = the bound
+//    on |(1 - alpha32) - (1 - alpha)|.  T < gamma
 //    is decided in fp32 unless T32 lies within D of gamma; then the model-warp
 //    is abandoned and k_fixup (raster.cu) replays it with EXACT arithmetic.
 #include "raster_common.cuh"
@@ -46,39 +49,72 @@ struct __align__(16) Staged {
     double a, b2, c;  // conic (a, 2b, c)
     float q_lo, q_hi, o;
     uint32_t p;       // assembled position (for the fp64 re-decision)
-    float r, g, b, pad;
+    float r, g, b, om_o;  // colour; 1 - opacity (rounded once from fp64)
 };
 
 __device__ __forceinline__ uint32_t slice_any(unsigned ballot, int shift) { return ((ballot >> shift) & 0xffu) != 0u; }
 
 // Quad state: four pixels, slot s = (x0 + (s & 1), y0 + (s >> 1)).
 struct Quad {
+    double T64[4];  // transmittance, exact product of the fp32-accurate factors
     float T[4], D[4], C[4][3];
     int cnt[4];
 };
 
 // fp32 alphas of the quad pixels selected by `need` from their fp64 q; sets
-// bit s of the returned mask when alpha_s >= theta.  Pixels inside the
-// bracket are re-decided with the reference formula (rare, divergent).
+// bit s of the returned mask when alpha_s >= theta.  Also returns, per pixel,
+// the transmittance factor om = 1 - alpha and ef, the bound on the relative
+// error of om times om (so a blend adds T * ef to the absolute bound on T).
+// Pixels inside the bracket are re-decided with the reference formula (rare).
 __device__ __forceinline__ uint32_t quad_alphas(const Staged &sg, double lx0, double ly0, int x0, int y0,
                                                 uint32_t need, const Workspace &ws, double th64, float al[4],
-                                                float rel[4], uint32_t &n_redecide) {
+                                                double om[4], float ef[4], uint32_t &n_redecide) {
     const double dx0 = lx0 - sg.mx, dx1 = (lx0 + 1.0) - sg.mx;
     const double dy0 = ly0 - sg.my, dy1 = (ly0 + 1.0) - sg.my;
     const double ax0 = sg.a * dx0, ax1 = sg.a * dx1, bx0 = sg.b2 * dx0, bx1 = sg.b2 * dx1;
     const double cy0 = (sg.c * dy0) * dy0, cy1 = (sg.c * dy1) * dy1;
     const double q[4] = {fma(ax0, dx0, fma(bx0, dy0, cy0)), fma(ax1, dx1, fma(bx1, dy0, cy0)),
                          fma(ax0, dx0, fma(bx0, dy1, cy1)), fma(ax1, dx1, fma(bx1, dy1, cy1))};
-    uint32_t pass = 0, amb = 0;
+    uint32_t pass = 0, amb = 0, hi = 0;
+    float q32[4];
 #pragma unroll
     for (int s = 0; s < 4; s++) {
-        const float q32 = (float)q[s];
-        const float e = sg.o * ex2_approx(kNegHalfLog2e * q32);
+        q32[s] = (float)q[s];
+        const float e = sg.o * ex2_approx(kNegHalfLog2e * q32[s]);
         al[s] = fminf(e, (float)kAlphaClamp);
-        // clamped: alpha32 = fp32(0.99) differs from the fp64 clamp by 9.5e-9
-        rel[s] = e >= 0.99000105f ? 1.0e-8f : fmaf(6.0e-8f, q32, 3.8e-7f);
-        pass |= (q32 < sg.q_lo ? 1u : 0u) << s;
-        amb |= (q32 >= sg.q_lo && q32 <= sg.q_hi ? 1u : 0u) << s;
+        om[s] = 1.0 - (double)al[s];  // exact
+        // |alpha32 - alpha| <= alpha (3.8e-7 + 6e-8 q): ex2.approx, exponent and opacity roundings
+        ef[s] = al[s] * fmaf(6.0e-8f, q32[s], 3.8e-7f);
+        hi |= (e > 0.5f ? 1u : 0u) << s;
+        pass |= (q32[s] < sg.q_lo ? 1u : 0u) << s;
+        amb |= (q32[s] >= sg.q_lo && q32[s] <= sg.q_hi ? 1u : 0u) << s;
+    }
+    hi &= need;
+    if (__any_sync(0xffffffffu, hi != 0u)) {
+        // high alpha: 1 - alpha = (1 - o) + o (1 - e^{-q/2}) keeps ~5e-7 relative accuracy
+        // (1 - alpha32 would lose it by a factor alpha / (1 - alpha)); clamped alpha is exactly 0.99
+#pragma unroll
+        for (int s = 0; s < 4; s++) {
+            if (!((hi >> s) & 1u)) continue;
+            if (al[s] >= (float)kAlphaClamp && sg.o * ex2_approx(kNegHalfLog2e * q32[s]) >= 0.99000105f) {
+                om[s] = 1.0 - (double)kAlphaClamp;
+                ef[s] = 0.0f;
+            } else if (al[s] < (float)kAlphaClamp) {
+                const float x = 0.5f * q32[s];
+                float em = fmaf(-x, 1.0f / 362880.0f, 1.0f / 40320.0f);
+                em = fmaf(-x, em, 1.0f / 5040.0f);
+                em = fmaf(-x, em, 1.0f / 720.0f);
+                em = fmaf(-x, em, 1.0f / 120.0f);
+                em = fmaf(-x, em, 1.0f / 24.0f);
+                em = fmaf(-x, em, 1.0f / 6.0f);
+                em = fmaf(-x, em, 0.5f);
+                em = fmaf(-x, em, 1.0f);
+                em *= x;  // 1 - e^{-x}, x < ln 2
+                const float omf = fmaf(sg.o, em, sg.om_o);
+                om[s] = (double)omf;
+                ef[s] = 6.2e-7f * omf;
+            }
+        }
     }
     amb &= need;
     if (amb) {  // inside the bracket: decide with the reference formula in fp64
@@ -90,7 +126,8 @@ __device__ __forceinline__ uint32_t quad_alphas(const Staged &sg, double lx0, do
             const double a64 = alpha64((double)(x0 + (s & 1)) + 0.5, (double)(y0 + (s >> 1)) + 0.5, m.x, m.y, co.x,
                                        co.y, co.z, co.w);
             al[s] = (float)a64;
-            rel[s] = 6.0e-8f;
+            om[s] = 1.0 - a64;
+            ef[s] = 0.0f;
             pass |= (a64 >= th64 ? 1u : 0u) << s;
             n_redecide++;
         }
@@ -132,6 +169,7 @@ __global__ void __launch_bounds__(64, 8) k_raster_quad(Workspace ws, const uint3
     Quad st;
 #pragma unroll
     for (int s = 0; s < 4; s++) {
+        st.T64[s] = 1.0;
         st.T[s] = 1.0f;
         st.D[s] = 0.0f;
         st.C[s][0] = st.C[s][1] = st.C[s][2] = 0.0f;
@@ -164,7 +202,7 @@ __global__ void __launch_bounds__(64, 8) k_raster_quad(Workspace ws, const uint3
             sv.r = col.x;
             sv.g = col.y;
             sv.b = col.z;
-            sv.pad = 0.0f;
+            sv.om_o = f.w;
             s_g[tid] = sv;
         }
         __syncthreads();
@@ -175,10 +213,11 @@ __global__ void __launch_bounds__(64, 8) k_raster_quad(Workspace ws, const uint3
             const Staged &sg = s_g[j];
             const uint32_t mw_live = slice_any(lb, shift);
             n_live += __popc(live);
-            float al[4], rel[4];
+            float al[4], ef[4];
+            double om[4];
             uint32_t blend;
             if (W == 0 || W == 1) {
-                blend = quad_alphas(sg, lx0, ly0, x0, y0, live, ws, th64, al, rel, n_redecide);
+                blend = quad_alphas(sg, lx0, ly0, x0, y0, live, ws, th64, al, om, ef, n_redecide);
                 if (W == 0) {
                     c_alpha += mw_live;
                 } else {  // w = 1: every pixel is its own group and leader
@@ -190,7 +229,7 @@ __global__ void __launch_bounds__(64, 8) k_raster_quad(Workspace ws, const uint3
                 // leader phase: the leader pixel's alpha counts even if that pixel is done (rasterize.py:281)
                 const bool glive = W == 2 ? live != 0u : (lb & gmask) != 0u;
                 const uint32_t lneed = (leader_thread && glive) ? 1u : 0u;
-                const uint32_t lpass = quad_alphas(sg, lx0, ly0, x0, y0, lneed, ws, th64, al, rel, n_redecide);
+                const uint32_t lpass = quad_alphas(sg, lx0, ly0, x0, y0, lneed, ws, th64, al, om, ef, n_redecide);
                 const unsigned pb = __ballot_sync(0xffffffffu, lpass != 0u);
                 c_leader += mw_live;
                 c_alpha += slice_any(pb, shift);
@@ -198,7 +237,7 @@ __global__ void __launch_bounds__(64, 8) k_raster_quad(Workspace ws, const uint3
                 if (pb != 0u) {  // member phase (rasterize.py:283-289), skipped when no leader of the warp passed
                     const bool my_pass = (pb >> (W == 2 ? lane : leader_lane)) & 1u;
                     const uint32_t mneed = my_pass ? live : 0u;
-                    blend = quad_alphas(sg, lx0, ly0, x0, y0, mneed, ws, th64, al, rel, n_redecide);
+                    blend = quad_alphas(sg, lx0, ly0, x0, y0, mneed, ws, th64, al, om, ef, n_redecide);
                 }
             }
             const unsigned bb = __ballot_sync(0xffffffffu, blend != 0u);
@@ -215,9 +254,10 @@ __global__ void __launch_bounds__(64, 8) k_raster_quad(Workspace ws, const uint3
                 st.C[s][0] = fmaf(wgt, sg.r, st.C[s][0]);
                 st.C[s][1] = fmaf(wgt, sg.g, st.C[s][1]);
                 st.C[s][2] = fmaf(wgt, sg.b, st.C[s][2]);
-                const float t1 = t0 * (1.0f - a);
+                st.T64[s] *= on ? om[s] : 1.0;
+                const float t1 = (float)st.T64[s];
                 st.T[s] = t1;
-                const float d1 = fmaf(st.D[s], 1.0f - a, fmaf(wgt, rel[s], 1.2e-7f * t1));
+                const float d1 = fmaf(st.D[s], (float)(on ? om[s] : 1.0), t0 * ef[s]);
                 st.D[s] = on ? d1 : st.D[s];
                 st.cnt[s] += on ? 1 : 0;
                 const bool done = on && (t1 + d1 < gm_lo);
