@@ -144,7 +144,6 @@ Workspace carve_workspace(void *base, long long n_max, long long cap, int width,
     w.hist = c.take<uint32_t>(256LL * kChunkBlocksMax + 256);  // + per-digit totals
     w.counters = c.take<uint32_t>(CNT_COUNT);
     w.pairs64 = c.take<unsigned long long>(1);
-    w.fix_list = c.take<uint32_t>(tiles * 8);
     w.bytes = c.off;
     return w;
 }

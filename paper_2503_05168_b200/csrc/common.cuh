@@ -41,9 +41,8 @@ struct SceneK {
 enum {
     CNT_WS = 0,      // assembled splats
     CNT_BINNED = 1,  // splats with >= 1 tile
-    CNT_PAIRS = 2,   // tile pairs (u64 split over two u32? no: see pairs64)
+    CNT_PAIRS = 2,   // tile pairs (0 on overflow; the u64 count is in stats)
     CNT_OVERFLOW = 3,
-    CNT_FIX = 4,     // FAST raster: abandoned model-warps queued for k_fixup
     CNT_COUNT = 8
 };
 
@@ -73,7 +72,6 @@ struct Workspace {
     uint32_t *hist;                  // 256 * kChunkBlocksMax
     uint32_t *counters;              // CNT_COUNT
     unsigned long long *pairs64;     // total tile pairs (u64)
-    uint32_t *fix_list;              // fast path: flagged (tile, warp) entries
     size_t bytes;
 };
 

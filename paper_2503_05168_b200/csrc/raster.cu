@@ -2,8 +2,8 @@
 // contribution-aware engine (rasterize.py:249-322), with the reference's
 // 32-lane lockstep cost counters (rasterize.py:208-223, 291-313).
 //
-// Mapping: one CTA per 16x16 tile, one thread per pixel, and every hardware
-// warp IS one of the reference's model-warps:
+// EXACT mapping: one CTA per 16x16 tile, one thread per pixel, and every
+// hardware warp IS one of the reference's model-warps:
 //   ref / cr w=1 / cr w=2 : warp k = tile pixel rows 2k, 2k+1
 //   cr w=4                : warp k = 8x4 block (groups 2k, 2k+1 group-row-major)
 // so the counters are __any_sync votes of the real warp, the CR leader test is
@@ -15,11 +15,9 @@
 // decisions, counters):
 //  * EXACT: alpha and transmittance in fp64 in the reference's operation
 //    order (libdevice exp).
-//  * FAST (default): q in fp64 (8 DFMA-class ops, no cancellation trouble for
-//    elongated splats), alpha = o * ex2.approx(q) and T in fp32, each with a
-//    certified error bound.  An alpha test inside its band is re-decided in
-//    fp64 by that lane; a T < gamma test inside its band abandons the whole
-//    model-warp, which k_fixup then replays exactly (EXACT arithmetic).
+//  * FAST (default, raster_fast.cu): 2x2 pixels per thread, fp64 q, fp32
+//    alpha with certified error bounds; undecidable tests are re-decided
+//    exactly in fp64 in place.
 #include "raster_common.cuh"
 
 namespace seele {
@@ -76,47 +74,6 @@ __global__ void __launch_bounds__(256) k_raster_exact(Workspace ws, const uint32
     if (lane == 0) add_counters<W>(stats, k);
 }
 
-// Replay of abandoned model-warps (FAST engine) with EXACT arithmetic; one
-// warp per entry, splats read straight from the workspace records.
-template <int W>
-__global__ void __launch_bounds__(128) k_fixup(Workspace ws, const uint32_t *__restrict__ pair_pos, CamK cam, CfgK cfg,
-                                               float *image, int32_t *contrib, int64_t *stats) {
-    const uint32_t n_fix = ws.counters[CNT_FIX];
-    const int lane = threadIdx.x & 31;
-    const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    const uint32_t n_w = (gridDim.x * blockDim.x) >> 5;
-    int leader;
-    unsigned gmask;
-    group_of<W>(lane, leader, gmask);
-    const bool is_leader = lane == leader;
-    for (uint32_t e = gw; e < n_fix; e += n_w) {
-        const uint32_t code = ws.fix_list[e];
-        const int tile = (int)(code >> 3), warp = (int)(code & 7);
-        int lx, ly;
-        pixel_of<W>(warp, lane, lx, ly);
-        const int x = (tile % cam.tiles_x) * kTile + lx, y = (tile / cam.tiles_x) * kTile + ly;
-        const bool valid = x < cam.width && y < cam.height;
-        const double px = x + 0.5, py = y + 0.5;
-        Px64 s{1.0, 0.0, 0.0, 0.0, 0, !valid};
-        Counters k{0, 0, 0};
-        const uint2 rg = ws.ranges[tile];
-        for (uint32_t j = rg.x; j < rg.y; j++) {
-            const uint32_t p = __ldg(pair_pos + j);
-            const double2 m = ws.mean[p];
-            const double4 co = ws.conic_op[p];
-            const float4 col = ws.color[p];
-            if (!step64<W>(s, px, py, is_leader, leader, gmask, m.x, m.y, co.x, co.y, co.z, co.w, col.x, col.y, col.z,
-                           cfg.alpha_theta, cfg.gamma, k))
-                break;
-        }
-        if (valid) write_pixel(image, contrib, cam.width, x, y, s.C0, s.C1, s.C2, s.T, s.cnt, cfg);
-        if (lane == 0) {
-            add_counters<W>(stats, k);
-            atomicAdd((unsigned long long *)(stats + SEELE_STAT_FIXUP_WARPS), 1ull);
-        }
-    }
-}
-
 template <int W>
 void launch_engine(const Workspace &ws, const uint32_t *pair_pos, const CamK &cam, const CfgK &cfg, float *image,
                    int32_t *contrib, int64_t *stats, cudaStream_t st) {
@@ -126,8 +83,7 @@ void launch_engine(const Workspace &ws, const uint32_t *pair_pos, const CamK &ca
         note_launches(1);
     } else {
         launch_raster_fast(W, ws, pair_pos, cam, cfg, image, contrib, stats, st);
-        k_fixup<W><<<592, 128, 0, st>>>(ws, pair_pos, cam, cfg, image, contrib, stats);
-        note_launches(2);
+        note_launches(1);
     }
 }
 

@@ -9,8 +9,7 @@
 // threads, i.e. one byte of a warp ballot:
 //   ref / cr w=1 / cr w=2 : model-warp k = quad row k (pixel rows 2k, 2k+1)
 //   cr w=4                : model-warp k = 4x2 quads (groups 2k, 2k+1)
-// so the lockstep counters are per-byte "any" tests of the real ballots, and an
-// abandoned model-warp is 8 threads that stop together.
+// so the lockstep counters are per-byte "any" tests of the real ballots.
 //
 // Contribution-aware engine (rasterize.py:249-322): for w = 2 the group IS the
 // thread's quad, so the leader test is one alpha per thread and the member
@@ -31,8 +30,9 @@
 //    carries T as the fp64 product of its factors (no rounding drift) and an
 //    absolute bound D >= |T64 - T|:  D' = D (1 - alpha) + T ef, ef = the bound
 //    on |(1 - alpha32) - (1 - alpha)|.  T < gamma
-//    is decided in fp32 unless T32 lies within D of gamma; then the model-warp
-//    is abandoned and k_fixup (raster.cu) replays it with EXACT arithmetic.
+//    is decided in fp32 unless T lies within D of gamma; then that pixel's
+//    transmittance is recomputed exactly in fp64 over the tile list so far
+//    (exact_transmittance) and the decision is the reference's.
 #include "raster_common.cuh"
 
 namespace seele {
@@ -135,6 +135,56 @@ __device__ __forceinline__ uint32_t quad_alphas(const Staged &sg, double lx0, do
     return pass & need;
 }
 
+// Exact fp64 transmittance of pixel (px, py) after the tile's splats k0..k1
+// (reference semantics, rasterize.py:146-177), for a pixel live throughout:
+// it blends splat k iff alpha_k >= theta and, for CR, its group leader's
+// alpha_k >= theta (a live pixel keeps its group live).
+// alpha >= theta decided like the fast path (fp64 q against the certified
+// bracket, reference formula inside it); returns alpha64 when it passes.
+__device__ __forceinline__ bool exact_test(double px, double py, const double2 &m, const double4 &co, float q_lo,
+                                           float q_hi, double th, double &a) {
+    const double dx = px - m.x, dy = py - m.y;
+    const double q = fma(co.x * dx, dx, fma(2.0 * co.y * dx, dy, (co.z * dy) * dy));
+    const float q32 = (float)q;
+    if (q32 > q_hi) return false;
+    if (q32 < q_lo) {
+        a = fmin(co.w * exp(-0.5 * q), kAlphaClamp);
+        return true;
+    }
+    a = alpha64(px, py, m.x, m.y, co.x, co.y, co.z, co.w);
+    return a >= th;
+}
+
+template <int W>
+__device__ __forceinline__ double exact_transmittance(const Workspace &ws, const uint32_t *__restrict__ pair_pos,
+                                                   uint32_t k0, uint32_t k1, int px, int py, int lx, int ly,
+                                                   double th) {
+    constexpr int U = 2;  // independent record loads in flight
+    double T = 1.0;
+    for (uint32_t k = k0; k <= k1; k += U) {
+        double2 m[U];
+        double4 co[U];
+        float4 f[U];
+#pragma unroll
+        for (int u = 0; u < U; u++) {
+            if (k + u > k1) break;
+            const uint32_t p = pair_pos[k + u];
+            m[u] = ws.mean[p];
+            co[u] = ws.conic_op[p];
+            f[u] = ws.fast[p];
+        }
+#pragma unroll
+        for (int u = 0; u < U; u++) {
+            if (k + u > k1) break;
+            double a;
+            if (W >= 2 && !exact_test(lx + 0.5, ly + 0.5, m[u], co[u], f[u].x, f[u].y, th, a)) continue;
+            if (!exact_test(px + 0.5, py + 0.5, m[u], co[u], f[u].x, f[u].y, th, a)) continue;
+            T = __dmul_rn(T, __dsub_rn(1.0, a));
+        }
+    }
+    return T;
+}
+
 template <int W>
 __global__ void __launch_bounds__(64, 8) k_raster_quad(Workspace ws, const uint32_t *__restrict__ pair_pos, CamK cam,
                                                        CfgK cfg, float *image, int32_t *contrib, int64_t *stats) {
@@ -175,7 +225,8 @@ __global__ void __launch_bounds__(64, 8) k_raster_quad(Workspace ws, const uint3
         st.C[s][0] = st.C[s][1] = st.C[s][2] = 0.0f;
         st.cnt[s] = 0;
     }
-    bool abandoned = false;
+    // CR group leader pixel (rasterize.py:235-246): top-left pixel of the w x w group
+    const int lead_x = W == 4 ? ox + 4 * (bx >> 1) : x0, lead_y = W == 4 ? oy + 4 * (by >> 1) : y0;
     uint32_t c_alpha = 0, c_blend = 0, c_leader = 0, n_redecide = 0, n_tamb = 0;
     uint32_t n_live = 0, n_blend = 0;  // pixel-level work (roofline model in bench.py)
     const uint2 rg = ws.ranges[tile];
@@ -265,12 +316,22 @@ __global__ void __launch_bounds__(64, 8) k_raster_quad(Workspace ws, const uint3
                 live &= ~((done ? 1u : 0u) << s);
                 amb |= (unsure ? 1u : 0u) << s;
             }
-            if (__any_sync(0xffffffffu, amb != 0u)) {
-                const unsigned ab = __ballot_sync(0xffffffffu, amb != 0u);
+            if (amb != 0u) {
+                // T < gamma undecidable in fp32: recompute this pixel's transmittance exactly (fp64,
+                // reference formula) over every splat up to this one, then decide.  A live pixel's
+                // blends depend only on its own alphas (and its group leader's for CR), so this is
+                // self-contained; rare, and the other warps of the SM keep running meanwhile.
                 n_tamb += __popc(amb);
-                if (slice_any(ab, shift)) {
-                    abandoned = true;  // the whole model-warp (8 threads) stops; k_fixup replays it
-                    live = 0u;
+                const uint32_t k_end = b0 + (uint32_t)j;
+#pragma unroll
+                for (int s = 0; s < 4; s++) {
+                    if (!((amb >> s) & 1u)) continue;
+                    const double T = exact_transmittance<W>(ws, pair_pos, rg.x, k_end, x0 + (s & 1), y0 + (s >> 1),
+                                                            lead_x, lead_y, th64);
+                    st.T64[s] = T;
+                    st.T[s] = (float)T;
+                    st.D[s] = 0.0f;
+                    if (T < cfg.gamma) live &= ~(1u << s);
                 }
             }
         }
@@ -285,13 +346,6 @@ __global__ void __launch_bounds__(64, 8) k_raster_quad(Workspace ws, const uint3
         if (w_tamb) atomicAdd(st + SEELE_STAT_T_AMBIGUOUS, (unsigned long long)w_tamb);
         if (w_live) atomicAdd(st + SEELE_STAT_LIVE_PIXEL_STEPS, (unsigned long long)w_live);
         if (w_blend) atomicAdd(st + SEELE_STAT_PIXEL_BLENDS, (unsigned long long)w_blend);
-    }
-    if (abandoned) {
-        if (i == 0) {
-            const uint32_t slot = atomicAdd(ws.counters + CNT_FIX, 1u);
-            ws.fix_list[slot] = ((uint32_t)tile << 3) | (uint32_t)mw;
-        }
-        return;
     }
 #pragma unroll
     for (int s = 0; s < 4; s++) {
