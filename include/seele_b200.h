@@ -125,7 +125,10 @@ enum {
 };
 
 /* Bytes of workspace needed for up to n_max assembled splats, pair_capacity
- * tile pairs and a width x height image. */
+ * tile pairs and a width x height image (n_max, pair_capacity < 2^30; at most
+ * 65536 pixels per axis).  The caller zero-fills a workspace ONCE when it
+ * allocates it: the radix passes' look-back words are epoch-tagged and never
+ * cleared per frame. */
 size_t seele_workspace_bytes(int64_t n_max, int64_t pair_capacity, int32_t width, int32_t height);
 
 /* One frame: plan_frame (render.py:90-141) + every tile of render_frame

@@ -92,8 +92,8 @@ int check_camera(const seele_camera *c) {
     if (!(c->fov_x > 0.0 && c->fov_x < M_PI) || !(c->fov_y > 0.0 && c->fov_y < M_PI))
         return fail(SEELE_ERR_DATA, "fov must lie in (0, pi)");
     long long tiles_x = (c->width + kTile - 1) / kTile, tiles_y = (c->height + kTile - 1) / kTile;
-    if (tiles_x > 32767 || tiles_y > 32767 || tiles_x * tiles_y >= (1ll << 29))
-        return fail(SEELE_ERR_INVALID_ARGUMENT, "image too large");
+    if (tiles_x > kMaxTileAxis || tiles_y > kMaxTileAxis)
+        return fail(SEELE_ERR_INVALID_ARGUMENT, "image too large (at most 4096 pixels per axis)");
     return SEELE_OK;
 }
 
@@ -120,7 +120,15 @@ Workspace carve_workspace(void *base, long long n_max, long long cap, int width,
     Carver c{static_cast<char *>(base)};
     Workspace w;
     const long long n = n_max > 0 ? n_max : 1;
-    const long long tiles = (long long)((width + kTile - 1) / kTile) * ((height + kTile - 1) / kTile);
+    const int tiles_x = (width + kTile - 1) / kTile, tiles_y = (height + kTile - 1) / kTile;
+    const long long tiles = (long long)tiles_x * tiles_y;
+    // never-cleared state first (epoch + look-back words; zero-filled once by the owner)
+    w.epoch = c.take<uint32_t>(1);
+    w.look_tiles_d = (n + kSortTile - 1) / kSortTile;
+    // the column pass has at most one partial chunk per row beyond cap / tile
+    w.look_tiles_p = (cap + kSortTile - 1) / kSortTile + kMaxTileAxis + 1;
+    w.look = c.take<unsigned long long>(kDepthPasses * w.look_tiles_d * 256 + w.look_tiles_d +
+                                        2 * w.look_tiles_p * 256);
     w.status = c.take<uint8_t>(n);
     w.depth = c.take<double>(n);
     w.tiles = c.take<uint32_t>(n);
@@ -129,19 +137,23 @@ Workspace carve_workspace(void *base, long long n_max, long long cap, int width,
     w.conic_op = c.take<double4>(n);
     w.color = c.take<float4>(n);
     w.fast = c.take<float4>(n);
-    w.dkey[0] = c.take<uint64_t>(n);
-    w.dkey[1] = c.take<uint64_t>(n);
+    w.dkey[0] = c.take<uint32_t>(n);
+    w.dkey[1] = c.take<uint32_t>(n);
+    w.long_runs = c.take<uint2>(kLongRunsMax);
     w.dval[0] = c.take<uint32_t>(n);
     w.dval[1] = c.take<uint32_t>(n);
-    w.poff = c.take<unsigned long long>(n + 1);
-    w.tile_r0 = c.take<uint32_t>(cap / 2048 + 2);
-    w.pkey[0] = c.take<uint32_t>(cap);
-    w.pkey[1] = c.take<uint32_t>(cap);
-    w.pval[0] = c.take<uint32_t>(cap);
-    w.pval[1] = c.take<uint32_t>(cap);
+    w.poff = c.take<uint32_t>(n + 1);
+    w.tile_r0 = c.take<uint32_t>(cap / kSortTile + 2);
+    w.ent_x = c.take<uint32_t>(cap);
+    w.ent_p = c.take<uint32_t>(cap);
+    w.pfinal = c.take<uint32_t>(cap);
     w.ranges = c.take<uint2>(tiles);
-    w.block_sums = c.take<unsigned long long>(kChunkBlocksMax + 1);
-    w.hist = c.take<uint32_t>(256LL * kChunkBlocksMax + 256);  // + per-digit totals
+    w.dhist = c.take<uint32_t>(kDepthPasses * 256);
+    w.row_start = c.take<uint32_t>(kMaxTileAxis + 2);
+    w.chunk_first = c.take<uint32_t>(kMaxTileAxis + 2);
+    w.tile_diff = c.take<int32_t>((long long)(tiles_x + 1) * (tiles_y + 1));
+    w.row_diff = c.take<int32_t>(tiles_y + 1);
+    w.minmax = c.take<unsigned long long>(2);
     w.counters = c.take<uint32_t>(CNT_COUNT);
     w.pairs64 = c.take<unsigned long long>(1);
     w.bytes = c.off;
@@ -184,6 +196,14 @@ __global__ void k_export_splats(Workspace ws, long long n, int8_t *status, doubl
     }
 }
 
+__global__ void k_export_ranges(const uint2 *ranges, int n, int32_t *out) {
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= n) return;
+    const uint2 r = ranges[t];
+    out[2 * t] = r.x < r.y ? (int32_t)r.x : 0;  // empty tiles -> (0, 0)
+    out[2 * t + 1] = r.x < r.y ? (int32_t)r.y : 0;
+}
+
 }  // namespace
 }  // namespace seele
 
@@ -220,7 +240,7 @@ int seele_render(const seele_scene *scene, const int64_t *ranges_dev, int32_t n_
     }
     if (n_ranges < 1 || n_ranges > SEELE_MAX_RANGES || !ranges_dev)
         return fail(SEELE_ERR_INVALID_ARGUMENT, "need 1..64 working-set ranges, got %d", n_ranges);
-    if (n_max < 1 || n_max > (1ll << 31) - 1 || pair_capacity < 1 || pair_capacity > (1ll << 31) - 1)
+    if (n_max < 1 || n_max >= (1ll << 30) || pair_capacity < 1 || pair_capacity >= (1ll << 30))
         return fail(SEELE_ERR_INVALID_ARGUMENT, "n_max / pair_capacity out of range");
     if (!workspace || !image_dev || !stats_dev) return fail(SEELE_ERR_INVALID_ARGUMENT, "null output or workspace");
     const Workspace ws = carve_workspace(workspace, n_max, pair_capacity, cam->width, cam->height);
@@ -250,23 +270,18 @@ int seele_render(const seele_scene *scene, const int64_t *ranges_dev, int32_t n_
     sk.plane_stride = scene->plane_stride;
 
     cudaError_t e;
-    if ((e = cudaMemsetAsync(stats_dev, 0, sizeof(int64_t) * SEELE_STAT_COUNT, st)) != cudaSuccess)
-        return cuda_fail(e, "memset stats");
-    if ((e = cudaMemsetAsync(ws.counters, 0, sizeof(uint32_t) * CNT_COUNT, st)) != cudaSuccess)
-        return cuda_fail(e, "memset counters");
     const int sms = sm_count();
-    const int G = chunk_grid(sms);
     long long pre_blocks = (n_max + 255) / 256;
     const int pre_grid = (int)(pre_blocks < 16LL * sms ? (pre_blocks > 0 ? pre_blocks : 1) : 16LL * sms);
+    launch_frame_begin(ws, ck, stats_dev, st);
     prof_mark(0, st);
     launch_preprocess(sk, ranges_dev, n_ranges, ck, cf, ws, stats_dev, pre_grid, st);
     prof_mark(1, st);
-    uint32_t *sorted_pos = nullptr, *pair_pos = nullptr, *pair_tile = nullptr;
-    launch_depth_rank(ws, n_max, G, stats_dev, &sorted_pos, st);
+    launch_depth_sort(ws, n_max, stats_dev, st);
     prof_mark(2, st);
-    launch_binning(ws, sorted_pos, n_max, pair_capacity, ck, G, stats_dev, &pair_pos, &pair_tile, st);
+    launch_binning(ws, n_max, pair_capacity, ck, stats_dev, st);
     prof_mark(3, st);
-    launch_raster(ws, pair_pos, ck, cf, image_dev, contrib_dev, stats_dev, st);
+    launch_raster(ws, ws.pfinal, ck, cf, image_dev, contrib_dev, stats_dev, st);
     prof_mark(4, st);
     if ((e = cudaGetLastError()) != cudaSuccess) return cuda_fail(e, "seele_render launch");
     return SEELE_OK;
@@ -323,17 +338,16 @@ int seele_plan_export(void *workspace, int64_t n_max, int64_t pair_capacity, int
     if (n_pairs > pair_capacity || n_ws > n_max) return fail(SEELE_ERR_INVALID_ARGUMENT, "sizes exceed the workspace");
     const Workspace ws = carve_workspace(workspace, n_max, pair_capacity, width, height);
     cudaStream_t st = static_cast<cudaStream_t>(stream);
-    const long long n_tiles_all = (long long)((width + kTile - 1) / kTile) * ((height + kTile - 1) / kTile);
-    const int buf = pair_buffer((int)n_tiles_all);
+    const long long tiles = (long long)((width + kTile - 1) / kTile) * ((height + kTile - 1) / kTile);
     cudaError_t e = cudaSuccess;
     if (out->pair_pos && n_pairs > 0)
-        e = cudaMemcpyAsync(out->pair_pos, ws.pval[buf], sizeof(uint32_t) * n_pairs, cudaMemcpyDeviceToDevice, st);
-    if (e == cudaSuccess && out->pair_tile && n_pairs > 0)
-        e = cudaMemcpyAsync(out->pair_tile, ws.pkey[buf], sizeof(uint32_t) * n_pairs, cudaMemcpyDeviceToDevice, st);
-    const long long tiles = (long long)((width + kTile - 1) / kTile) * ((height + kTile - 1) / kTile);
-    if (e == cudaSuccess && out->ranges)
-        e = cudaMemcpyAsync(out->ranges, ws.ranges, sizeof(uint2) * tiles, cudaMemcpyDeviceToDevice, st);
+        e = cudaMemcpyAsync(out->pair_pos, ws.pfinal, sizeof(uint32_t) * n_pairs, cudaMemcpyDeviceToDevice, st);
     if (e != cudaSuccess) return cuda_fail(e, "seele_plan_export copy");
+    if (out->pair_tile && n_pairs > 0) launch_fill_pair_tiles(ws.ranges, (int)tiles, out->pair_tile, st);
+    if (out->ranges) {
+        k_export_ranges<<<(int)((tiles + 255) / 256), 256, 0, st>>>(ws.ranges, (int)tiles, out->ranges);
+        note_launches(1);
+    }
     if (n_ws > 0)
         k_export_splats<<<(int)((n_ws + 255) / 256 < 4096 ? (n_ws + 255) / 256 : 4096), 256, 0, st>>>(
             ws, n_ws, out->status, out->depth, out->rect, out->mean, out->conic, out->opacity, out->color);

@@ -1,447 +1,867 @@
-// Tile binning and sort on sm_100a.  Every size is read from device memory,
-// so a frame needs no host round trip:
-//   1. ordered compaction of the binned splats (assembled order)        [scan]
-//   2. stable LSD radix sort of their fp64 depth bits                    [depth rank]
-//      -> order by (depth, assembled position), the reference's
-//         (depth, gaussian_ref) tie-break (sorting.py:43, render.py:108)
-//   3. exclusive scan of tile counts in depth-rank order, then pair emission
-//      load-balanced by pairs (key = tile id, value = assembled position)
-//                                                                        [bin_tiles,
-//      preprocess.py:159-189]
-//   4. stable LSD radix sort on the tile id (ceil(log2 tiles) bits): stability
-//      keeps depth-rank order inside a tile -> (tile_id, depth, ref) order of
-//      sort_intersections (sorting.py:32-54)
-//   5. per-tile [start, end) ranges                                     [sorting.py:46-53]
+// Depth ordering, tile binning and the tile sort on sm_100a.  Every size is
+// read from device memory, so a frame needs no host round trip:
 //
-// Radix passes: per-block digit histograms, one scan block per digit, and a
-// scatter that ranks IPT x 256 items per iteration stably (warp
-// __match_any_sync + per-(sub-round, warp) digit prefixes), stages them in
-// shared memory in digit order and writes digit runs coalesced.
-#include "common.cuh"
+//   depth sort   stable LSD radix sort of all assembled splats on
+//                key = fp64 depth bits - min binned bits (binned splats;
+//                the others get key = range + 1 and sort last), value =
+//                assembled position.  Input in assembled order, so ties
+//                break by position = the reference's (depth, gaussian_ref)
+//                order (sorting.py:43, render.py:108).  One up-front
+//                histogram kernel + one onesweep kernel per 8-bit digit;
+//                passes beyond the key's significant bits exit at once.
+//   pair scan    exclusive scan of tile counts in depth-rank order
+//                (decoupled look-back), first rank of every 4096-pair
+//                emission tile, per-axis tile histograms (difference arrays)
+//                from which the last CTA derives every tile-sort digit base.
+//   emission     bin_tiles (preprocess.py:159-189) in depth-rank order, key
+//                = ty << xb | tx (sorted key = linear tile id), fused with
+//                the first stable radix pass of the tile sort.
+//   tile sort    remaining passes; the last one writes only the splat
+//                position of each pair (final order = sort_intersections,
+//                sorting.py:32-54) and the per-tile [start, end) ranges
+//                (sorting.py:46-53) by atomicMin / atomicMax of its runs.
+#include "onesweep.cuh"
 
 namespace seele {
 
+using namespace sweep;
+
+#ifdef SEELE_SORT_TRACE
+__device__ unsigned long long g_trace[8][4096][6];
+__device__ __forceinline__ unsigned long long gtime() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+#define TRACE(pass, t, k) \
+    if (threadIdx.x == 0 && (t) < 4096) g_trace[pass][t][k] = gtime();
+#else
+#define TRACE(pass, t, k)
+#endif
+
 namespace {
 
-__device__ __forceinline__ long long chunk_size(long long n, int G) {
-    long long c = (n + G - 1) / G;
-    return (c + 1023) / 1024 * 1024;
+// Depth-sort key: the fp64 depth quantised to 24 bits over [min, max] of the
+// binned depths.  Every IEEE operation is monotone, so key(d) is monotone
+// non-decreasing in d: sorting by key orders by depth except inside runs of
+// equal keys, which the fix-up re-sorts by (fp64 depth, position).
+struct DepthKey {
+    double lo, scale;
+};
+
+__device__ __forceinline__ DepthKey depth_key(const Workspace &ws) {
+    DepthKey k;
+    const unsigned long long lo = ws.minmax[0], hi = ws.minmax[1];
+    k.lo = 0.0;
+    k.scale = 0.0;
+    if (lo <= hi) {
+        k.lo = __longlong_as_double((long long)lo);
+        const double span = __longlong_as_double((long long)hi) - k.lo;
+        k.scale = span > 0.0 ? 16777214.0 / span : 0.0;
+    }
+    return k;
 }
 
-// 256-thread block exclusive scan of one value per thread.
-template <typename T>
-__device__ __forceinline__ T block_exclusive_scan(T v, T &total) {
-    __shared__ T s_warp[8];
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    T x = v;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-        T y = __shfl_up_sync(0xffffffffu, x, o);
-        if (lane >= o) x += y;
+__device__ __forceinline__ uint32_t depth_quant(const DepthKey &k, uint32_t tiles, double d) {
+    if (tiles == 0u) return 0xffffffu;  // not binned: after every binned splat
+    const double q = floor((d - k.lo) * k.scale);
+    return q < 16777214.0 ? (uint32_t)q : 0xfffffeu;
+}
+
+// ---- frame start ---------------------------------------------------------------
+
+__global__ void k_frame_begin(Workspace ws, int64_t *stats, int n_diff, int tiles_y) {
+    const int tid = blockIdx.x * blockDim.x + threadIdx.x, stride = gridDim.x * blockDim.x;
+    if (tid == 0) {
+        *ws.epoch += 1u;
+        ws.minmax[0] = ~0ull;
+        ws.minmax[1] = 0ull;
+        *ws.pairs64 = 0ull;
     }
-    if (lane == 31) s_warp[warp] = x;
+    if (tid < SEELE_STAT_COUNT) stats[tid] = 0;
+    if (tid < CNT_COUNT) ws.counters[tid] = 0u;
+    for (int i = tid; i < kDepthPasses * 256; i += stride) ws.dhist[i] = 0u;
+    for (int i = tid; i < n_diff; i += stride) ws.tile_diff[i] = 0;
+    for (int i = tid; i <= tiles_y; i += stride) ws.row_diff[i] = 0;
+}
+
+// ---- depth sort ------------------------------------------------------------------
+
+__global__ void __launch_bounds__(256) k_depth_hist(Workspace ws) {
+    __shared__ uint32_t h[kDepthPasses][256];
+    __shared__ bool s_last;
+    const int tid = threadIdx.x;
+    for (int i = tid; i < kDepthPasses * 256; i += 256) (&h[0][0])[i] = 0u;
     __syncthreads();
-    if (warp == 0) {
-        T w = lane < 8 ? s_warp[lane] : T(0);
+    const DepthKey k = depth_key(ws);
+    const uint32_t n = ws.counters[CNT_WS];
+    constexpr int U = 8;
+    for (uint32_t i0 = blockIdx.x * 256 * U + tid; i0 < n; i0 += gridDim.x * 256 * U) {
+        uint32_t tl[U];
+        double d[U];
 #pragma unroll
-        for (int o = 1; o < 8; o <<= 1) {
-            T y = __shfl_up_sync(0xffffffffu, w, o);
-            if (lane >= o) w += y;
+        for (int u = 0; u < U; u++) {
+            const uint32_t i = min(i0 + u * 256, n - 1);
+            tl[u] = ws.tiles[i];
+            d[u] = ws.depth[i];
         }
-        if (lane < 8) s_warp[lane] = w;  // inclusive
-    }
-    __syncthreads();
-    T warp_off = warp ? s_warp[warp - 1] : T(0);
-    total = s_warp[7];
-    __syncthreads();
-    return warp_off + x - v;
-}
-
-// ---- 1. ordered compaction of binned splats ----------------------------------
-
-__global__ void __launch_bounds__(256) k_compact_reduce(Workspace ws) {
-    const long long n = ws.counters[CNT_WS];
-    const long long c = chunk_size(n, gridDim.x);
-    const long long b0 = (long long)blockIdx.x * c, b1 = min(b0 + c, n);
-    unsigned long long acc = 0;
-    for (long long i = b0 + threadIdx.x; i < b1; i += blockDim.x) acc += ws.tiles[i] > 0 ? 1ull : 0ull;
-    unsigned long long tot;
-    block_exclusive_scan<unsigned long long>(acc, tot);
-    if (threadIdx.x == 0) ws.block_sums[blockIdx.x] = tot;
-}
-
-__global__ void __launch_bounds__(1024) k_compact_sums(Workspace ws, int G) {
-    __shared__ unsigned long long s[kChunkBlocksMax];
-    for (int i = threadIdx.x; i < G; i += blockDim.x) s[i] = ws.block_sums[i];
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        unsigned long long run = 0;
-        for (int i = 0; i < G; i++) {
-            const unsigned long long v = s[i];
-            s[i] = run;
-            run += v;
-        }
-        ws.counters[CNT_BINNED] = (uint32_t)run;
-    }
-    __syncthreads();
-    for (int i = threadIdx.x; i < G; i += blockDim.x) ws.block_sums[i] = s[i];
-}
-
-__global__ void __launch_bounds__(256) k_compact_write(Workspace ws) {
-    const long long n = ws.counters[CNT_WS];
-    const long long c = chunk_size(n, gridDim.x);
-    const long long b0 = (long long)blockIdx.x * c, b1 = min(b0 + c, n);
-    unsigned long long run = ws.block_sums[blockIdx.x];
-    for (long long t0 = b0; t0 < b1; t0 += blockDim.x) {
-        const long long i = t0 + threadIdx.x;
-        const unsigned v = (i < b1 && ws.tiles[i] > 0) ? 1u : 0u;
-        unsigned long long tot;
-        const unsigned long long ex = block_exclusive_scan<unsigned long long>(v, tot) + run;
-        if (v) {
-            ws.dkey[0][ex] = (uint64_t)__double_as_longlong(ws.depth[i]);
-            ws.dval[0][ex] = (uint32_t)i;
-        }
-        run += tot;
-    }
-}
-
-// ---- stable LSD radix sort passes ---------------------------------------------
-
-template <typename K>
-__global__ void __launch_bounds__(256) k_radix_hist(const K *__restrict__ keys, const uint32_t *n_ptr, int shift,
-                                                    int bits, uint32_t *hist) {
-    __shared__ uint32_t h[256];
-    const int nd = 1 << bits;
-    h[threadIdx.x] = 0;
-    __syncthreads();
-    const long long n = *n_ptr;
-    const long long c = chunk_size(n, gridDim.x);
-    const long long b0 = (long long)blockIdx.x * c, b1 = min(b0 + c, n);
-    const K mask = (K)(nd - 1);
-    for (long long i = b0 + threadIdx.x; i < b1; i += blockDim.x)
-        atomicAdd(&h[(uint32_t)((keys[i] >> shift) & mask)], 1u);
-    __syncthreads();
-    if (threadIdx.x < nd) hist[(long long)threadIdx.x * gridDim.x + blockIdx.x] = h[threadIdx.x];
-}
-
-// Per digit d (one block each): exclusive scan over the G block counts of that
-// digit, in place, and the digit total into tot[d].
-__global__ void __launch_bounds__(256) k_radix_scan(uint32_t *hist, uint32_t *tot, int G) {
-    uint32_t *row = hist + (long long)blockIdx.x * G;
-    const int per = (G + 255) / 256;
-    const int a = threadIdx.x * per, b = min(a + per, G);
-    uint32_t sum = 0;
-    for (int i = a; i < b; i++) sum += row[i];
-    uint32_t total;
-    uint32_t run = block_exclusive_scan<uint32_t>(sum, total);
-    for (int i = a; i < b; i++) {
-        const uint32_t v = row[i];
-        row[i] = run;
-        run += v;
-    }
-    if (threadIdx.x == 0) tot[blockIdx.x] = total;
-}
-
-template <typename K, int IPT>
-__global__ void __launch_bounds__(256) k_radix_scatter(const K *__restrict__ kin, const uint32_t *__restrict__ vin,
-                                                       K *__restrict__ kout, uint32_t *__restrict__ vout,
-                                                       const uint32_t *n_ptr, int shift, int bits,
-                                                       const uint32_t *__restrict__ hist,
-                                                       const uint32_t *__restrict__ tot) {
-    constexpr int TILE = 256 * IPT;
-    __shared__ uint32_t s_base[256];            // global destination of the next item of each digit
-    __shared__ uint32_t s_loc[256];             // digit offsets inside the staged tile
-    __shared__ uint16_t s_wh[IPT][8][256];      // per (sub-round, warp, digit) counts -> prefixes
-    __shared__ K s_key[TILE];
-    __shared__ uint32_t s_val[TILE];
-    const int nd = 1 << bits;
-    const int G = gridDim.x;
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    uint32_t digit_total;
-    const uint32_t digit_base = block_exclusive_scan<uint32_t>(tid < nd ? tot[tid] : 0u, digit_total);
-    s_base[tid] = tid < nd ? digit_base + hist[(long long)tid * G + blockIdx.x] : 0u;
 #pragma unroll
-    for (int r = 0; r < IPT; r++)
-        for (int w = 0; w < 8; w++) s_wh[r][w][tid] = 0;
-    __syncthreads();
-    const long long n = *n_ptr;
-    const long long c = chunk_size(n, G);
-    const long long b0 = (long long)blockIdx.x * c, b1 = min(b0 + c, n);
-    const K mask = (K)(nd - 1);
-    const unsigned lt = (1u << lane) - 1u;
-    for (long long t0 = b0; t0 < b1; t0 += TILE) {
-        const int n_tile = (int)min((long long)TILE, b1 - t0);
-        K key[IPT];
-        uint32_t val[IPT], dig[IPT], rank[IPT];
+        for (int u = 0; u < U; u++) {
+            if (i0 + u * 256 >= n) break;
+            const uint32_t key = depth_quant(k, tl[u], d[u]);
 #pragma unroll
-        for (int r = 0; r < IPT; r++) {  // striped: item t0 + r*256 + tid keeps the input order
-            const int li = r * 256 + tid;
-            const bool valid = li < n_tile;
-            dig[r] = 0xffffffffu;
-            if (valid) {
-                key[r] = kin[t0 + li];
-                val[r] = vin[t0 + li];
-                dig[r] = (uint32_t)((key[r] >> shift) & mask);
+            for (int p = 0; p < kDepthPasses; p++) atomicAdd(&h[p][(key >> (8 * p)) & 0xffu], 1u);
+        }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int p = 0; p < kDepthPasses; p++)
+        if (h[p][tid]) atomicAdd(&ws.dhist[p * 256 + tid], h[p][tid]);
+    __threadfence();
+    __syncthreads();
+    if (tid == 0) s_last = atomicAdd(&ws.counters[CNT_DONE_HIST], 1u) == gridDim.x - 1;
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
+    // last CTA: digit totals -> exclusive digit bases (256 threads, one digit each)
+    for (int p = 0; p < kDepthPasses; p++) {
+        const uint32_t v = *(volatile uint32_t *)&ws.dhist[p * 256 + tid];
+        __shared__ uint32_t s_v[256];
+        s_v[tid] = v;
+        __syncthreads();
+        if (tid == 0) {
+            uint32_t run = 0;
+            for (int d = 0; d < 256; d++) {
+                const uint32_t c = s_v[d];
+                s_v[d] = run;
+                run += c;
             }
-            const unsigned peers = __match_any_sync(0xffffffffu, dig[r]);
-            rank[r] = __popc(peers & lt);
-            if (valid && rank[r] == 0) s_wh[r][warp][dig[r]] = (uint16_t)__popc(peers);
         }
         __syncthreads();
-        uint32_t cnt = 0;
-        if (tid < nd) {
-#pragma unroll
-            for (int r = 0; r < IPT; r++)
-#pragma unroll
-                for (int w = 0; w < 8; w++) {
-                    const uint32_t v = s_wh[r][w][tid];
-                    s_wh[r][w][tid] = (uint16_t)cnt;
-                    cnt += v;
-                }
-        }
-        uint32_t tile_total;
-        const uint32_t loc = block_exclusive_scan<uint32_t>(cnt, tile_total);
-        if (tid < nd) s_loc[tid] = loc;
+        ws.dhist[p * 256 + tid] = s_v[tid];
         __syncthreads();
+    }
+}
+
+// One 8-bit pass of the depth sort.  Pass 0 builds its keys from the
+// preprocess outputs (value = assembled position).
+__global__ void __launch_bounds__(NT, 2) k_depth_pass(Workspace ws, int pass) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    RankSmem &rs = *reinterpret_cast<RankSmem *>(smem);
+    uint32_t *skey = reinterpret_cast<uint32_t *>(smem + sizeof(RankSmem));
+    uint32_t *sval = skey + TILE;
+    __shared__ uint32_t s_base[RADIX];
+#ifdef SEELE_SORT_TRACE
+    const unsigned long long t_enter = gtime();
+#endif
+    const uint32_t t = take_ticket(&ws.counters[CNT_TICKET + kLookDepth + pass]);
+    const uint32_t n = ws.counters[CNT_WS];
+    const uint32_t t0 = t * TILE;
+    if (t0 >= n) return;
+#ifdef SEELE_SORT_TRACE
+    if (threadIdx.x == 0 && t < 4096) g_trace[pass][t][0] = t_enter;
+#endif
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int shift = 8 * pass;
+    uint32_t key[IPT], val[IPT], dig[IPT], pos[IPT];
+    const uint32_t ib = t0 + warp * 32 * IPT + lane;
+    if (pass == 0) {
+        const DepthKey dk = depth_key(ws);
+        uint32_t tl[IPT];
+        double d[IPT];
 #pragma unroll
         for (int r = 0; r < IPT; r++) {
-            if (dig[r] == 0xffffffffu) continue;
-            const uint32_t li = s_loc[dig[r]] + s_wh[r][warp][dig[r]] + rank[r];
-            s_key[li] = key[r];
-            s_val[li] = val[r];
+            const uint32_t i = min(ib + r * 32, n - 1);
+            tl[r] = ws.tiles[i];
+            d[r] = ws.depth[i];
         }
-        __syncthreads();
-        for (int li = tid; li < n_tile; li += 256) {  // digit runs land on consecutive addresses
-            const K k = s_key[li];
-            const uint32_t d = (uint32_t)((k >> shift) & mask);
-            const uint32_t dst = s_base[d] + (uint32_t)li - s_loc[d];
-            kout[dst] = k;
-            vout[dst] = s_val[li];
-        }
-        __syncthreads();
-        if (tid < nd) {
-            s_base[tid] += cnt;
 #pragma unroll
-            for (int r = 0; r < IPT; r++)
-                for (int w = 0; w < 8; w++) s_wh[r][w][tid] = 0;
+        for (int r = 0; r < IPT; r++) {
+            key[r] = depth_quant(dk, tl[r], d[r]);
+            val[r] = ib + r * 32;
         }
-        __syncthreads();
+    } else {
+        const uint32_t *kin = ws.dkey[(pass + 1) & 1];
+        const uint32_t *vin = ws.dval[(pass + 1) & 1];
+#pragma unroll
+        for (int r = 0; r < IPT; r++) {
+            const uint32_t i = min(ib + r * 32, n - 1);
+            key[r] = kin[i];
+            val[r] = vin[i];
+        }
     }
-}
-
-template <typename K>
-int radix_sort(K *keys[2], uint32_t *vals[2], const uint32_t *n_ptr, int begin_bit, int end_bit, uint32_t *hist,
-               uint32_t *tot, int G, cudaStream_t st) {
-    int cur = 0;
-    for (int shift = begin_bit; shift < end_bit; shift += 8) {
-        const int bits = min(8, end_bit - shift);
-        k_radix_hist<K><<<G, 256, 0, st>>>(keys[cur], n_ptr, shift, bits, hist);
-        k_radix_scan<<<1 << bits, 256, 0, st>>>(hist, tot, G);
-        k_radix_scatter<K, 4><<<G, 256, 0, st>>>(keys[cur], vals[cur], keys[cur ^ 1], vals[cur ^ 1], n_ptr, shift,
-                                                 bits, hist, tot);
-        cur ^= 1;
-        note_launches(3);
-    }
-    return cur;
-}
-
-// ---- 3. pair emission, load-balanced by pairs ----------------------------------
-
-// Exclusive scan of the tile counts in depth-rank order -> first pair of each rank.
-__global__ void __launch_bounds__(256) k_pairs_reduce(Workspace ws, const uint32_t *__restrict__ sorted_pos) {
-    const long long n = ws.counters[CNT_BINNED];
-    const long long c = chunk_size(n, gridDim.x);
-    const long long b0 = (long long)blockIdx.x * c, b1 = min(b0 + c, n);
-    unsigned long long acc = 0;
-    for (long long r = b0 + threadIdx.x; r < b1; r += blockDim.x) acc += ws.tiles[sorted_pos[r]];
-    unsigned long long tot;
-    block_exclusive_scan<unsigned long long>(acc, tot);
-    if (threadIdx.x == 0) ws.block_sums[blockIdx.x] = tot;
-}
-
-__global__ void __launch_bounds__(1024) k_pairs_sums(Workspace ws, int G, long long cap, int64_t *stats) {
-    __shared__ unsigned long long s[kChunkBlocksMax];
-    for (int i = threadIdx.x; i < G; i += blockDim.x) s[i] = ws.block_sums[i];
+#pragma unroll
+    for (int r = 0; r < IPT; r++) dig[r] = ib + r * 32 < n ? (key[r] >> shift) & 0xffu : NO_DIGIT;
+#ifdef SEELE_SORT_TRACE
     __syncthreads();
-    if (threadIdx.x == 0) {
-        unsigned long long run = 0;
-        for (int i = 0; i < G; i++) {
-            const unsigned long long v = s[i];
-            s[i] = run;
-            run += v;
+    TRACE(pass, t, 1)
+#endif
+    uint32_t count;
+    block_rank(dig, pos, rs, count);
+    TRACE(pass, t, 2)
+    if (tid < RADIX) {
+        const uint32_t ex = lookback(ws.look_region(kLookDepth + pass) + tid, RADIX, t,
+                                     *ws.epoch * 16u + (uint32_t)(kLookDepth + pass), count, t == 0);
+        s_base[tid] = ws.dhist[pass * 256 + tid] + ex - rs.start[tid];
+    }
+#ifdef SEELE_SORT_TRACE
+    __syncthreads();
+    TRACE(pass, t, 3)
+#endif
+#pragma unroll
+    for (int r = 0; r < IPT; r++) {
+        if (dig[r] == NO_DIGIT) continue;
+        skey[pos[r]] = key[r];
+        sval[pos[r]] = val[r];
+    }
+    __syncthreads();
+    const int nv = (int)min((uint32_t)TILE, n - t0);
+    uint32_t *kout = ws.dkey[pass & 1];
+    uint32_t *vout = ws.dval[pass & 1];
+    for (int i = tid; i < nv; i += NT) {
+        const uint32_t k = skey[i];
+        const uint32_t dst = s_base[(k >> shift) & 0xffu] + (uint32_t)i;
+        kout[dst] = k;
+        vout[dst] = sval[i];
+    }
+#ifdef SEELE_SORT_TRACE
+    __syncthreads();
+    TRACE(pass, t, 4)
+#endif
+}
+
+// (fp64 depth, position) order inside one run of equal quantised keys.
+__device__ __forceinline__ bool depth_less(double da, uint32_t pa, double db, uint32_t pb) {
+    return da < db || (da == db && pa < pb);
+}
+
+// Exact order inside runs of equal 32-bit keys among the binned splats:
+// short runs by the thread at the run start (insertion sort, already sorted
+// by position), runs longer than 32 are queued for k_depth_fix_long.
+__global__ void __launch_bounds__(256) k_depth_fixup(Workspace ws, const int64_t *stats) {
+    constexpr int U = 8;  // positions per thread, keys loaded up front
+    const uint32_t n = (uint32_t)stats[SEELE_STAT_BINNED];
+    const uint32_t *key = ws.dkey[kDepthFinal];
+    uint32_t *val = ws.dval[kDepthFinal];
+    const uint32_t i0 = (blockIdx.x * blockDim.x + threadIdx.x) * U;
+    if (i0 + 1 >= n) return;
+    uint32_t k[U + 2];  // k[j + 1] = key[i0 + j], j = -1 .. U
+#pragma unroll
+    for (int j = 0; j < U + 2; j++) {
+        const long long i = (long long)i0 + j - 1;
+        k[j] = (i >= 0 && i < (long long)n) ? key[i] : (j == 0 ? 0xfffffffeu : 0xffffffffu);
+    }
+    if (i0 == 0) k[0] = ~k[1];
+#pragma unroll
+    for (int j = 0; j < U; j++) {
+        const uint32_t i = i0 + j;
+        if (i + 1 >= n || k[j + 2] != k[j + 1] || k[j] == k[j + 1]) continue;  // not the start of a run >= 2
+        const uint32_t kk = k[j + 1];
+        uint32_t e = i + 2;
+        while (e < n && e - i < 32 && key[e] == kk) e++;
+        if (e < n && key[e] == kk) {  // long run: queue it
+            while (e < n && key[e] == kk) e++;
+            const uint32_t slot = atomicAdd(&ws.counters[CNT_LONG_RUNS], 1u);
+            if (slot < kLongRunsMax) ws.long_runs[slot] = make_uint2(i, e - i);
+            continue;
         }
-        stats[SEELE_STAT_TILE_PAIRS] = (int64_t)run;
-        const bool over = run > (unsigned long long)cap;
-        ws.counters[CNT_OVERFLOW] = over ? 1u : 0u;
-        ws.counters[CNT_PAIRS] = over ? 0u : (uint32_t)run;
+        const int m = (int)(e - i);
+        if (m == 2) {  // the common case: one pair, in registers
+            const uint32_t p0 = val[i], p1 = val[i + 1];
+            const double d0 = ws.depth[p0], d1 = ws.depth[p1];
+            if (depth_less(d1, p1, d0, p0)) {
+                val[i] = p1;
+                val[i + 1] = p0;
+            }
+            continue;
+        }
+        uint32_t p[32];
+        double d[32];
+        for (int q = 0; q < m; q++) {
+            p[q] = val[i + q];
+            d[q] = ws.depth[p[q]];
+        }
+        bool moved = false;
+        for (int q = 1; q < m; q++) {
+            const uint32_t pq = p[q];
+            const double dq = d[q];
+            int z = q - 1;
+            while (z >= 0 && depth_less(dq, pq, d[z], p[z])) {
+                p[z + 1] = p[z];
+                d[z + 1] = d[z];
+                z--;
+            }
+            if (z + 1 != q) moved = true;
+            p[z + 1] = pq;
+            d[z + 1] = dq;
+        }
+        if (moved)
+            for (int q = 0; q < m; q++) val[i + q] = p[q];
+    }
+}
+
+// Long equal-key runs (rare: > 32 splats within one quantisation step): one
+// CTA per run, each item's rank = number of run items before it in
+// (depth, position) order.  Runs up to kFixSmem items are staged in shared
+// memory; longer ones are ranked from global memory into the spare buffer.
+constexpr int kFixSmem = 4096;
+
+__global__ void __launch_bounds__(512) k_depth_fix_long(Workspace ws) {
+    __shared__ double s_d[kFixSmem];
+    __shared__ uint32_t s_p[kFixSmem];
+    const uint32_t nq = min(ws.counters[CNT_LONG_RUNS], (uint32_t)kLongRunsMax);
+    uint32_t *val = ws.dval[kDepthFinal];
+    uint32_t *spare = ws.dval[kDepthFinal ^ 1];
+    for (uint32_t q = blockIdx.x; q < nq; q += gridDim.x) {
+        const uint2 run = ws.long_runs[q];
+        const uint32_t s = run.x, m = run.y;
+        if (m <= (uint32_t)kFixSmem) {
+            for (uint32_t j = threadIdx.x; j < m; j += blockDim.x) {
+                s_p[j] = val[s + j];
+                s_d[j] = ws.depth[s_p[j]];
+            }
+            __syncthreads();
+            for (uint32_t j = threadIdx.x; j < m; j += blockDim.x) {
+                const double dj = s_d[j];
+                const uint32_t pj = s_p[j];
+                uint32_t r = 0;
+                for (uint32_t k = 0; k < m; k++) r += depth_less(s_d[k], s_p[k], dj, pj);
+                val[s + r] = pj;
+            }
+            __syncthreads();
+        } else {
+            for (uint32_t j = threadIdx.x; j < m; j += blockDim.x) {
+                const uint32_t pj = val[s + j];
+                const double dj = ws.depth[pj];
+                uint32_t r = 0;
+                for (uint32_t k = 0; k < m; k++) {
+                    const uint32_t pk = val[s + k];
+                    r += depth_less(ws.depth[pk], pk, dj, pj);
+                }
+                spare[s + r] = pj;
+            }
+            __syncthreads();
+            for (uint32_t j = threadIdx.x; j < m; j += blockDim.x) val[s + j] = spare[s + j];
+            __syncthreads();
+        }
+    }
+}
+
+// ---- row entries: offsets, tile counts, ranges -------------------------------------
+
+// bin_tiles (preprocess.py:159-189) of splat rank r covers rect [x0,x1] x [y0,y1]
+// -> one row entry per covered tile row y (x range [x0, x1]) and w * h pairs.
+// This persistent kernel scans the entry counts h in depth-rank order
+// (decoupled look-back over 4096-rank tiles) into poff, marks the first rank
+// of every 4096-entry tile of the row pass, counts pairs, and accumulates the
+// 2D difference array of per-tile pair counts and the 1D one of per-row entry
+// counts.  The last CTA turns those into the tile ranges (sorting.py:46-53),
+// the row bases of the row pass and the chunk table of the column pass.
+__global__ void __launch_bounds__(NT) k_pair_scan(Workspace ws, int tiles_x, int tiles_y, long long cap, int use_smem,
+                                                  int64_t *stats) {
+    extern __shared__ int32_t s_diff[];  // [(tiles_y + 1) * (tiles_x + 1)] if use_smem
+    __shared__ int32_t s_row[kMaxTileAxis + 1];
+    __shared__ bool s_last;
+    __shared__ uint32_t s_prev;
+    __shared__ unsigned long long s_pairs;
+    const int tid = threadIdx.x;
+    const int tx1 = tiles_x + 1;
+    const int ndiff = tx1 * (tiles_y + 1);
+    if (use_smem)
+        for (int i = tid; i < ndiff; i += NT) s_diff[i] = 0;
+    for (int i = tid; i <= tiles_y; i += NT) s_row[i] = 0;
+    if (tid == 0) s_pairs = 0ull;
+    int32_t *diff = use_smem ? s_diff : ws.tile_diff;
+    const uint32_t n = (uint32_t)stats[SEELE_STAT_BINNED];
+    const uint32_t *sorted = ws.dval[kDepthFinal];
+    const uint32_t n_etiles = (uint32_t)(cap / TILE) + 1u;  // tile_r0 entries kept (capacity)
+    unsigned long long my_pairs = 0ull;
+    while (true) {
+        const uint32_t t = take_ticket(&ws.counters[CNT_TICKET + kLookScan]);
+        if (t * TILE >= n) break;
+        const uint32_t r0 = t * TILE + tid * IPT;
+        uint32_t h[IPT];
+        uint32_t sum = 0;
+#pragma unroll
+        for (int k = 0; k < IPT; k++) {
+            h[k] = 0u;
+            const uint32_t r = r0 + k;
+            if (r < n) {
+                const short4 rc = ws.rect[sorted[r]];
+                const int w = rc.y - rc.x + 1, hh = rc.w - rc.z + 1;
+                h[k] = (uint32_t)hh;
+                my_pairs += (unsigned long long)(w * hh);
+                atomicAdd(&diff[rc.z * tx1 + rc.x], 1);
+                atomicAdd(&diff[rc.z * tx1 + rc.y + 1], -1);
+                atomicAdd(&diff[(rc.w + 1) * tx1 + rc.x], -1);
+                atomicAdd(&diff[(rc.w + 1) * tx1 + rc.y + 1], 1);
+                atomicAdd(&s_row[rc.z], 1);
+                atomicAdd(&s_row[rc.w + 1], -1);
+            }
+            sum += h[k];
+        }
+        uint32_t agg;
+        const uint32_t ex = block_scan<uint32_t>(sum, agg);
+        if (tid == 0) s_prev = lookback(ws.look_region(kLookScan), 1, t, *ws.epoch * 16u + kLookScan, agg, t == 0);
+        __syncthreads();
+        uint32_t run = s_prev + ex;
+#pragma unroll
+        for (int k = 0; k < IPT; k++) {
+            const uint32_t r = r0 + k;
+            if (r >= n) break;
+            ws.poff[r] = run;
+            const uint32_t end = run + h[k];
+            for (uint32_t e = (run + TILE - 1) / TILE; e * TILE < end && e < n_etiles; e++) ws.tile_r0[e] = r;
+            if (r == n - 1) ws.poff[n] = end;
+            run = end;
+        }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) my_pairs += __shfl_xor_sync(0xffffffffu, my_pairs, o);
+    if ((tid & 31) == 0 && my_pairs) atomicAdd(&s_pairs, my_pairs);
+    __syncthreads();
+    if (tid == 0 && s_pairs) atomicAdd(ws.pairs64, s_pairs);
+    if (use_smem)
+        for (int i = tid; i < ndiff; i += NT)
+            if (s_diff[i]) atomicAdd(&ws.tile_diff[i], s_diff[i]);
+    for (int i = tid; i <= tiles_y; i += NT)
+        if (s_row[i]) atomicAdd(&ws.row_diff[i], s_row[i]);
+    __threadfence();
+    __syncthreads();
+    if (tid == 0) s_last = atomicAdd(&ws.counters[CNT_DONE_SCAN], 1u) == gridDim.x - 1;
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
+    // ---- last CTA: per-tile counts -> ranges; row bases; chunk table
+    const unsigned long long total = *(volatile unsigned long long *)ws.pairs64;
+    const bool over = total > (unsigned long long)cap;
+    int32_t *g = use_smem ? s_diff : ws.tile_diff;  // in shared memory when it fits
+    if (use_smem)
+        for (int i = tid; i < ndiff; i += NT) s_diff[i] = *(volatile int32_t *)&ws.tile_diff[i];
+    __syncthreads();
+    // 2D prefix sum in place: rows (one warp per row, lane-parallel scan), then columns
+    {
+        const int lane = tid & 31, warp = tid >> 5;
+        const int per = (tiles_x + 31) / 32;
+        for (int y = warp; y < tiles_y; y += NT / 32) {
+            int32_t *row = g + y * tx1;
+            int32_t run = 0;
+            for (int j = 0; j < per; j++) {
+                const int x = lane * per + j;
+                if (x < tiles_x) run += row[x];
+            }
+            int32_t incl = run;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int32_t v = __shfl_up_sync(0xffffffffu, incl, o);
+                if (lane >= o) incl += v;
+            }
+            int32_t acc = incl - run;
+            for (int j = 0; j < per; j++) {
+                const int x = lane * per + j;
+                if (x < tiles_x) {
+                    acc += row[x];
+                    row[x] = acc;
+                }
+            }
+        }
+    }
+    __syncthreads();
+    for (int x = tid; x < tiles_x; x += NT) {
+        int32_t acc = 0;
+        for (int y = 0; y < tiles_y; y++) {
+            acc += g[y * tx1 + x];
+            g[y * tx1 + x] = acc;
+        }
+    }
+    __syncthreads();
+    // exclusive scan of the per-tile counts in linear tile order -> ranges
+    const int n_tiles = tiles_x * tiles_y;
+    const int per = (n_tiles + NT - 1) / NT;
+    const int a0 = tid * per, a1 = min(a0 + per, n_tiles);
+    uint32_t part = 0;
+    for (int i = a0; i < a1; i++) part += (uint32_t)g[(i / tiles_x) * tx1 + i % tiles_x];
+    uint32_t all;
+    uint32_t acc = block_scan<uint32_t>(part, all);
+    for (int i = a0; i < a1; i++) {
+        const uint32_t c = (uint32_t)g[(i / tiles_x) * tx1 + i % tiles_x];
+        ws.ranges[i] = over ? make_uint2(0u, 0u) : make_uint2(acc, acc + c);
+        acc += c;
+    }
+    // entries per row -> row bases (row pass digit bases) and column-pass chunks
+    for (int i = tid; i <= tiles_y; i += NT) s_row[i] = *(volatile int32_t *)&ws.row_diff[i];
+    __syncthreads();
+    if (tid == 0) {
+        int32_t rc = 0;
+        uint32_t e = 0, c = 0;
+        for (int y = 0; y < tiles_y; y++) {
+            rc += s_row[y];
+            ws.row_start[y] = e;
+            ws.chunk_first[y] = c;
+            e += (uint32_t)rc;
+            c += ((uint32_t)rc + TILE - 1) / TILE;
+        }
+        ws.row_start[tiles_y] = e;
+        ws.chunk_first[tiles_y] = c;
+        stats[SEELE_STAT_TILE_PAIRS] = (int64_t)total;
         stats[SEELE_STAT_OVERFLOW] = over ? 1 : 0;
-        ws.poff[ws.counters[CNT_BINNED]] = run;  // sentinel for the emission search
+        ws.counters[CNT_OVERFLOW] = over ? 1u : 0u;
+        ws.counters[CNT_PAIRS] = over ? 0u : (uint32_t)total;
+        ws.counters[CNT_ENTRIES] = over ? 0u : e;
+        ws.counters[CNT_CHUNKS] = over ? 0u : c;
+    }
+}
+
+// ---- row pass ----------------------------------------------------------------------
+
+struct RowSmem {
+    RankSmem rs;
+    uint32_t s_base[RADIX];
+    union {
+        struct {  // the ranks overlapping this tile
+            uint32_t off[TILE + 3];
+            uint32_t pos[TILE + 2];
+            uint32_t rect[TILE + 2];  // x0 | x1 << 8 | y0 << 16
+        } e;
+        struct {  // the row-sorted tile
+            uint32_t x[TILE];
+            uint32_t p[TILE];
+        } g;
+    } u;
+    uint32_t gx[TILE];  // generated entries in emission order
+    uint32_t gp[TILE];
+};
+
+// Emits the row entries of 4096 consecutive entry slots in depth-rank order
+// (ty-major inside a splat, like bin_tiles) and scatters them stably by row:
+// one onesweep pass whose digit is the tile row.
+__global__ void __launch_bounds__(NT, 2) k_row_pass(Workspace ws, int64_t *stats) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    RowSmem &S = *reinterpret_cast<RowSmem *>(smem);
+    const uint32_t E = ws.counters[CNT_ENTRIES];
+    const uint32_t t = take_ticket(&ws.counters[CNT_TICKET + kLookRows]);
+    const uint32_t base = t * TILE;
+    if (base >= E) return;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const uint32_t n = (uint32_t)stats[SEELE_STAT_BINNED];
+    const uint32_t *sorted = ws.dval[kDepthFinal];
+    const uint32_t end = min(base + (uint32_t)TILE, E);
+    const uint32_t r0 = ws.tile_r0[t];
+    const uint32_t r1 = end < E ? ws.tile_r0[t + 1] : n - 1;  // last rank overlapping
+    const int nr = (int)(r1 - r0 + 1);
+    for (int k = tid; k <= nr; k += NT) {
+        S.u.e.off[k] = ws.poff[r0 + k];
+        if (k < nr) {
+            const uint32_t p = sorted[r0 + k];
+            const short4 rc = ws.rect[p];
+            S.u.e.pos[k] = p;
+            S.u.e.rect[k] = (uint32_t)rc.x | ((uint32_t)rc.y << 8) | ((uint32_t)rc.z << 16);
+        }
     }
     __syncthreads();
-    for (int i = threadIdx.x; i < G; i += blockDim.x) ws.block_sums[i] = s[i];
-}
-
-__global__ void __launch_bounds__(256) k_pairs_scan(Workspace ws, const uint32_t *__restrict__ sorted_pos) {
-    const long long n = ws.counters[CNT_BINNED];
-    const long long c = chunk_size(n, gridDim.x);
-    const long long b0 = (long long)blockIdx.x * c, b1 = min(b0 + c, n);
-    unsigned long long run = ws.block_sums[blockIdx.x];
-    for (long long t0 = b0; t0 < b1; t0 += blockDim.x) {
-        const long long r = t0 + threadIdx.x;
-        const unsigned long long v = r < b1 ? (unsigned long long)ws.tiles[sorted_pos[r]] : 0ull;
-        unsigned long long tot;
-        const unsigned long long ex = block_exclusive_scan<unsigned long long>(v, tot) + run;
-        if (r < b1) ws.poff[r] = ex;
-        run += tot;
+    const uint32_t i0 = base + (uint32_t)tid * IPT;
+    if (i0 < end) {
+        int lo = 0, hi = nr - 1;
+        while (lo < hi) {
+            const int mid = (lo + hi + 1) >> 1;
+            if (S.u.e.off[mid] <= i0) lo = mid; else hi = mid - 1;
+        }
+        uint32_t rc = S.u.e.rect[lo];
+        uint32_t y = (rc >> 16) + (i0 - S.u.e.off[lo]);
+        uint32_t next = S.u.e.off[lo + 1];
+        uint32_t p = S.u.e.pos[lo];
+        const uint32_t stop = min(i0 + (uint32_t)IPT, end);
+        for (uint32_t i = i0; i < stop; i++) {
+            if (i == next) {
+                lo++;
+                rc = S.u.e.rect[lo];
+                y = rc >> 16;
+                next = S.u.e.off[lo + 1];
+                p = S.u.e.pos[lo];
+            }
+            S.gx[i - base] = (rc & 0xffffu) | (y << 16);
+            S.gp[i - base] = p;
+            y++;
+        }
+    }
+    __syncthreads();
+    const int nv = (int)(end - base);
+    uint32_t xk[IPT], pv[IPT], dig[IPT], pos[IPT];
+#pragma unroll
+    for (int r = 0; r < IPT; r++) {
+        const int i = warp * 32 * IPT + r * 32 + lane;
+        dig[r] = NO_DIGIT;
+        if (i < nv) {
+            xk[r] = S.gx[i];
+            pv[r] = S.gp[i];
+            dig[r] = xk[r] >> 16;
+        }
+    }
+    uint32_t count;
+    block_rank(dig, pos, S.rs, count);
+    if (tid < RADIX) {
+        const uint32_t ex =
+            lookback(ws.look_region(kLookRows) + tid, RADIX, t, *ws.epoch * 16u + kLookRows, count, t == 0);
+        S.s_base[tid] = ws.row_start[min(tid, kMaxTileAxis)] + ex - S.rs.start[tid];
+    }
+#pragma unroll
+    for (int r = 0; r < IPT; r++) {
+        if (dig[r] == NO_DIGIT) continue;
+        S.u.g.x[pos[r]] = xk[r];
+        S.u.g.p[pos[r]] = pv[r];
+    }
+    __syncthreads();
+    for (int i = tid; i < nv; i += NT) {
+        const uint32_t x = S.u.g.x[i];
+        const uint32_t dst = S.s_base[x >> 16] + (uint32_t)i;
+        ws.ent_x[dst] = x;
+        ws.ent_p[dst] = S.u.g.p[i];
     }
 }
 
-// bin_tiles emission (preprocess.py:179-189) in depth-rank order, balanced by
-// pairs: pair tile t = [t * kEmitTile, (t + 1) * kEmitTile) starts inside rank
-// tile_r0[t] (found per rank by k_emit_starts, no search).  A block stages
-// the ranks overlapping its tile, and each thread expands 8 consecutive pairs
-// (ty-major, tx-minor inside a splat) with one search and a walk.
-constexpr int kEmitTile = 2048;
-constexpr int kEmitPerThread = kEmitTile / 256;
+// ---- column pass ---------------------------------------------------------------------
 
-__global__ void __launch_bounds__(256) k_emit_starts(Workspace ws) {
-    const long long n = ws.counters[CNT_BINNED];
-    for (long long r = (long long)blockIdx.x * blockDim.x + threadIdx.x; r < n; r += (long long)gridDim.x * blockDim.x) {
-        const unsigned long long a = ws.poff[r], b = ws.poff[r + 1];
-        for (unsigned long long t = (a + kEmitTile - 1) / kEmitTile; t * kEmitTile < b; t++) ws.tile_r0[t] = (uint32_t)r;
+constexpr int kColW = kMaxTileAxis + 1;
+constexpr int kColStage = 16384;  // pairs staged per column group (64 KB + 16 KB)
+
+struct ColSmem {
+    int32_t cnt[NT / 32][kColW];      // per-warp counts -> per-warp staging offsets
+    uint32_t mask[NT / 32][kColW];    // per-round lanes covering each column
+    uint32_t cstart[kColW + 1];       // chunk-local first slot of each column
+    uint32_t gbase[kColW];            // global slot of the chunk's first pair of each column
+    uint32_t stage[kColStage];
+    uint8_t stx[kColStage];
+    uint32_t gfirst[kColW + 1];       // column groups that fit the staging buffer
+    int n_groups;
+    uint32_t row;
+};
+
+// One chunk (<= 4096 entries) of one tile row: expands every entry into its
+// pairs and writes them to their final slots.  Inside the row, the pairs of
+// tile (ty, tx) come from the entries covering tx in entry (= depth-rank)
+// order, so slot = ranges[tile].x + (pairs of tx in earlier chunks of the
+// row: look-back along the row's chunks) + (entries covering tx earlier in
+// this chunk).  The last term: per-warp counts + exclusive scan over warps,
+// and inside a warp round (32 entries) every lane ORs its bit into the lane
+// mask of each column it covers, so its rank at column v is
+// popc(mask_v & lanes_below) -- work proportional to the entry's width.
+// Pairs are staged by column in shared memory and copied out as contiguous
+// runs.
+__global__ void __launch_bounds__(NT, 1) k_col_pass(Workspace ws, int tiles_x, int tiles_y) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    ColSmem &S = *reinterpret_cast<ColSmem *>(smem);
+    const uint32_t C = ws.counters[CNT_CHUNKS];
+    const uint32_t t = take_ticket(&ws.counters[CNT_TICKET + kLookCols]);
+    if (t >= C) return;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    if (tid == 0) {  // row of chunk t: last y with chunk_first[y] <= t
+        int lo = 0, hi = tiles_y - 1;
+        while (lo < hi) {
+            const int mid = (lo + hi + 1) >> 1;
+            if (ws.chunk_first[mid] <= t) lo = mid; else hi = mid - 1;
+        }
+        S.row = (uint32_t)lo;
     }
-}
-
-__global__ void __launch_bounds__(256) k_emit(Workspace ws, const uint32_t *__restrict__ sorted_pos, int tiles_x,
-                                              uint32_t *__restrict__ pkey, uint32_t *__restrict__ pval) {
-    __shared__ unsigned long long s_off[kEmitTile + 2];
-    __shared__ uint32_t s_pos[kEmitTile + 1];
-    __shared__ short4 s_rc[kEmitTile + 1];
-    if (ws.counters[CNT_OVERFLOW]) return;
-    const long long n = ws.counters[CNT_BINNED];
-    const unsigned long long k_total = ws.counters[CNT_PAIRS];
-    const unsigned long long n_tiles = (k_total + kEmitTile - 1) / kEmitTile;
-    for (unsigned long long t = blockIdx.x; t < n_tiles; t += gridDim.x) {
-        const unsigned long long base = t * kEmitTile, end = min(base + kEmitTile, k_total);
-        const long long r0 = ws.tile_r0[t];
-        const long long r1 = t + 1 < n_tiles ? (long long)ws.tile_r0[t + 1] : n - 1;  // last rank overlapping
-        const int nr = (int)(r1 - r0 + 1);
-        for (int k = threadIdx.x; k <= nr; k += blockDim.x) {
-            s_off[k] = ws.poff[r0 + k];
-            if (k < nr) {
-                const uint32_t p = sorted_pos[r0 + k];
-                s_pos[k] = p;
-                s_rc[k] = ws.rect[p];
+    for (int i = lane; i < kColW; i += 32) {
+        S.cnt[warp][i] = 0;
+        S.mask[warp][i] = 0u;
+    }
+    __syncthreads();
+    const int ty = (int)S.row;
+    const uint32_t k = t - ws.chunk_first[ty];
+    const uint32_t s = ws.row_start[ty] + k * TILE, e = min(s + (uint32_t)TILE, ws.row_start[ty + 1]);
+    uint32_t x0[IPT], x1[IPT], pv[IPT];
+    const uint32_t wb = s + (uint32_t)(warp * 32 * IPT) + lane;
+#pragma unroll
+    for (int r = 0; r < IPT; r++) {
+        const uint32_t i = min(wb + r * 32, e - 1);
+        const uint32_t x = ws.ent_x[i];
+        pv[r] = ws.ent_p[i];
+        const bool valid = wb + r * 32 < e;
+        x0[r] = valid ? (x & 0xffu) : 1u;  // absent: empty interval [1, 0]
+        x1[r] = valid ? ((x >> 8) & 0xffu) : 0u;
+    }
+#pragma unroll
+    for (int r = 0; r < IPT; r++) {
+        if (x0[r] > x1[r]) continue;
+        atomicAdd(&S.cnt[warp][x0[r]], 1);
+        atomicAdd(&S.cnt[warp][x1[r] + 1], -1);
+    }
+    __syncwarp();
+    constexpr int PER = (kColW + 31) / 32;  // columns per lane in warp-wide scans
+    {
+        int32_t v[PER], run = 0;
+#pragma unroll
+        for (int j = 0; j < PER; j++) {
+            const int c = lane * PER + j;
+            v[j] = c < kColW ? S.cnt[warp][c] : 0;
+            run += v[j];
+        }
+        int32_t incl = run;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += y;
+        }
+        int32_t acc = incl - run;
+#pragma unroll
+        for (int j = 0; j < PER; j++) {
+            const int c = lane * PER + j;
+            acc += v[j];
+            if (c < kColW) S.cnt[warp][c] = acc;
+        }
+    }
+    __syncthreads();
+    uint32_t tot = 0;
+    if (tid < kColW) {
+#pragma unroll
+        for (int w = 0; w < NT / 32; w++) {
+            const int32_t c = S.cnt[w][tid];
+            S.cnt[w][tid] = (int32_t)tot;
+            tot += (uint32_t)c;
+        }
+    }
+    uint32_t chunk_total;
+    const uint32_t cs = block_scan<uint32_t>(tid < tiles_x ? tot : 0u, chunk_total);
+    if (tid < tiles_x) {
+        S.cstart[tid] = cs;
+        const uint32_t ex = lookback(ws.look_region(kLookCols) + tid, RADIX, t, *ws.epoch * 16u + kLookCols, tot,
+                                     k == 0);
+        S.gbase[tid] = ws.ranges[ty * tiles_x + tid].x + ex;
+#pragma unroll
+        for (int w = 0; w < NT / 32; w++) S.cnt[w][tid] += (int32_t)cs;  // chunk-local staging offsets
+    }
+    if (tid == 0) S.cstart[tiles_x] = chunk_total;
+    __syncthreads();
+    if (tid == 0) {
+        int g = 0;
+        S.gfirst[0] = 0;
+        if (chunk_total > (uint32_t)kColStage) {  // rare: greedy column groups that fit the staging buffer
+            uint32_t gs = 0;
+            for (int c = 0; c < tiles_x; c++) {
+                if (S.cstart[c + 1] - gs > (uint32_t)kColStage) {
+                    S.gfirst[++g] = (uint32_t)c;
+                    gs = S.cstart[c];
+                }
             }
         }
+        S.gfirst[++g] = (uint32_t)tiles_x;
+        S.n_groups = g;
+    }
+    __syncthreads();
+    const unsigned lt = (1u << lane) - 1u;
+    for (int grp = 0; grp < S.n_groups; grp++) {
+        const uint32_t ca = S.gfirst[grp], cb = S.gfirst[grp + 1];
+        const uint32_t sbase = S.cstart[ca];
+#pragma unroll 1
+        for (int r = 0; r < IPT; r++) {
+            // columns of this entry inside the current group
+            const uint32_t a = max(x0[r], ca), b = min(x1[r] + 1u, cb);  // [a, b)
+            for (uint32_t v = a; v < b; v++) atomicOr(&S.mask[warp][v], 1u << lane);
+            __syncwarp();
+            for (uint32_t v = a; v < b; v++) {
+                const uint32_t m = S.mask[warp][v];
+                const uint32_t slot = (uint32_t)S.cnt[warp][v] + __popc(m & lt) - sbase;
+                S.stage[slot] = pv[r];
+                S.stx[slot] = (uint8_t)v;
+            }
+            __syncwarp();
+            for (uint32_t v = a; v < b; v++) {  // the highest covering lane advances the column
+                const uint32_t m = S.mask[warp][v];
+                if ((m >> lane) == 1u) {
+                    S.cnt[warp][v] += __popc(m);
+                    S.mask[warp][v] = 0u;
+                }
+            }
+            __syncwarp();
+        }
         __syncthreads();
-        const unsigned long long i0 = base + (unsigned long long)threadIdx.x * kEmitPerThread;
-        if (i0 < end) {
-            int lo = 0, hi = nr - 1;  // rank holding pair i0
-            while (lo < hi) {
-                const int mid = (lo + hi + 1) >> 1;
-                if (s_off[mid] <= i0) lo = mid; else hi = mid - 1;
-            }
-            short4 rc = s_rc[lo];
-            int w = rc.y - rc.x + 1;
-            const int local = (int)(i0 - s_off[lo]);
-            int ty = rc.z + local / w;
-            int tx = rc.x + local % w;
-            unsigned long long next = s_off[lo + 1];
-            uint32_t p = s_pos[lo];
-            const unsigned long long stop = min(i0 + kEmitPerThread, end);
-            for (unsigned long long i = i0; i < stop; i++) {
-                if (i == next) {  // next splat
-                    lo++;
-                    rc = s_rc[lo];
-                    w = rc.y - rc.x + 1;
-                    ty = rc.z;
-                    tx = rc.x;
-                    next = s_off[lo + 1];
-                    p = s_pos[lo];
-                }
-                pkey[i] = (uint32_t)(ty * tiles_x + tx);
-                pval[i] = p;
-                if (++tx > rc.y) {
-                    tx = rc.x;
-                    ty++;
-                }
-            }
+        const uint32_t n_stage = S.cstart[cb] - sbase;
+        for (uint32_t i = tid; i < n_stage; i += NT) {
+            const uint32_t v = S.stx[i];
+            ws.pfinal[S.gbase[v] + (i + sbase - S.cstart[v])] = S.stage[i];
         }
         __syncthreads();
     }
 }
 
-// ---- 5. ranges --------------------------------------------------------------------
-
-__global__ void k_clear_ranges(uint2 *ranges, int n_tiles) {
-    for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < n_tiles; t += gridDim.x * blockDim.x)
-        ranges[t] = make_uint2(0u, 0u);
-}
-
-__global__ void __launch_bounds__(256) k_ranges(Workspace ws, const uint32_t *__restrict__ pkey) {
-    const long long k = ws.counters[CNT_PAIRS];
-    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < k; i += (long long)gridDim.x * blockDim.x) {
-        const uint32_t t = pkey[i];
-        if (i == 0 || pkey[i - 1] != t) ws.ranges[t].x = (uint32_t)i;
-        if (i == k - 1 || pkey[i + 1] != t) ws.ranges[t].y = (uint32_t)(i + 1);
+__global__ void k_fill_pair_tiles(const uint2 *ranges, int n_tiles, int32_t *pair_tile) {
+    for (int t = blockIdx.x; t < n_tiles; t += gridDim.x) {
+        const uint2 r = ranges[t];
+        for (uint32_t i = r.x + threadIdx.x; i < r.y; i += blockDim.x) pair_tile[i] = t;
     }
-}
-
-}  // namespace
-
-int chunk_grid(int sms) {
-    int g = 4 * sms;
-    return g > kChunkBlocksMax ? kChunkBlocksMax : g;
 }
 
 int key_bits(int n) {
-    int b = 1;
+    int b = 0;
     while ((1 << b) < n) b++;
     return b;
 }
 
-// Which ping-pong buffer holds the sorted pairs (seele_plan_export).
-int pair_buffer(int n_tiles) { return ((key_bits(n_tiles) + 7) / 8) & 1; }
-
-void launch_depth_rank(const Workspace &ws, long long n_max, int grid, int64_t *stats, uint32_t **sorted_pos,
-                       cudaStream_t st) {
-    (void)stats;
-    const int G = grid;
-    k_compact_reduce<<<G, 256, 0, st>>>(ws);
-    k_compact_sums<<<1, 1024, 0, st>>>(ws, G);
-    k_compact_write<<<G, 256, 0, st>>>(ws);
-    note_launches(3);
-    uint64_t *k[2] = {ws.dkey[0], ws.dkey[1]};
-    uint32_t *v[2] = {ws.dval[0], ws.dval[1]};
-    // positive doubles order like their bit patterns; bit 63 (sign) is always 0
-    (void)n_max;
-    const int Gd = G;
-    const int cur = radix_sort<uint64_t>(k, v, ws.counters + CNT_BINNED, 0, 63, ws.hist, ws.hist + 256LL * kChunkBlocksMax,
-                                         Gd, st);
-    *sorted_pos = v[cur];
+template <typename K>
+void set_smem(K kernel, size_t bytes) {
+    static bool done = false;  // per instantiation
+    if (!done) {
+        cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+        done = true;
+    }
 }
 
-void launch_binning(const Workspace &ws, const uint32_t *sorted_pos, long long n_max, long long cap, const CamK &cam,
-                    int grid, int64_t *stats, uint32_t **pair_pos, uint32_t **pair_tile, cudaStream_t st) {
-    (void)n_max;
-    const int G = grid;
-    k_pairs_reduce<<<G, 256, 0, st>>>(ws, sorted_pos);
-    k_pairs_sums<<<1, 1024, 0, st>>>(ws, G, cap, stats);
-    k_pairs_scan<<<G, 256, 0, st>>>(ws, sorted_pos);
-    k_emit_starts<<<G, 256, 0, st>>>(ws);
-    k_emit<<<G, 256, 0, st>>>(ws, sorted_pos, cam.tiles_x, ws.pkey[0], ws.pval[0]);
-    note_launches(5);
-    const int n_tiles = cam.tiles_x * cam.tiles_y;
-    uint32_t *k[2] = {ws.pkey[0], ws.pkey[1]};
-    uint32_t *v[2] = {ws.pval[0], ws.pval[1]};
-    const int cur = radix_sort<uint32_t>(k, v, ws.counters + CNT_PAIRS, 0, key_bits(n_tiles), ws.hist,
-                                         ws.hist + 256LL * kChunkBlocksMax, G, st);
-    k_clear_ranges<<<(n_tiles + 255) / 256, 256, 0, st>>>(ws.ranges, n_tiles);
-    k_ranges<<<G, 256, 0, st>>>(ws, k[cur]);
-    note_launches(2);
-    *pair_pos = v[cur];
-    *pair_tile = k[cur];
+long long ceil_div(long long a, long long b) { return (a + b - 1) / b; }
+
+}  // namespace
+
+void launch_frame_begin(const Workspace &ws, const CamK &cam, int64_t *stats, cudaStream_t st) {
+    const int n_diff = (cam.tiles_x + 1) * (cam.tiles_y + 1);
+    int grid = (n_diff + 255) / 256;
+    grid = grid < 8 ? 8 : (grid > 256 ? 256 : grid);
+    k_frame_begin<<<grid, 256, 0, st>>>(ws, stats, n_diff, cam.tiles_y);
+    note_launches(1);
+}
+
+void launch_depth_sort(const Workspace &ws, long long n_max, int64_t *stats, cudaStream_t st) {
+    const int hist_grid = (int)std::min<long long>(ceil_div(n_max, 256 * 8), 4 * 148);
+    k_depth_hist<<<hist_grid > 0 ? hist_grid : 1, 256, 0, st>>>(ws);
+    const size_t smem = sizeof(RankSmem) + 2 * sizeof(uint32_t) * TILE;
+    set_smem(k_depth_pass, smem);
+    const int grid = (int)ceil_div(n_max, TILE);
+    for (int p = 0; p < kDepthPasses; p++) k_depth_pass<<<grid, NT, smem, st>>>(ws, p);
+    const int fix_grid = (int)ceil_div(n_max, 256 * 8);
+    k_depth_fixup<<<fix_grid > 0 ? fix_grid : 1, 256, 0, st>>>(ws, stats);
+    k_depth_fix_long<<<64, 512, 0, st>>>(ws);
+    note_launches(3 + kDepthPasses);
+}
+
+void launch_binning(const Workspace &ws, long long n_max, long long cap, const CamK &cam, int64_t *stats,
+                    cudaStream_t st) {
+    static int sms = 0;
+    if (!sms) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        if (sms <= 0) sms = 148;
+    }
+    const size_t diff_bytes = sizeof(int32_t) * (cam.tiles_x + 1) * (cam.tiles_y + 1);
+    const int use_smem = diff_bytes <= 160 * 1024;
+    const size_t scan_smem = use_smem ? diff_bytes : 0;
+    set_smem(k_pair_scan, 160 * 1024);
+    const int scan_grid = (int)std::min<long long>(ceil_div(n_max, TILE), 2 * sms);
+    k_pair_scan<<<scan_grid > 0 ? scan_grid : 1, NT, scan_smem, st>>>(ws, cam.tiles_x, cam.tiles_y, cap, use_smem,
+                                                                      stats);
+    set_smem(k_row_pass, sizeof(RowSmem));
+    k_row_pass<<<(int)ceil_div(cap, TILE), NT, sizeof(RowSmem), st>>>(ws, stats);
+    set_smem(k_col_pass, sizeof(ColSmem));
+    k_col_pass<<<(int)(ceil_div(cap, TILE) + cam.tiles_y), NT, sizeof(ColSmem), st>>>(ws, cam.tiles_x, cam.tiles_y);
+    note_launches(3);
+}
+
+#ifdef SEELE_SORT_TRACE
+void debug_trace(void *dst) { cudaMemcpyFromSymbol(dst, g_trace, sizeof(g_trace)); }
+#endif
+
+void launch_fill_pair_tiles(const uint2 *ranges, int n_tiles, int32_t *pair_tile, cudaStream_t st) {
+    k_fill_pair_tiles<<<n_tiles < 4096 ? n_tiles : 4096, 256, 0, st>>>(ranges, n_tiles, pair_tile);
+    note_launches(1);
 }
 
 }  // namespace seele

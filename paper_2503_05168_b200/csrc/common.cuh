@@ -11,8 +11,6 @@ constexpr int kTile = 16;            // TILE_SIZE (model.py:17)
 constexpr int kTilePixels = 256;
 constexpr int kWarp = 32;            // WARP_SIZE (rasterize.py:30)
 constexpr double kAlphaClamp = 0.99; // ALPHA_CLAMP (rasterize.py:32)
-constexpr int kChunkBlocksMax = 2048;  // upper bound of the chunked scan / sort grid
-constexpr int kSortBlock = 256;
 
 // Per-frame camera constants, computed once on the host in fp64 exactly as
 // CameraPose.focal / principal_point / rotation_matrix do (model.py:170-184).
@@ -37,18 +35,39 @@ struct SceneK {
     long long plane_stride;
 };
 
-// Scalar counters living in the workspace (device).
+// Scalar counters living in the workspace (device), zeroed by every frame.
 enum {
-    CNT_WS = 0,      // assembled splats
-    CNT_BINNED = 1,  // splats with >= 1 tile
-    CNT_PAIRS = 2,   // tile pairs (0 on overflow; the u64 count is in stats)
+    CNT_WS = 0,           // assembled splats
+    CNT_ENTRIES = 1,      // row entries (one per binned splat and tile row it covers)
+    CNT_PAIRS = 2,        // tile pairs (0 on overflow; the u64 count is in stats)
     CNT_OVERFLOW = 3,
-    CNT_COUNT = 8
+    CNT_LONG_RUNS = 4,    // equal depth-key runs queued for the CTA fix-up
+    CNT_DONE_HIST = 5,    // last-block tickets
+    CNT_DONE_SCAN = 6,
+    CNT_CHUNKS = 7,       // row chunks of the column pass
+    CNT_TICKET = 8,       // 16 per-pass tile tickets
+    CNT_COUNT = 32
 };
+
+#ifndef SEELE_SORT_NT
+#define SEELE_SORT_NT 512
+#endif
+#ifndef SEELE_SORT_IPT
+#define SEELE_SORT_IPT 8
+#endif
+constexpr int kSortTile = SEELE_SORT_NT * SEELE_SORT_IPT;  // items per onesweep CTA tile (onesweep.cuh TILE)
+constexpr int kDepthPasses = 3;   // 8-bit passes of the 24-bit depth key
+constexpr int kDepthFinal = (kDepthPasses - 1) & 1;  // ping-pong buffer holding the sorted order
+constexpr int kLongRunsMax = 4096; // equal-key runs longer than this many go to the CTA fix-up
+constexpr int kMaxTileAxis = 256;  // tiles per image axis (row / column digits fit one pass)
+constexpr int kLookDepth = 0;     // look-back regions (pass ids)
+constexpr int kLookScan = 3;
+constexpr int kLookRows = 4;
+constexpr int kLookCols = 5;
 
 // Workspace carve-up; identical on every call for the same (n_max, cap, w, h).
 struct Workspace {
-    // per assembled splat
+    // per assembled splat (preprocess)
     uint8_t *status;
     double *depth;
     uint32_t *tiles;
@@ -56,23 +75,42 @@ struct Workspace {
     double2 *mean;
     double4 *conic_op;   // (a, b, c, opacity)
     float4 *color;       // (r, g, b, 0)
-    float4 *fast;        // FAST raster: (q_lo, q_hi, opacity32, 0) alpha-test bracket in q
-    // compaction + depth rank
-    uint64_t *dkey[2];
+    float4 *fast;        // FAST raster: (q_lo, q_hi, opacity32, 1 - opacity)
+    // depth sort (ping-pong): key = depth quantised monotonically to 24 bits,
+    // value = assembled position; the sorted order ends in dkey/dval[kDepthFinal]
+    uint32_t *dkey[2];
     uint32_t *dval[2];
-    // first pair of each depth-ranked splat (+ total); u64 to detect overflow
-    unsigned long long *poff;
-    uint32_t *tile_r0;   // first rank of each 2048-pair emission tile
-    // pairs
-    uint32_t *pkey[2];
-    uint32_t *pval[2];
-    uint2 *ranges;
-    // scan / sort scratch
-    unsigned long long *block_sums;  // kChunkBlocksMax + 1
-    uint32_t *hist;                  // 256 * kChunkBlocksMax
-    uint32_t *counters;              // CNT_COUNT
-    unsigned long long *pairs64;     // total tile pairs (u64)
+    uint2 *long_runs;    // [kLongRunsMax] (start, length) of long equal-key runs
+    // first row entry of each depth-ranked binned splat (+ sentinel) and first
+    // rank of each 4096-entry tile of the row pass
+    uint32_t *poff;
+    uint32_t *tile_r0;
+    // row entries grouped by tile row (row pass output): packed x0 | x1 << 8 |
+    // ty << 16, and the splat's assembled position
+    uint32_t *ent_x;
+    uint32_t *ent_p;
+    uint32_t *pfinal;    // sorted pair -> assembled position (sort_intersections order)
+    uint2 *ranges;       // per tile [start, end)
+    // scratch
+    unsigned long long *look;  // epoch-tagged look-back status words
+    long long look_tiles_d, look_tiles_p;  // tiles per depth / pair pass region
+    uint32_t *dhist;     // [kDepthPasses][256] digit totals -> exclusive offsets
+    uint32_t *row_start; // [kMaxTileAxis + 1] first entry of each tile row
+    uint32_t *chunk_first;  // [kMaxTileAxis + 1] first column-pass chunk of each row
+    int32_t *tile_diff;  // [(tiles_y + 1) x (tiles_x + 1)] 2D difference array of tile counts
+    int32_t *row_diff;   // [tiles_y + 1] entries per row (difference array)
+    unsigned long long *minmax;  // min / max fp64 bits of binned depths
+    uint32_t *counters;  // CNT_COUNT
+    uint32_t *epoch;     // frame epoch (never cleared)
+    unsigned long long *pairs64;  // total tile pairs (u64)
     size_t bytes;
+
+    __device__ __forceinline__ unsigned long long *look_region(int pass) const {
+        if (pass < kLookScan) return look + (size_t)pass * look_tiles_d * 256;
+        if (pass == kLookScan) return look + (size_t)kDepthPasses * look_tiles_d * 256;
+        return look + (size_t)kDepthPasses * look_tiles_d * 256 + look_tiles_d +
+               (size_t)(pass - kLookRows) * look_tiles_p * 256;
+    }
 };
 
 Workspace carve_workspace(void *base, long long n_max, long long cap, int width, int height);
@@ -84,13 +122,13 @@ void launch_preprocess(const SceneK &s, const int64_t *ranges, int n_ranges, con
 void launch_select(const CamK &cam, const double *centroids, int n, int m, double beta,
                    const double *mean3, double scale, const int64_t *chunks, int32_t *out_ids,
                    int64_t *ranges_out, cudaStream_t st);
-// compaction of binned splats in assembled order + stable depth sort.
-// Returns pointers (inside ws) of the depth-sorted positions via *sorted_pos.
-void launch_depth_rank(const Workspace &ws, long long n_max, int grid, int64_t *stats,
-                       uint32_t **sorted_pos, cudaStream_t st);
-void launch_binning(const Workspace &ws, const uint32_t *sorted_pos, long long n_max, long long cap,
-                    const CamK &cam, int grid, int64_t *stats, uint32_t **pair_pos,
-                    uint32_t **pair_tile, cudaStream_t st);
+// frame start: counters, stats, epoch, range / histogram init (binning.cu)
+void launch_frame_begin(const Workspace &ws, const CamK &cam, int64_t *stats, cudaStream_t st);
+// stable depth sort of the assembled splats (binned first, by (depth, position)).
+void launch_depth_sort(const Workspace &ws, long long n_max, int64_t *stats, cudaStream_t st);
+// pair offsets, emission + tile sort, ranges; final pair -> position in ws.pfinal.
+void launch_binning(const Workspace &ws, long long n_max, long long cap, const CamK &cam, int64_t *stats,
+                    cudaStream_t st);
 void launch_raster(const Workspace &ws, const uint32_t *pair_pos, const CamK &cam,
                    const CfgK &cfg, float *image, int32_t *contrib, int64_t *stats,
                    cudaStream_t st);
@@ -99,9 +137,8 @@ void launch_raster_fast(int W, const Workspace &ws, const uint32_t *pair_pos, co
                         const CfgK &cfg, float *image, int32_t *contrib, int64_t *stats,
                         cudaStream_t st);
 
-// grid of the chunked scan / sort kernels (binning.cu)
-int chunk_grid(int sms);
-int pair_buffer(int n_tiles);      // ping-pong buffer holding the sorted pairs
+
+void launch_fill_pair_tiles(const uint2 *ranges, int n_tiles, int32_t *pair_tile, cudaStream_t st);
 
 // Counts kernels this library has launched (seele_launch_count, api.cu).
 void note_launches(int n);

@@ -126,9 +126,45 @@ __device__ __forceinline__ void load_splat(const SceneK &sc, long long i, int sh
     normalize4(g.q);  // Gaussian3D.__post_init__ (model.py:122, 76-80)
 }
 
-__device__ __forceinline__ void warp_count_add(int64_t *dst, int pred) {
-    unsigned b = __ballot_sync(0xffffffffu, pred);
-    if ((threadIdx.x & 31) == 0 && b) atomicAdd((unsigned long long *)dst, (unsigned long long)__popc(b));
+// Block-level reduction of the per-thread frame counters and of the min / max
+// fp64 bit pattern of binned depths (the depth sort's key range): one atomic
+// per counter per CTA instead of one per warp and iteration.
+__device__ __forceinline__ void flush_block(const Workspace &ws, int64_t *stats, uint32_t (&c)[4],
+                                            unsigned long long kmin, unsigned long long kmax) {
+    __shared__ uint32_t s_c[4];
+    __shared__ unsigned long long s_min, s_max;
+    if (threadIdx.x < 4) s_c[threadIdx.x] = 0u;
+    if (threadIdx.x == 0) {
+        s_min = ~0ull;
+        s_max = 0ull;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < 4; k++) {
+        const uint32_t v = __reduce_add_sync(0xffffffffu, c[k]);
+        if ((threadIdx.x & 31) == 0 && v) atomicAdd(&s_c[k], v);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        kmin = min(kmin, __shfl_xor_sync(0xffffffffu, kmin, o));
+        kmax = max(kmax, __shfl_xor_sync(0xffffffffu, kmax, o));
+    }
+    if ((threadIdx.x & 31) == 0) {
+        atomicMin(&s_min, kmin);
+        atomicMax(&s_max, kmax);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        unsigned long long *st = (unsigned long long *)stats;
+        if (s_c[0]) atomicAdd(st + SEELE_STAT_CULLED_NEAR, (unsigned long long)s_c[0]);
+        if (s_c[1]) atomicAdd(st + SEELE_STAT_DROPPED_DEGENERATE, (unsigned long long)s_c[1]);
+        if (s_c[2]) atomicAdd(st + SEELE_STAT_PROJECTED, (unsigned long long)s_c[2]);
+        if (s_c[3]) atomicAdd(st + SEELE_STAT_BINNED, (unsigned long long)s_c[3]);
+        if (s_min <= s_max) {
+            atomicMin(&ws.minmax[0], s_min);
+            atomicMax(&ws.minmax[1], s_max);
+        }
+    }
 }
 
 template <int LAYOUT>
@@ -153,13 +189,13 @@ __global__ void __launch_bounds__(256, 3) k_preprocess(SceneK sc, const int64_t 
     const long long n_ws = s_prefix[n_ranges];
     const int sh_planes = cfg.sh_degree >= 3 ? 4 : (cfg.sh_degree == 2 ? 3 : 1);
     const long long stride = (long long)gridDim.x * blockDim.x;
-    const long long n_iter = (n_ws + stride - 1) / stride;  // uniform trip count for the warp votes
-    for (long long it = 0; it < n_iter; it++) {
-        const long long p = it * stride + (long long)blockIdx.x * blockDim.x + threadIdx.x;
-        const bool active = p < n_ws;
-        int status = 3;  // 3 = inactive lane
+    uint32_t cnt[4] = {0u, 0u, 0u, 0u};
+    unsigned long long kmin = ~0ull, kmax = 0ull;
+    for (long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x; p < n_ws; p += stride) {
+        int status = 3;
         uint32_t n_tiles = 0;
-        if (active) {
+        unsigned long long zbits = 0ull;
+        {
             int r = 0;
             while (r + 1 < n_ranges && s_prefix[r + 1] <= p) r++;
             const long long i = s_start[r] + (p - s_prefix[r]);
@@ -258,6 +294,7 @@ __global__ void __launch_bounds__(256, 3) k_preprocess(SceneK sc, const int64_t 
                         }
                     }
                     ws.depth[p] = z;
+                    zbits = (unsigned long long)__double_as_longlong(z);
                     ws.mean[p] = make_double2(m0, m1);
                     ws.conic_op[p] = make_double4(ca, cb, cc, g.o);
                     ws.color[p] = col;
@@ -281,11 +318,16 @@ __global__ void __launch_bounds__(256, 3) k_preprocess(SceneK sc, const int64_t 
             ws.rect[p] = rect;
             ws.tiles[p] = n_tiles;
         }
-        warp_count_add(stats + SEELE_STAT_CULLED_NEAR, status == 1);
-        warp_count_add(stats + SEELE_STAT_DROPPED_DEGENERATE, status == 2);
-        warp_count_add(stats + SEELE_STAT_PROJECTED, status == 0);
-        warp_count_add(stats + SEELE_STAT_BINNED, n_tiles > 0);
+        cnt[0] += status == 1;
+        cnt[1] += status == 2;
+        cnt[2] += status == 0;
+        if (n_tiles > 0) {
+            cnt[3] += 1u;
+            kmin = zbits < kmin ? zbits : kmin;
+            kmax = zbits > kmax ? zbits : kmax;
+        }
     }
+    flush_block(ws, stats, cnt, kmin, kmax);
 }
 
 // K0: select_clusters (residency.py:38-54) with pose_feature (compiler.py:113-121).

@@ -205,7 +205,7 @@ class FrameRenderer:
         nbytes = int(self.lib.seele_workspace_bytes(n_max, cap, int(width), int(height)))
         self.workspace = None
         torch.cuda.empty_cache()
-        self.workspace = torch.empty(nbytes, dtype=torch.uint8, device=self.device)
+        self.workspace = torch.zeros(nbytes, dtype=torch.uint8, device=self.device)  # look-back words must start zeroed
         self.n_max, self.pair_capacity, self.size = n_max, cap, (int(width), int(height))
 
     def render(self, scene: DeviceScene, cam: CameraPose, cfg: EngineConfig, *, ranges: torch.Tensor | None = None,
