@@ -342,8 +342,9 @@ def run_ours(args):
             "stages": stages,
             "work": {"working_set": int(n_ws), "binned": int(binned), "tile_pairs": int(pairs),
                      "live_pixel_steps": int(live), "blends": int(blends),
-                     "fixup_warps": int(ctr[_native.STAT_FIXUP_WARPS]),
-                     "alpha_redecide": int(ctr[_native.STAT_ALPHA_REDECIDE])},
+                     "skipped_pixel_steps": int(ctr[_native.STAT_SKIPPED_PIXEL_STEPS]),
+                     "alpha_redecide": int(ctr[_native.STAT_ALPHA_REDECIDE]),
+                     "t_ambiguous": int(ctr[_native.STAT_T_AMBIGUOUS])},
             "e2e": {"value": e2e_value, "unit": "frames/s", "h2d_bytes_per_step": 96, "d2h_bytes_per_step": d2h,
                     "api": "ResidentRenderer.render_frame(cam, cfg, output='numpy32')"},
             "gpu_launches": int(launches),

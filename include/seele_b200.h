@@ -116,7 +116,7 @@ enum {
     SEELE_STAT_BINNED = 8,      /* splats with >= 1 tile */
     SEELE_STAT_WORKING_SET = 9, /* assembled splat count */
     SEELE_STAT_OVERFLOW = 10,   /* 1 if tile pairs exceeded the workspace capacity */
-    SEELE_STAT_FIXUP_WARPS = 11,/* reserved (0) */
+    SEELE_STAT_SKIPPED_PIXEL_STEPS = 11, /* fast path: live (pixel, splat) steps skipped by the warp-region test */
     SEELE_STAT_ALPHA_REDECIDE = 12, /* fast path: lane alpha tests re-decided in fp64 */
     SEELE_STAT_T_AMBIGUOUS = 13,    /* fast path: pixel T < gamma tests decided by exact fp64 recomputation */
     SEELE_STAT_LIVE_PIXEL_STEPS = 14, /* fast path: (live pixel, iterated splat) pairs */

@@ -27,7 +27,7 @@ STAT_PROJECTED = 7
 STAT_BINNED = 8
 STAT_WORKING_SET = 9
 STAT_OVERFLOW = 10
-STAT_FIXUP_WARPS = 11
+STAT_SKIPPED_PIXEL_STEPS = 11
 STAT_ALPHA_REDECIDE = 12
 STAT_T_AMBIGUOUS = 13
 STAT_LIVE_PIXEL_STEPS = 14

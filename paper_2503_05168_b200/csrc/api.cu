@@ -136,7 +136,9 @@ Workspace carve_workspace(void *base, long long n_max, long long cap, int width,
     w.mean = c.take<double2>(n);
     w.conic_op = c.take<double4>(n);
     w.color = c.take<float4>(n);
-    w.fast = c.take<float4>(n);
+    w.rc = c.take<float4>(n);
+    w.rq = c.take<float4>(n);
+    w.bbox = c.take<float4>(n);
     w.dkey[0] = c.take<uint32_t>(n);
     w.dkey[1] = c.take<uint32_t>(n);
     w.long_runs = c.take<uint2>(kLongRunsMax);

@@ -74,8 +74,11 @@ struct Workspace {
     short4 *rect;
     double2 *mean;
     double4 *conic_op;   // (a, b, c, opacity)
-    float4 *color;       // (r, g, b, 0)
-    float4 *fast;        // FAST raster: (q_lo, q_hi, opacity32, 1 - opacity)
+    float4 *color;       // (r, g, b, 1 - opacity)
+    // FAST raster records (raster_fast.cu); q' = q log2(e) / 2 so alpha = o 2^-q'
+    float4 *rc;          // (l11, l21, l22, opacity): Cholesky factor of the conic in q' units, fp32
+    float4 *rq;          // (q_lo', q_hi', e0, e1): alpha-test bracket, alpha error |da/a| <= e0 + e1 q'
+    float4 *bbox;        // (x_min, x_max, y_min, y_max) of {q' <= q_hi'} in pixel coordinates
     // depth sort (ping-pong): key = depth quantised monotonically to 24 bits,
     // value = assembled position; the sorted order ends in dkey/dval[kDepthFinal]
     uint32_t *dkey[2];

@@ -126,6 +126,68 @@ __device__ __forceinline__ void load_splat(const SceneK &sc, long long i, int sh
     normalize4(g.q);  // Gaussian3D.__post_init__ (model.py:122, 76-80)
 }
 
+// FAST raster record of one projected splat (raster_fast.cu), fp64 here.
+//
+// The raster evaluates q' = k q, k = log2(e) / 2, in fp32 in Cholesky form
+// q' = (l11 dx + l21 dy)^2 + (l22 dy)^2, with (l11, l21, l22) = fl32 of the
+// factor of k C (C = conic), and the tile-relative mean as a hi + lo float
+// pair:  dx = fl(fl(px - mx_hi) - mx_lo), dx1 = fl(dx + 1),
+// u1 = fma(l11, dx, fl(l21 dy)), q' = fma(u1, u1, fl(fl(l22 dy)^2)).
+// With u = 2^-24, P = sqrt(trace(k C)) and |d| the pixel-to-mean distance:
+// |eta_dx|, |eta_dy| <= 3u (|d| + 1) and the coefficient / product roundings
+// give |q'32 - q'| <= 2u (5|d| + 3) P sqrt(q') + 4u q'.  With |d|^2 <=
+// q' / lmin' this is <= u q' (4 + 10 sqrt(tr / lmin)) + 6u P sqrt(q'),
+// linearised around the threshold (sqrt(x) <= (s + x / s) / 2, s^2 = q_th')
+// and taken with a 1.25 safety factor: |q'32 - q'| <= e0q + e1q q'.  No
+// cancellation in the sum of squares: the error grows like sqrt(kappa), not
+// kappa (the direct a dx^2 + 2b dx dy + c dy^2 form).
+// The alpha-test bracket [q_lo', q_hi'] widens q_th' = k 2 ln(o / theta)
+// (rasterize.py:146-151, 209: alpha >= theta <=> q <= q_th) by that bound,
+// the fp64-vs-numpy evaluation difference (1e-15 kappa) and two roundings.
+// The alpha relative error model adds ex2.approx (2^-21.5), the rounding of o
+// and of o e, and ln 2 times the q' error: e0 = 4.7e-7 + ln2 e0q, e1 = ln2 e1q.
+// bbox = axis-aligned box of {q' <= q_hi'}; the raster refines it with the
+// exact minimum of q' over each warp's pixel rectangle.
+__device__ __forceinline__ void write_raster_record(const Workspace &ws, long long p, double m0, double m1, double ca,
+                                                    double cb, double cc, double o, double theta) {
+    const double K = 0.72134752044448170368;  // log2(e) / 2
+    const double u = 5.9604644775390625e-08;  // 2^-24
+    const double qth = 2.0 * log(o / theta);
+    const double tr = ca + cc, disc = sqrt(0.25 * (ca - cc) * (ca - cc) + cb * cb);
+    const double lmin = fmax(0.5 * tr - disc, 1e-300);
+    const double det = ca * cc - cb * cb;
+    float4 rq = make_float4(-INFINITY, -INFINITY, 0.f, 0.f);
+    float4 bb = make_float4(INFINITY, -INFINITY, INFINITY, -INFINITY);
+    if (qth >= 0.0) {
+        const double qt = K * qth;
+        const double P = sqrt(K * tr);
+        const double sq = fmax(sqrt(qt), 1e-3);
+        const double e0q = 1.25 * 3.0 * u * P * sq;
+        const double e1q = 1.25 * (u * (4.0 + 10.0 * sqrt(tr / lmin)) + 3.0 * u * P / sq);
+        const double delta = e0q + e1q * qt + qt * (1e-15 * 2.0 * tr / lmin + 2.0 * u) + 1e-30;
+        rq.x = __double2float_rd(qt - delta);
+        rq.y = delta < 1e6 ? __double2float_ru(qt + delta) : INFINITY;
+        rq.z = (float)(4.7e-7 + 0.6931471805599453 * e0q);
+        rq.w = (float)(0.6931471805599453 * e1q);
+        // bounding box of {q <= q_hi' / k}: half extents sqrt(Q Sigma_xx), sqrt(Q Sigma_yy), Sigma = conic^-1
+        const double Q = (double)rq.y / K;
+        if (isfinite(Q) && det > 0.0) {
+            const double hx = sqrt(Q * (cc / det)) * (1.0 + 1e-6) + 1e-4;
+            const double hy = sqrt(Q * (ca / det)) * (1.0 + 1e-6) + 1e-4;
+            bb = make_float4(__double2float_rd(m0 - hx), __double2float_ru(m0 + hx), __double2float_rd(m1 - hy),
+                             __double2float_ru(m1 + hy));
+        } else {
+            bb = make_float4(-INFINITY, INFINITY, -INFINITY, INFINITY);
+        }
+    }
+    const double l11 = sqrt(K * ca);
+    const double l21 = K * cb / l11;
+    const double l22 = sqrt(fmax(K * det / ca, 0.0));
+    ws.rc[p] = make_float4((float)l11, (float)l21, (float)l22, (float)o);
+    ws.rq[p] = rq;
+    ws.bbox[p] = bb;
+}
+
 // Block-level reduction of the per-thread frame counters and of the min / max
 // fp64 bit pattern of binned depths (the depth sort's key range): one atomic
 // per counter per CTA instead of one per warp and iteration.
@@ -275,7 +337,7 @@ __global__ void __launch_bounds__(256, 3) k_preprocess(SceneK sc, const int64_t 
                         col.y = (float)sh_channel([&](int k) { return shp[16 + k]; }, vx, vy, vz, cfg.sh_degree);
                         col.z = (float)sh_channel([&](int k) { return shp[32 + k]; }, vx, vy, vz, cfg.sh_degree);
                     }
-                    col.w = 0.f;
+                    col.w = (float)(1.0 - g.o);
                     double r2 = 9.0;  // MAX_RADIUS_SQ
                     if (cfg.opacity_aware) {
                         r2 = 2.0 * log(g.o / cfg.alpha_theta);
@@ -298,20 +360,7 @@ __global__ void __launch_bounds__(256, 3) k_preprocess(SceneK sc, const int64_t 
                     ws.mean[p] = make_double2(m0, m1);
                     ws.conic_op[p] = make_double4(ca, cb, cc, g.o);
                     ws.color[p] = col;
-                    // FAST raster alpha-test bracket (raster.cu): alpha >= theta  <=>  q <= q_th =
-                    // 2 ln(o / theta) (rasterize.py:146-151, 209).  The kernel rounds its fp64 q to
-                    // fp32 (rel. 2^-24) and its fp64 q differs from numpy's by <= 1e-15 kappa,
-                    // kappa = 2 (a + c) / lambda_min bounding the term cancellation.
-                    const double qth = 2.0 * log(g.o / cfg.alpha_theta);
-                    const double tr = ca + cc, disc = sqrt(0.25 * (ca - cc) * (ca - cc) + cb * cb);
-                    const double lmin = fmax(0.5 * tr - disc, 1e-300);
-                    const double slack = 1.3e-7 + 1e-15 * (2.0 * tr / lmin);
-                    float q_lo = -INFINITY, q_hi = -INFINITY;
-                    if (qth >= 0.0) {
-                        q_lo = __double2float_rd(qth * (1.0 - slack) - 1e-30);
-                        q_hi = slack < 0.5 ? __double2float_ru(qth * (1.0 + slack) + 1e-30) : INFINITY;
-                    }
-                    ws.fast[p] = make_float4(q_lo, q_hi, (float)g.o, (float)(1.0 - g.o));
+                    write_raster_record(ws, p, m0, m1, ca, cb, cc, g.o, cfg.alpha_theta);
                 }
             }
             ws.status[p] = (uint8_t)status;
