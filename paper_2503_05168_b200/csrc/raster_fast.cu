@@ -168,6 +168,47 @@ __device__ __forceinline__ uint32_t quad_alphas(const Staged &sg, const float q[
     return pass & need;
 }
 
+// alpha >= theta of one pixel (the CR group leader, slot 0 of its quad),
+// same arithmetic as quad_alphas.
+__device__ __forceinline__ bool pixel_alpha(const Staged &sg, float q, int px, int py, const Workspace &ws,
+                                            double th64, float &al, float &om, float &ef, uint32_t &n_redecide) {
+    const float e = sg.o * ex2_approx(-q);
+    al = fminf(e, (float)kAlphaClamp);
+    om = 1.0f - al;
+    ef = fmaf(al, fmaf(sg.e1, q, sg.e0), 6.0e-8f);
+    bool pass = q < sg.q_lo;
+    if (e > 0.5f) {
+        if (e >= 0.99f * (1.0f + 4.0f * fmaf(sg.e1, q, sg.e0))) {
+            om = (float)(1.0 - kAlphaClamp);
+            ef = 1.0e-9f;
+        } else if (al < (float)kAlphaClamp) {
+            const float x = 0.69314718f * q;
+            float em = fmaf(-x, 1.0f / 362880.0f, 1.0f / 40320.0f);
+            em = fmaf(-x, em, 1.0f / 5040.0f);
+            em = fmaf(-x, em, 1.0f / 720.0f);
+            em = fmaf(-x, em, 1.0f / 120.0f);
+            em = fmaf(-x, em, 1.0f / 24.0f);
+            em = fmaf(-x, em, 1.0f / 6.0f);
+            em = fmaf(-x, em, 0.5f);
+            em = fmaf(-x, em, 1.0f);
+            em *= x;
+            om = fmaf(sg.o, em, sg.om_o);
+            ef = fmaf(6.2e-7f, om, al * fmaf(sg.e1, q, sg.e0));
+        }
+    }
+    if (!pass && q <= sg.q_hi) {
+        const double2 m = ws.mean[sg.p];
+        const double4 co = ws.conic_op[sg.p];
+        const double a64 = alpha64((double)px + 0.5, (double)py + 0.5, m.x, m.y, co.x, co.y, co.z, co.w);
+        al = (float)a64;
+        om = (float)(1.0 - a64);
+        ef = 1.0e-9f;
+        pass = a64 >= th64;
+        n_redecide++;
+    }
+    return pass;
+}
+
 // Exact fp64 transmittance of pixel (px, py) after the tile's splats k0..k1
 // (reference semantics, rasterize.py:146-177), for a pixel live throughout:
 // it blends splat k iff alpha_k >= theta and, for CR, its group leader's
@@ -254,8 +295,13 @@ __global__ void __launch_bounds__(64, 8) k_raster_quad(Workspace ws, const uint3
     }
     // CR group leader pixel (rasterize.py:235-246): top-left pixel of the w x w group
     const int lead_x = W == 4 ? ox + 4 * (bx >> 1) : x0, lead_y = W == 4 ? oy + 4 * (by >> 1) : y0;
-    uint32_t c_alpha = 0, c_blend = 0, c_leader = 0, n_redecide = 0, n_tamb = 0;
-    uint32_t n_live = 0, n_blend = 0, n_skip = 0;  // pixel-level work (bench.py work model)
+    // Per pixel: number of tile splats it was live for (its death step); out-of-image pixels 0.
+    // The reference charges a model-warp's alpha_eval (ref) / leader_eval (cr) once per splat while
+    // any of its pixels is live, i.e. the max death step over its pixels.
+    uint32_t di[4];
+#pragma unroll
+    for (int s = 0; s < 4; s++) di[s] = ((valid >> s) & 1u) ? 0xffffffffu : 0u;
+    uint32_t c_alpha = 0, c_blend = 0, n_redecide = 0, n_tamb = 0, n_skip = 0;
     const uint2 rg = ws.ranges[tile];
 
     Staged *s_g = s_stage[warp];
@@ -315,49 +361,46 @@ __global__ void __launch_bounds__(64, 8) k_raster_quad(Workspace ws, const uint3
             } else {
                 j = nb;  // no more relevant splats: charge the rest of the batch
             }
-            const uint32_t mw_live = slice_any(lb, shift);
-            const uint32_t gap = (uint32_t)(j - jprev - 1);  // skipped splats: one lockstep step each
-            if (gap) {
-                if (W == 0) c_alpha += gap * mw_live; else c_leader += gap * mw_live;
-                n_live += gap * __popc(live);
-                n_skip += gap * __popc(live);
-            }
+            const uint32_t gap = (uint32_t)(j - jprev - 1);  // skipped splats (charged via the death steps)
+            if (gap) n_skip += gap * __popc(live);
             if (j >= nb) break;
             jprev = j;
+            const uint32_t step = b0 + (uint32_t)j - rg.x + 1u;  // tile splats processed including this one
             const Staged &sg = s_g[j];
-            n_live += __popc(live);
             float q[4], al[4], om[4], ef[4];
             quad_q(sg, lx0, ly0, q);
             uint32_t blend;
             if (W == 0 || W == 1) {
                 blend = quad_alphas(sg, q, x0, y0, live, ws, th64, al, om, ef, n_redecide);
-                if (W == 0) {
-                    c_alpha += mw_live;
-                } else {  // w = 1: every pixel is its own group and leader
+                if (W == 1) {  // every pixel is its own group and leader
                     const unsigned pb = __ballot_sync(0xffffffffu, blend != 0u);
-                    c_leader += mw_live;
                     c_alpha += slice_any(pb, shift);
                 }
             } else {
                 // leader phase: the leader pixel's alpha counts even if that pixel is done (rasterize.py:281)
                 const bool glive = W == 2 ? live != 0u : (lb & gmask) != 0u;
-                const uint32_t lneed = (leader_thread && glive) ? 1u : 0u;
-                const uint32_t lpass = quad_alphas(sg, q, x0, y0, lneed, ws, th64, al, om, ef, n_redecide);
-                const unsigned pb = __ballot_sync(0xffffffffu, lpass != 0u);
-                c_leader += mw_live;
+                bool lpass = false;
+                float al0 = 0.f, om0 = 1.f, ef0 = 0.f;
+                if (leader_thread && glive) lpass = pixel_alpha(sg, q[0], x0, y0, ws, th64, al0, om0, ef0, n_redecide);
+                const unsigned pb = __ballot_sync(0xffffffffu, lpass);
                 c_alpha += slice_any(pb, shift);
                 blend = 0u;
                 if (pb != 0u) {  // member phase (rasterize.py:283-289), skipped when no leader of the warp passed
                     const bool my_pass = (pb >> (W == 2 ? lane : leader_lane)) & 1u;
-                    const uint32_t mneed = my_pass ? live : 0u;
-                    blend = quad_alphas(sg, q, x0, y0, mneed, ws, th64, al, om, ef, n_redecide);
+                    const uint32_t mine = leader_thread ? 1u : 0u;  // slot 0 is this thread's leader pixel
+                    blend = quad_alphas(sg, q, x0, y0, my_pass ? (live & ~mine) : 0u, ws, th64, al, om, ef, n_redecide);
+                    if (leader_thread) {
+                        al[0] = al0;
+                        om[0] = om0;
+                        ef[0] = ef0;
+                        blend |= (my_pass && (live & 1u)) ? 1u : 0u;  // leader pixel: lpass is its own alpha test
+                    }
                 }
             }
             const unsigned bb = __ballot_sync(0xffffffffu, blend != 0u);
             if (bb == 0u) continue;
             c_blend += slice_any(bb, shift);
-            n_blend += __popc(blend);
-            uint32_t amb = 0;
+            uint32_t near = 0;
 #pragma unroll
             for (int s = 0; s < 4; s++) {  // _blend (rasterize.py:169-177), predicated per pixel
                 const bool on = (blend >> s) & 1u;
@@ -371,39 +414,66 @@ __global__ void __launch_bounds__(64, 8) k_raster_quad(Workspace ws, const uint3
                 st.T[s] = on ? t1 : t0;
                 st.D[s] = on ? d1 : st.D[s];
                 st.cnt[s] += on ? 1 : 0;
-                const bool done = on && (t1 + d1 < gm);
-                const bool unsure = on && !done && (t1 - d1 < gm);
-                live &= ~((done ? 1u : 0u) << s);
-                amb |= (unsure ? 1u : 0u) << s;
+                near |= (on && t1 - d1 < gm ? 1u : 0u) << s;  // T may be below gamma: decide below
             }
-            unsigned ambw = __ballot_sync(0xffffffffu, amb != 0u);
-            while (ambw) {
-                // T < gamma undecidable in fp32: recompute that pixel's transmittance exactly (fp64, reference
-                // formula) over every splat of the tile up to this one, all 32 lanes together, then decide.  A
-                // live pixel's blends depend only on its own alphas (and its group leader's for CR).
-                const int src = __ffs(ambw) - 1;
-                const uint32_t am = __shfl_sync(0xffffffffu, amb, src);
-                const int s = __ffs(am) - 1;
-                const int px = __shfl_sync(0xffffffffu, x0, src) + (s & 1);
-                const int py = __shfl_sync(0xffffffffu, y0, src) + (s >> 1);
-                const int gx = __shfl_sync(0xffffffffu, lead_x, src), gy = __shfl_sync(0xffffffffu, lead_y, src);
-                const double T = exact_transmittance<W>(ws, pair_pos, rg.x, b0 + (uint32_t)j, px, py, gx, gy, th64);
-                if (lane == src) {
-                    n_tamb++;
+            if (__any_sync(0xffffffffu, near != 0u)) {
+                uint32_t amb = 0;
 #pragma unroll
-                    for (int ss = 0; ss < 4; ss++) {
-                        if (ss != s) continue;
-                        st.T[ss] = (float)T;
-                        st.D[ss] = 6.0e-8f * (float)T;
-                        if (T < cfg.gamma) live &= ~(1u << ss);
+                for (int s = 0; s < 4; s++) {
+                    if (!((near >> s) & 1u)) continue;
+                    if (st.T[s] + st.D[s] < gm) {  // surely below: done (rasterize.py:177)
+                        live &= ~(1u << s);
+                        di[s] = step;
+                    } else {
+                        amb |= 1u << s;
                     }
-                    amb &= ~(1u << s);
                 }
-                ambw = __ballot_sync(0xffffffffu, amb != 0u);
+                unsigned ambw = __ballot_sync(0xffffffffu, amb != 0u);
+                while (ambw) {
+                    // T < gamma undecidable in fp32: recompute that pixel's transmittance exactly (fp64,
+                    // reference formula) over every splat of the tile up to this one, all 32 lanes together,
+                    // then decide.  A live pixel's blends depend only on its own alphas (and its group
+                    // leader's for CR).
+                    const int src = __ffs(ambw) - 1;
+                    const uint32_t am = __shfl_sync(0xffffffffu, amb, src);
+                    const int s = __ffs(am) - 1;
+                    const int px = __shfl_sync(0xffffffffu, x0, src) + (s & 1);
+                    const int py = __shfl_sync(0xffffffffu, y0, src) + (s >> 1);
+                    const int gx = __shfl_sync(0xffffffffu, lead_x, src), gy = __shfl_sync(0xffffffffu, lead_y, src);
+                    const double T = exact_transmittance<W>(ws, pair_pos, rg.x, b0 + (uint32_t)j, px, py, gx, gy, th64);
+                    if (lane == src) {
+                        n_tamb++;
+#pragma unroll
+                        for (int ss = 0; ss < 4; ss++) {
+                            if (ss != s) continue;
+                            st.T[ss] = (float)T;
+                            st.D[ss] = 6.0e-8f * (float)T;
+                            if (T < cfg.gamma) {
+                                live &= ~(1u << ss);
+                                di[ss] = step;
+                            }
+                        }
+                        amb &= ~(1u << s);
+                    }
+                    ambw = __ballot_sync(0xffffffffu, amb != 0u);
+                }
             }
             lb = __ballot_sync(0xffffffffu, live != 0u);
         }
     }
+    // pixels still live at the end took every splat of the list
+    uint32_t n_live = 0, n_blend = 0, mw_steps = 0;
+#pragma unroll
+    for (int s = 0; s < 4; s++) {
+        if (di[s] == 0xffffffffu) di[s] = rg.y > rg.x ? rg.y - rg.x : 0u;
+        n_live += di[s];
+        n_blend += (uint32_t)st.cnt[s];
+        mw_steps = max(mw_steps, di[s]);
+    }
+#pragma unroll
+    for (int o = 1; o < 8; o <<= 1) mw_steps = max(mw_steps, __shfl_xor_sync(0xffffffffu, mw_steps, o));
+    uint32_t c_leader = 0;
+    if (W == 0) c_alpha = mw_steps; else c_leader = mw_steps;
     const uint32_t w_red = __reduce_add_sync(0xffffffffu, n_redecide);
     const uint32_t w_tamb = __reduce_add_sync(0xffffffffu, n_tamb);
     const uint32_t w_live = __reduce_add_sync(0xffffffffu, n_live);
