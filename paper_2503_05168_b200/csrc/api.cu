@@ -131,7 +131,6 @@ Workspace carve_workspace(void *base, long long n_max, long long cap, int width,
                                         2 * w.look_tiles_p * 256);
     w.status = c.take<uint8_t>(n);
     w.depth = c.take<double>(n);
-    w.tiles = c.take<uint32_t>(n);
     w.rect = c.take<short4>(n);
     w.mean = c.take<double2>(n);
     w.conic_op = c.take<double4>(n);

@@ -62,8 +62,8 @@ __device__ __forceinline__ DepthKey depth_key(const Workspace &ws) {
     return k;
 }
 
-__device__ __forceinline__ uint32_t depth_quant(const DepthKey &k, uint32_t tiles, double d) {
-    if (tiles == 0u) return 0xffffffu;  // not binned: after every binned splat
+__device__ __forceinline__ uint32_t depth_quant(const DepthKey &k, short4 rect, double d) {
+    if (rect.x > rect.y) return 0xffffffu;  // not binned (empty tile rect): after every binned splat
     const double q = floor((d - k.lo) * k.scale);
     return q < 16777214.0 ? (uint32_t)q : 0xfffffeu;
 }
@@ -97,12 +97,12 @@ __global__ void __launch_bounds__(256) k_depth_hist(Workspace ws) {
     const uint32_t n = ws.counters[CNT_WS];
     constexpr int U = 8;
     for (uint32_t i0 = blockIdx.x * 256 * U + tid; i0 < n; i0 += gridDim.x * 256 * U) {
-        uint32_t tl[U];
+        short4 tl[U];
         double d[U];
 #pragma unroll
         for (int u = 0; u < U; u++) {
             const uint32_t i = min(i0 + u * 256, n - 1);
-            tl[u] = ws.tiles[i];
+            tl[u] = ws.rect[i];
             d[u] = ws.depth[i];
         }
 #pragma unroll
@@ -167,12 +167,12 @@ __global__ void __launch_bounds__(NT, 2) k_depth_pass(Workspace ws, int pass) {
     const uint32_t ib = t0 + warp * 32 * IPT + lane;
     if (pass == 0) {
         const DepthKey dk = depth_key(ws);
-        uint32_t tl[IPT];
+        short4 tl[IPT];
         double d[IPT];
 #pragma unroll
         for (int r = 0; r < IPT; r++) {
             const uint32_t i = min(ib + r * 32, n - 1);
-            tl[r] = ws.tiles[i];
+            tl[r] = ws.rect[i];
             d[r] = ws.depth[i];
         }
 #pragma unroll
@@ -349,8 +349,13 @@ __global__ void __launch_bounds__(512) k_depth_fix_long(Workspace ws) {
 
 // ---- row entries: offsets, tile counts, ranges -------------------------------------
 
+// Row entries cover at most kSegW columns (wider ones are split; pieces of one
+// splat cover disjoint columns, so the per-column order is unaffected): the
+// column pass's per-entry loops stay short.
+constexpr uint32_t kSegW = 8;
+
 // bin_tiles (preprocess.py:159-189) of splat rank r covers rect [x0,x1] x [y0,y1]
-// -> one row entry per covered tile row y (x range [x0, x1]) and w * h pairs.
+// -> ceil(w / kSegW) row entries per covered tile row y and w * h pairs.
 // This persistent kernel scans the entry counts h in depth-rank order
 // (decoupled look-back over 4096-rank tiles) into poff, marks the first rank
 // of every 4096-entry tile of the row pass, counts pairs, and accumulates the
@@ -389,14 +394,15 @@ __global__ void __launch_bounds__(NT) k_pair_scan(Workspace ws, int tiles_x, int
             if (r < n) {
                 const short4 rc = ws.rect[sorted[r]];
                 const int w = rc.y - rc.x + 1, hh = rc.w - rc.z + 1;
-                h[k] = (uint32_t)hh;
+                const int nseg = (w + kSegW - 1) / kSegW;  // row entries are split into <= kSegW columns
+                h[k] = (uint32_t)(hh * nseg);
                 my_pairs += (unsigned long long)(w * hh);
                 atomicAdd(&diff[rc.z * tx1 + rc.x], 1);
                 atomicAdd(&diff[rc.z * tx1 + rc.y + 1], -1);
                 atomicAdd(&diff[(rc.w + 1) * tx1 + rc.x], -1);
                 atomicAdd(&diff[(rc.w + 1) * tx1 + rc.y + 1], 1);
-                atomicAdd(&s_row[rc.z], 1);
-                atomicAdd(&s_row[rc.w + 1], -1);
+                atomicAdd(&s_row[rc.z], nseg);
+                atomicAdd(&s_row[rc.w + 1], -nseg);
             }
             sum += h[k];
         }
@@ -567,7 +573,10 @@ __global__ void __launch_bounds__(NT, 2) k_row_pass(Workspace ws, int64_t *stats
             if (S.u.e.off[mid] <= i0) lo = mid; else hi = mid - 1;
         }
         uint32_t rc = S.u.e.rect[lo];
-        uint32_t y = (rc >> 16) + (i0 - S.u.e.off[lo]);
+        uint32_t xa = rc & 0xffu, xb = (rc >> 8) & 0xffu;
+        uint32_t nseg = (xb - xa + kSegW) / kSegW;
+        const uint32_t local = i0 - S.u.e.off[lo];
+        uint32_t y = (rc >> 16) + local / nseg, seg = local % nseg;
         uint32_t next = S.u.e.off[lo + 1];
         uint32_t p = S.u.e.pos[lo];
         const uint32_t stop = min(i0 + (uint32_t)IPT, end);
@@ -575,13 +584,21 @@ __global__ void __launch_bounds__(NT, 2) k_row_pass(Workspace ws, int64_t *stats
             if (i == next) {
                 lo++;
                 rc = S.u.e.rect[lo];
+                xa = rc & 0xffu;
+                xb = (rc >> 8) & 0xffu;
+                nseg = (xb - xa + kSegW) / kSegW;
                 y = rc >> 16;
+                seg = 0;
                 next = S.u.e.off[lo + 1];
                 p = S.u.e.pos[lo];
             }
-            S.gx[i - base] = (rc & 0xffffu) | (y << 16);
+            const uint32_t s0 = xa + seg * kSegW, s1 = min(xb, s0 + kSegW - 1);
+            S.gx[i - base] = s0 | (s1 << 8) | (y << 16);
             S.gp[i - base] = p;
-            y++;
+            if (++seg == nseg) {
+                seg = 0;
+                y++;
+            }
         }
     }
     __syncthreads();
@@ -622,7 +639,7 @@ __global__ void __launch_bounds__(NT, 2) k_row_pass(Workspace ws, int64_t *stats
 // ---- column pass ---------------------------------------------------------------------
 
 constexpr int kColW = kMaxTileAxis + 1;
-constexpr int kColStage = 16384;  // pairs staged per column group (64 KB + 16 KB)
+constexpr int kColStage = 12288;  // pairs staged per column group (48 KB + 12 KB)
 
 struct ColSmem {
     int32_t cnt[NT / 32][kColW];      // per-warp counts -> per-warp staging offsets
@@ -632,6 +649,7 @@ struct ColSmem {
     uint32_t stage[kColStage];
     uint8_t stx[kColStage];
     uint32_t gfirst[kColW + 1];       // column groups that fit the staging buffer
+    uint32_t chunk_first[kColW + 1];
     int n_groups;
     uint32_t row;
 };
@@ -647,18 +665,20 @@ struct ColSmem {
 // popc(mask_v & lanes_below) -- work proportional to the entry's width.
 // Pairs are staged by column in shared memory and copied out as contiguous
 // runs.
-__global__ void __launch_bounds__(NT, 1) k_col_pass(Workspace ws, int tiles_x, int tiles_y) {
+__global__ void __launch_bounds__(NT, 2) k_col_pass(Workspace ws, int tiles_x, int tiles_y) {
     extern __shared__ __align__(16) unsigned char smem[];
     ColSmem &S = *reinterpret_cast<ColSmem *>(smem);
     const uint32_t C = ws.counters[CNT_CHUNKS];
     const uint32_t t = take_ticket(&ws.counters[CNT_TICKET + kLookCols]);
     if (t >= C) return;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    for (int y = tid; y < tiles_y; y += NT) S.chunk_first[y] = ws.chunk_first[y];
+    __syncthreads();
     if (tid == 0) {  // row of chunk t: last y with chunk_first[y] <= t
         int lo = 0, hi = tiles_y - 1;
         while (lo < hi) {
             const int mid = (lo + hi + 1) >> 1;
-            if (ws.chunk_first[mid] <= t) lo = mid; else hi = mid - 1;
+            if (S.chunk_first[mid] <= t) lo = mid; else hi = mid - 1;
         }
         S.row = (uint32_t)lo;
     }

@@ -70,7 +70,6 @@ struct Workspace {
     // per assembled splat (preprocess)
     uint8_t *status;
     double *depth;
-    uint32_t *tiles;
     short4 *rect;
     double2 *mean;
     double4 *conic_op;   // (a, b, c, opacity)

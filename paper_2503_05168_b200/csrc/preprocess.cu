@@ -18,13 +18,15 @@ namespace seele {
 
 namespace {
 
-__constant__ double kSH_C0 = 0.28209479177387814;
-__constant__ double kSH_C1 = 0.4886025119029199;
-__constant__ double kSH_C2[5] = {1.0925484305920792, -1.0925484305920792, 0.31539156525252005,
-                                 -1.0925484305920792, 0.5462742152960396};
-__constant__ double kSH_C3[7] = {-0.5900435899266435, 2.890611442640554, -0.4570457994644658,
-                                 0.3731763325901154, -0.4570457994644658, 1.445305721320277,
-                                 -0.5900435899266435};
+// SH constants (model.py:24-41).  The colour only feeds the blend (image
+// tolerance 1e-3, plan colours compared at 1e-6), so it is evaluated in fp32.
+constexpr float kSH_C0 = 0.28209479177387814f;
+constexpr float kSH_C1 = 0.4886025119029199f;
+__constant__ float kSH_C2[5] = {1.0925484305920792f, -1.0925484305920792f, 0.31539156525252005f,
+                             -1.0925484305920792f, 0.5462742152960396f};
+__constant__ float kSH_C3[7] = {-0.5900435899266435f, 2.890611442640554f, -0.4570457994644658f,
+                             0.3731763325901154f, -0.4570457994644658f, 1.445305721320277f,
+                             -0.5900435899266435f};
 
 __device__ __forceinline__ void quat_to_mat(double w, double x, double y, double z, double r[9]) {
     // model.py:83-93
@@ -42,23 +44,23 @@ __device__ __forceinline__ void quat_to_mat(double w, double x, double y, double
 // sh_to_color for one channel (model.py:276-305), then +0.5 and clamp at 0.
 // `s(k)` yields coefficient k of the channel (loaded on demand: each is used once).
 template <typename Coef>
-__device__ __forceinline__ double sh_channel(Coef s, double x, double y, double z, int degree) {
-    double c = kSH_C0 * s(0);
+__device__ __forceinline__ float sh_channel(Coef s, float x, float y, float z, int degree) {
+    float c = kSH_C0 * s(0);
     if (degree >= 1) c = c - kSH_C1 * y * s(1) + kSH_C1 * z * s(2) - kSH_C1 * x * s(3);
     if (degree >= 2) {
-        double xx = x * x, yy = y * y, zz = z * z, xy = x * y, yz = y * z, xz = x * z;
-        c = c + kSH_C2[0] * xy * s(4) + kSH_C2[1] * yz * s(5) + kSH_C2[2] * (2.0 * zz - xx - yy) * s(6) +
+        const float xx = x * x, yy = y * y, zz = z * z, xy = x * y, yz = y * z, xz = x * z;
+        c = c + kSH_C2[0] * xy * s(4) + kSH_C2[1] * yz * s(5) + kSH_C2[2] * (2.0f * zz - xx - yy) * s(6) +
             kSH_C2[3] * xz * s(7) + kSH_C2[4] * (xx - yy) * s(8);
         if (degree >= 3) {
-            c = c + kSH_C3[0] * y * (3.0 * xx - yy) * s(9) + kSH_C3[1] * xy * z * s(10) +
-                kSH_C3[2] * y * (4.0 * zz - xx - yy) * s(11) +
-                kSH_C3[3] * z * (2.0 * zz - 3.0 * xx - 3.0 * yy) * s(12) +
-                kSH_C3[4] * x * (4.0 * zz - xx - yy) * s(13) + kSH_C3[5] * z * (xx - yy) * s(14) +
-                kSH_C3[6] * x * (xx - 3.0 * yy) * s(15);
+            c = c + kSH_C3[0] * y * (3.0f * xx - yy) * s(9) + kSH_C3[1] * xy * z * s(10) +
+                kSH_C3[2] * y * (4.0f * zz - xx - yy) * s(11) +
+                kSH_C3[3] * z * (2.0f * zz - 3.0f * xx - 3.0f * yy) * s(12) +
+                kSH_C3[4] * x * (4.0f * zz - xx - yy) * s(13) + kSH_C3[5] * z * (xx - yy) * s(14) +
+                kSH_C3[6] * x * (xx - 3.0f * yy) * s(15);
         }
     }
-    c = c + 0.5;
-    return c > 0.0 ? c : 0.0;
+    c = c + 0.5f;
+    return c > 0.0f ? c : 0.0f;
 }
 
 // _axis_range (preprocess.py:149-156): inclusive [first, last]; first > last = none.
@@ -96,11 +98,11 @@ __device__ __forceinline__ double sigmoid_clip(double x) {
 }
 
 __device__ __forceinline__ void normalize4(double q[4]) {
-    double nrm = sqrt(q[0] * q[0] + q[1] * q[1] + q[2] * q[2] + q[3] * q[3]);
-    q[0] = q[0] / nrm;
-    q[1] = q[1] / nrm;
-    q[2] = q[2] / nrm;
-    q[3] = q[3] / nrm;
+    const double r = 1.0 / sqrt(q[0] * q[0] + q[1] * q[1] + q[2] * q[2] + q[3] * q[3]);
+    q[0] *= r;
+    q[1] *= r;
+    q[2] *= r;
+    q[3] *= r;
 }
 
 template <int LAYOUT>
@@ -149,10 +151,9 @@ __device__ __forceinline__ void load_splat(const SceneK &sc, long long i, int sh
 // bbox = axis-aligned box of {q' <= q_hi'}; the raster refines it with the
 // exact minimum of q' over each warp's pixel rectangle.
 __device__ __forceinline__ void write_raster_record(const Workspace &ws, long long p, double m0, double m1, double ca,
-                                                    double cb, double cc, double o, double theta) {
+                                                    double cb, double cc, double o, double qth) {
     const double K = 0.72134752044448170368;  // log2(e) / 2
     const double u = 5.9604644775390625e-08;  // 2^-24
-    const double qth = 2.0 * log(o / theta);
     const double tr = ca + cc, disc = sqrt(0.25 * (ca - cc) * (ca - cc) + cb * cb);
     const double lmin = fmax(0.5 * tr - disc, 1e-300);
     const double det = ca * cc - cb * cb;
@@ -271,10 +272,11 @@ __global__ void __launch_bounds__(256, 3) k_preprocess(SceneK sc, const int64_t 
             if (z <= cam.near_clip) {
                 status = 1;  // "near" (preprocess.py:101-103)
             } else {
-                const double m0 = cam.fx * t[0] / z + cam.cx;  // preprocess.py:107
-                const double m1 = cam.fy * t[1] / z + cam.cy;
-                const double j00 = cam.fx / z, j02 = -cam.fx * t[0] / (z * z);
-                const double j11 = cam.fy / z, j12 = -cam.fy * t[1] / (z * z);
+                const double rz = 1.0 / z;
+                const double m0 = cam.fx * t[0] * rz + cam.cx;  // preprocess.py:107
+                const double m1 = cam.fy * t[1] * rz + cam.cy;
+                const double j00 = cam.fx * rz, j02 = -cam.fx * t[0] * rz * rz;
+                const double j11 = cam.fy * rz, j12 = -cam.fy * t[1] * rz * rz;
                 double jw[6];
                 for (int c = 0; c < 3; c++) {
                     jw[c] = j00 * cam.w2v[c] + 0.0 * cam.w2v[3 + c] + j02 * cam.w2v[6 + c];
@@ -307,9 +309,11 @@ __global__ void __launch_bounds__(256, 3) k_preprocess(SceneK sc, const int64_t 
                     status = 2;  // "degenerate" (preprocess.py:122-124)
                 } else {
                     status = 0;
-                    const double ca = s11 / det, cb = -s01 / det, cc = s00 / det;
-                    const double nrm = sqrt(d[0] * d[0] + d[1] * d[1] + d[2] * d[2]);
-                    const double vx = d[0] / nrm, vy = d[1] / nrm, vz = d[2] / nrm;
+                    const double rdet = 1.0 / det;
+                    const double ca = s11 * rdet, cb = -s01 * rdet, cc = s00 * rdet;
+                    // view direction for SH (preprocess.py:129-130), fp32 like the colour
+                    const float rn = rsqrtf((float)(d[0] * d[0] + d[1] * d[1] + d[2] * d[2]));
+                    const float vx = (float)d[0] * rn, vy = (float)d[1] * rn, vz = (float)d[2] * rn;
                     float4 col;
                     if (LAYOUT == SEELE_LAYOUT_PLANES) {
                         // SH planes are read only for projected splats, one channel (4 x float4) at a time
@@ -326,27 +330,29 @@ __global__ void __launch_bounds__(256, 3) k_preprocess(SceneK sc, const int64_t 
                                 shc[4 * k + 2] = v.z;
                                 shc[4 * k + 3] = v.w;
                             }
-                            cc3[ch] = (float)sh_channel([&](int k) { return (double)shc[k]; }, vx, vy, vz, cfg.sh_degree);
+                            cc3[ch] = sh_channel([&](int k) { return shc[k]; }, vx, vy, vz, cfg.sh_degree);
                         }
                         col.x = cc3[0];
                         col.y = cc3[1];
                         col.z = cc3[2];
                     } else {
                         const double *shp = sc.sh + 48 * i;
-                        col.x = (float)sh_channel([&](int k) { return shp[k]; }, vx, vy, vz, cfg.sh_degree);
-                        col.y = (float)sh_channel([&](int k) { return shp[16 + k]; }, vx, vy, vz, cfg.sh_degree);
-                        col.z = (float)sh_channel([&](int k) { return shp[32 + k]; }, vx, vy, vz, cfg.sh_degree);
+                        col.x = sh_channel([&](int k) { return (float)shp[k]; }, vx, vy, vz, cfg.sh_degree);
+                        col.y = sh_channel([&](int k) { return (float)shp[16 + k]; }, vx, vy, vz, cfg.sh_degree);
+                        col.z = sh_channel([&](int k) { return (float)shp[32 + k]; }, vx, vy, vz, cfg.sh_degree);
                     }
                     col.w = (float)(1.0 - g.o);
+                    const double qth = 2.0 * log(g.o / cfg.alpha_theta);  // alpha >= theta <=> q <= qth
                     double r2 = 9.0;  // MAX_RADIUS_SQ
                     if (cfg.opacity_aware) {
-                        r2 = 2.0 * log(g.o / cfg.alpha_theta);
+                        r2 = qth;
                         r2 = r2 > 9.0 ? 9.0 : r2;
                         r2 = r2 < 0.0 ? 0.0 : r2;
                     }
                     if (r2 > 0.0) {
                         const double detp = ca * cc - cb * cb;
-                        const double hx = sqrt(r2 * (cc / detp)), hy = sqrt(r2 * (ca / detp));
+                        const double rdp = 1.0 / detp;
+                        const double hx = sqrt(r2 * (cc * rdp)), hy = sqrt(r2 * (ca * rdp));
                         int x0, x1, y0, y1;
                         axis_range(m0 - hx, m0 + hx, cam.tiles_x, x0, x1);
                         axis_range(m1 - hy, m1 + hy, cam.tiles_y, y0, y1);
@@ -360,12 +366,11 @@ __global__ void __launch_bounds__(256, 3) k_preprocess(SceneK sc, const int64_t 
                     ws.mean[p] = make_double2(m0, m1);
                     ws.conic_op[p] = make_double4(ca, cb, cc, g.o);
                     ws.color[p] = col;
-                    write_raster_record(ws, p, m0, m1, ca, cb, cc, g.o, cfg.alpha_theta);
+                    write_raster_record(ws, p, m0, m1, ca, cb, cc, g.o, qth);
                 }
             }
             ws.status[p] = (uint8_t)status;
             ws.rect[p] = rect;
-            ws.tiles[p] = n_tiles;
         }
         cnt[0] += status == 1;
         cnt[1] += status == 2;
