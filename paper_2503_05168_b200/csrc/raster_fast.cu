@@ -57,26 +57,29 @@ struct __align__(16) Staged {
 
 __device__ __forceinline__ uint32_t slice_any(unsigned ballot, int shift) { return ((ballot >> shift) & 0xffu) != 0u; }
 
-// Quad state: four pixels, slot s = (x0 + (s & 1), y0 + (s >> 1)).
+// Quad state: four pixels, slot s = (x0 + (s & 1), y0 + (s >> 1)); the two
+// pixels of a quad row r = s >> 1 are one float2 (.x = left, .y = right) so
+// the per-pixel math runs as packed fp32x2 instructions (FFMA2 / FMUL2 /
+// FADD2, per-element round-to-nearest: bit-identical to scalar fmaf).
 struct Quad {
-    float T[4], D[4], C[4][3];
+    float2 T[2], D[2], C[2][3];
     int cnt[4];
 };
 
+__device__ __forceinline__ float2 f2(float v) { return make_float2(v, v); }
+__device__ __forceinline__ float lane_of(const float2 &v, int c) { return c ? v.y : v.x; }
+
 // q' of the four quad pixels (fp32 Cholesky form, error model at
-// preprocess.cu write_raster_record).
-__device__ __forceinline__ void quad_q(const Staged &sg, float lx0, float ly0, float q[4]) {
-    const float dx0 = (lx0 - sg.mxh) - sg.mxl, dx1 = dx0 + 1.0f;
-    const float dy0 = (ly0 - sg.myh) - sg.myl, dy1 = dy0 + 1.0f;
-    const float t0 = sg.l21 * dy0, t1 = sg.l21 * dy1;
-    const float w0 = sg.l22 * dy0, w1 = sg.l22 * dy1;
-    const float ww0 = w0 * w0, ww1 = w1 * w1;
-    const float u00 = fmaf(sg.l11, dx0, t0), u10 = fmaf(sg.l11, dx1, t0);
-    const float u01 = fmaf(sg.l11, dx0, t1), u11 = fmaf(sg.l11, dx1, t1);
-    q[0] = fmaf(u00, u00, ww0);
-    q[1] = fmaf(u10, u10, ww0);
-    q[2] = fmaf(u01, u01, ww1);
-    q[3] = fmaf(u11, u11, ww1);
+// preprocess.cu write_raster_record): q[r] = (q of (x0, y0 + r), q of (x0 + 1, y0 + r)).
+__device__ __forceinline__ void quad_q(const Staged &sg, float2 lxp, float2 lyp, float2 q[2]) {
+    const float2 dx = __fadd2_rn(__fadd2_rn(lxp, f2(-sg.mxh)), f2(-sg.mxl));
+    const float2 dy = __fadd2_rn(__fadd2_rn(lyp, f2(-sg.myh)), f2(-sg.myl));
+    const float2 t = __fmul2_rn(f2(sg.l21), dy);
+    const float2 w = __fmul2_rn(f2(sg.l22), dy);
+    const float2 ww = __fmul2_rn(w, w);
+    const float2 u0 = __ffma2_rn(f2(sg.l11), dx, f2(t.x)), u1 = __ffma2_rn(f2(sg.l11), dx, f2(t.y));
+    q[0] = __ffma2_rn(u0, u0, f2(ww.x));
+    q[1] = __ffma2_rn(u1, u1, f2(ww.y));
 }
 
 // Conservative test whether some point of the pixel-centre rectangle
@@ -108,19 +111,24 @@ __device__ __forceinline__ bool rect_reaches(float mx, float my, float l11, floa
 // alpha >= theta of the quad pixels in `need` (bit s); fills al / om / ef for
 // them: om = 1 - alpha, ef = bound on |om - (1 - alpha_ref)|.  Pixels inside
 // the bracket are re-decided with the reference formula in fp64 (rare).
-__device__ __forceinline__ uint32_t quad_alphas(const Staged &sg, const float q[4], int x0, int y0, uint32_t need,
-                                                const Workspace &ws, double th64, float al[4], float om[4],
-                                                float ef[4], uint32_t &n_redecide) {
+__device__ __forceinline__ uint32_t quad_alphas(const Staged &sg, const float2 q[2], int x0, int y0, uint32_t need,
+                                                const Workspace &ws, double th64, float2 al[2], float2 om[2],
+                                                float2 ef[2], uint32_t &n_redecide) {
     uint32_t pass = 0, amb = 0, hi = 0;
 #pragma unroll
-    for (int s = 0; s < 4; s++) {
-        const float e = sg.o * ex2_approx(-q[s]);
-        al[s] = fminf(e, (float)kAlphaClamp);
-        om[s] = 1.0f - al[s];
-        ef[s] = fmaf(al[s], fmaf(sg.e1, q[s], sg.e0), 6.0e-8f);
-        hi |= (e > 0.5f ? 1u : 0u) << s;
-        pass |= (q[s] < sg.q_lo ? 1u : 0u) << s;
-        amb |= (q[s] >= sg.q_lo && q[s] <= sg.q_hi ? 1u : 0u) << s;
+    for (int r = 0; r < 2; r++) {
+        const float2 e = __fmul2_rn(f2(sg.o), make_float2(ex2_approx(-q[r].x), ex2_approx(-q[r].y)));
+        al[r] = make_float2(fminf(e.x, (float)kAlphaClamp), fminf(e.y, (float)kAlphaClamp));
+        om[r] = __ffma2_rn(al[r], f2(-1.0f), f2(1.0f));
+        ef[r] = __ffma2_rn(al[r], __ffma2_rn(f2(sg.e1), q[r], f2(sg.e0)), f2(6.0e-8f));
+#pragma unroll
+        for (int c = 0; c < 2; c++) {
+            const int s = 2 * r + c;
+            const float qs = lane_of(q[r], c);
+            hi |= (lane_of(e, c) > 0.5f ? 1u : 0u) << s;
+            pass |= (qs < sg.q_lo ? 1u : 0u) << s;
+            amb |= (qs >= sg.q_lo && qs <= sg.q_hi ? 1u : 0u) << s;
+        }
     }
     hi &= need;
     if (__any_sync(0xffffffffu, hi != 0u)) {
@@ -129,12 +137,15 @@ __device__ __forceinline__ uint32_t quad_alphas(const Staged &sg, const float q[
 #pragma unroll
         for (int s = 0; s < 4; s++) {
             if (!((hi >> s) & 1u)) continue;
-            const float e = sg.o * ex2_approx(-q[s]);
-            if (e >= 0.99f * (1.0f + 4.0f * fmaf(sg.e1, q[s], sg.e0))) {
-                om[s] = (float)(1.0 - kAlphaClamp);
-                ef[s] = 1.0e-9f;
-            } else if (al[s] < (float)kAlphaClamp) {
-                const float x = 0.69314718f * q[s];  // 1 - e^-x, x < ln 2
+            const int r = s >> 1, c = s & 1;
+            const float qs = lane_of(q[r], c), als = lane_of(al[r], c);
+            const float e = sg.o * ex2_approx(-qs);
+            float oms = lane_of(om[r], c), efs = lane_of(ef[r], c);
+            if (e >= 0.99f * (1.0f + 4.0f * fmaf(sg.e1, qs, sg.e0))) {
+                oms = (float)(1.0 - kAlphaClamp);
+                efs = 1.0e-9f;
+            } else if (als < (float)kAlphaClamp) {
+                const float x = 0.69314718f * qs;  // 1 - e^-x, x < ln 2
                 float em = fmaf(-x, 1.0f / 362880.0f, 1.0f / 40320.0f);
                 em = fmaf(-x, em, 1.0f / 5040.0f);
                 em = fmaf(-x, em, 1.0f / 720.0f);
@@ -144,9 +155,10 @@ __device__ __forceinline__ uint32_t quad_alphas(const Staged &sg, const float q[
                 em = fmaf(-x, em, 0.5f);
                 em = fmaf(-x, em, 1.0f);
                 em *= x;
-                om[s] = fmaf(sg.o, em, sg.om_o);
-                ef[s] = fmaf(6.2e-7f, om[s], al[s] * fmaf(sg.e1, q[s], sg.e0));
+                oms = fmaf(sg.o, em, sg.om_o);
+                efs = fmaf(6.2e-7f, oms, als * fmaf(sg.e1, qs, sg.e0));
             }
+            if (c) { om[r].y = oms; ef[r].y = efs; } else { om[r].x = oms; ef[r].x = efs; }
         }
     }
     amb &= need;
@@ -156,11 +168,11 @@ __device__ __forceinline__ uint32_t quad_alphas(const Staged &sg, const float q[
 #pragma unroll
         for (int s = 0; s < 4; s++) {
             if (!((amb >> s) & 1u)) continue;
-            const double a64 = alpha64((double)(x0 + (s & 1)) + 0.5, (double)(y0 + (s >> 1)) + 0.5, m.x, m.y, co.x,
-                                       co.y, co.z, co.w);
-            al[s] = (float)a64;
-            om[s] = (float)(1.0 - a64);
-            ef[s] = 1.0e-9f;
+            const int r = s >> 1, c = s & 1;
+            const double a64 = alpha64((double)(x0 + c) + 0.5, (double)(y0 + r) + 0.5, m.x, m.y, co.x, co.y, co.z,
+                                       co.w);
+            const float a32 = (float)a64, o32 = (float)(1.0 - a64);
+            if (c) { al[r].y = a32; om[r].y = o32; ef[r].y = 1.0e-9f; } else { al[r].x = a32; om[r].x = o32; ef[r].x = 1.0e-9f; }
             pass |= (a64 >= th64 ? 1u : 0u) << s;
             n_redecide++;
         }
@@ -278,6 +290,7 @@ __global__ void __launch_bounds__(64, 8) k_raster_quad(Workspace ws, const uint3
         if (x0 + (s & 1) < cam.width && y0 + (s >> 1) < cam.height) valid |= 1u << s;
     uint32_t live = valid;  // bit s: pixel s not done (out-of-image pixels start done)
     const float lx0 = 2 * bx + 0.5f, ly0 = 2 * by + 0.5f;  // tile-relative centre of pixel 0
+    const float2 lxp = make_float2(lx0, lx0 + 1.0f), lyp = make_float2(ly0, ly0 + 1.0f);
     // w = 4: the group is the 2x2 of quads whose top-left quad holds the leader pixel
     const int g_off = (i & 2);
     const int leader_lane = (lane & ~7) + g_off;
@@ -287,12 +300,13 @@ __global__ void __launch_bounds__(64, 8) k_raster_quad(Workspace ws, const uint3
     const float gm = (float)cfg.gamma;
     Quad st;
 #pragma unroll
-    for (int s = 0; s < 4; s++) {
-        st.T[s] = 1.0f;
-        st.D[s] = 0.0f;
-        st.C[s][0] = st.C[s][1] = st.C[s][2] = 0.0f;
-        st.cnt[s] = 0;
+    for (int r = 0; r < 2; r++) {
+        st.T[r] = f2(1.0f);
+        st.D[r] = f2(0.0f);
+        st.C[r][0] = st.C[r][1] = st.C[r][2] = f2(0.0f);
     }
+#pragma unroll
+    for (int s = 0; s < 4; s++) st.cnt[s] = 0;
     // CR group leader pixel (rasterize.py:235-246): top-left pixel of the w x w group
     const int lead_x = W == 4 ? ox + 4 * (bx >> 1) : x0, lead_y = W == 4 ? oy + 4 * (by >> 1) : y0;
     // Per pixel: number of tile splats it was live for (its death step); out-of-image pixels 0.
@@ -367,8 +381,8 @@ __global__ void __launch_bounds__(64, 8) k_raster_quad(Workspace ws, const uint3
             jprev = j;
             const uint32_t step = b0 + (uint32_t)j - rg.x + 1u;  // tile splats processed including this one
             const Staged &sg = s_g[j];
-            float q[4], al[4], om[4], ef[4];
-            quad_q(sg, lx0, ly0, q);
+            float2 q[2], al[2], om[2], ef[2];
+            quad_q(sg, lxp, lyp, q);
             uint32_t blend;
             if (W == 0 || W == 1) {
                 blend = quad_alphas(sg, q, x0, y0, live, ws, th64, al, om, ef, n_redecide);
@@ -381,7 +395,7 @@ __global__ void __launch_bounds__(64, 8) k_raster_quad(Workspace ws, const uint3
                 const bool glive = W == 2 ? live != 0u : (lb & gmask) != 0u;
                 bool lpass = false;
                 float al0 = 0.f, om0 = 1.f, ef0 = 0.f;
-                if (leader_thread && glive) lpass = pixel_alpha(sg, q[0], x0, y0, ws, th64, al0, om0, ef0, n_redecide);
+                if (leader_thread && glive) lpass = pixel_alpha(sg, q[0].x, x0, y0, ws, th64, al0, om0, ef0, n_redecide);
                 const unsigned pb = __ballot_sync(0xffffffffu, lpass);
                 c_alpha += slice_any(pb, shift);
                 blend = 0u;
@@ -390,9 +404,9 @@ __global__ void __launch_bounds__(64, 8) k_raster_quad(Workspace ws, const uint3
                     const uint32_t mine = leader_thread ? 1u : 0u;  // slot 0 is this thread's leader pixel
                     blend = quad_alphas(sg, q, x0, y0, my_pass ? (live & ~mine) : 0u, ws, th64, al, om, ef, n_redecide);
                     if (leader_thread) {
-                        al[0] = al0;
-                        om[0] = om0;
-                        ef[0] = ef0;
+                        al[0].x = al0;
+                        om[0].x = om0;
+                        ef[0].x = ef0;
                         blend |= (my_pass && (live & 1u)) ? 1u : 0u;  // leader pixel: lpass is its own alpha test
                     }
                 }
@@ -402,26 +416,32 @@ __global__ void __launch_bounds__(64, 8) k_raster_quad(Workspace ws, const uint3
             c_blend += slice_any(bb, shift);
             uint32_t near = 0;
 #pragma unroll
-            for (int s = 0; s < 4; s++) {  // _blend (rasterize.py:169-177), predicated per pixel
-                const bool on = (blend >> s) & 1u;
-                const float t0 = st.T[s];
-                const float wgt = on ? t0 * al[s] : 0.0f;
-                st.C[s][0] = fmaf(wgt, sg.r, st.C[s][0]);
-                st.C[s][1] = fmaf(wgt, sg.g, st.C[s][1]);
-                st.C[s][2] = fmaf(wgt, sg.b, st.C[s][2]);
-                const float t1 = t0 * om[s];
-                const float d1 = fmaf(st.D[s], om[s], t0 * ef[s]);
-                st.T[s] = on ? t1 : t0;
-                st.D[s] = on ? d1 : st.D[s];
-                st.cnt[s] += on ? 1 : 0;
-                near |= (on && t1 - d1 < gm ? 1u : 0u) << s;  // T may be below gamma: decide below
+            for (int r = 0; r < 2; r++) {  // _blend (rasterize.py:169-177) on a pixel pair, masked by 0/1 factors
+                const bool b0 = (blend >> (2 * r)) & 1u, b1 = (blend >> (2 * r + 1)) & 1u;
+                const float2 m = make_float2(b0 ? 1.0f : 0.0f, b1 ? 1.0f : 0.0f);
+                const float2 nm = make_float2(b0 ? 0.0f : 1.0f, b1 ? 0.0f : 1.0f);
+                const float2 t0 = st.T[r];
+                const float2 wgt = __fmul2_rn(t0, __fmul2_rn(al[r], m));  // T alpha, or 0
+                st.C[r][0] = __ffma2_rn(wgt, f2(sg.r), st.C[r][0]);
+                st.C[r][1] = __ffma2_rn(wgt, f2(sg.g), st.C[r][1]);
+                st.C[r][2] = __ffma2_rn(wgt, f2(sg.b), st.C[r][2]);
+                const float2 omm = __ffma2_rn(om[r], m, nm);  // 1 - alpha (exactly), or 1
+                const float2 t1 = __fmul2_rn(t0, omm);
+                const float2 d1 = __ffma2_rn(st.D[r], omm, __fmul2_rn(t0, __fmul2_rn(ef[r], m)));
+                st.T[r] = t1;
+                st.D[r] = d1;
+                const float2 lo = __fadd2_rn(t1, make_float2(-d1.x, -d1.y));
+                near |= ((lo.x < gm ? 1u : 0u) | (lo.y < gm ? 2u : 0u)) << (2 * r);
             }
+#pragma unroll
+            for (int s = 0; s < 4; s++) st.cnt[s] += (blend >> s) & 1u;
+            near &= blend;  // T may be below gamma: decide below
             if (__any_sync(0xffffffffu, near != 0u)) {
                 uint32_t amb = 0;
 #pragma unroll
                 for (int s = 0; s < 4; s++) {
                     if (!((near >> s) & 1u)) continue;
-                    if (st.T[s] + st.D[s] < gm) {  // surely below: done (rasterize.py:177)
+                    if (lane_of(st.T[s >> 1], s & 1) + lane_of(st.D[s >> 1], s & 1) < gm) {  // surely below: done
                         live &= ~(1u << s);
                         di[s] = step;
                     } else {
@@ -446,8 +466,13 @@ __global__ void __launch_bounds__(64, 8) k_raster_quad(Workspace ws, const uint3
 #pragma unroll
                         for (int ss = 0; ss < 4; ss++) {
                             if (ss != s) continue;
-                            st.T[ss] = (float)T;
-                            st.D[ss] = 6.0e-8f * (float)T;
+                            if (ss & 1) {
+                                st.T[ss >> 1].y = (float)T;
+                                st.D[ss >> 1].y = 6.0e-8f * (float)T;
+                            } else {
+                                st.T[ss >> 1].x = (float)T;
+                                st.D[ss >> 1].x = 6.0e-8f * (float)T;
+                            }
                             if (T < cfg.gamma) {
                                 live &= ~(1u << ss);
                                 di[ss] = step;
@@ -491,9 +516,11 @@ __global__ void __launch_bounds__(64, 8) k_raster_quad(Workspace ws, const uint3
     for (int s = 0; s < 4; s++) {
         if (!((valid >> s) & 1u)) continue;
         const long long pix = (long long)(y0 + (s >> 1)) * cam.width + x0 + (s & 1);
-        image[3 * pix + 0] = fmaf(st.T[s], (float)cfg.bg[0], st.C[s][0]);  // background (rasterize.py:228-231)
-        image[3 * pix + 1] = fmaf(st.T[s], (float)cfg.bg[1], st.C[s][1]);
-        image[3 * pix + 2] = fmaf(st.T[s], (float)cfg.bg[2], st.C[s][2]);
+        const int r = s >> 1, c = s & 1;
+        const float T = lane_of(st.T[r], c);
+        image[3 * pix + 0] = fmaf(T, (float)cfg.bg[0], lane_of(st.C[r][0], c));  // background (rasterize.py:228-231)
+        image[3 * pix + 1] = fmaf(T, (float)cfg.bg[1], lane_of(st.C[r][1], c));
+        image[3 * pix + 2] = fmaf(T, (float)cfg.bg[2], lane_of(st.C[r][2], c));
         if (contrib) contrib[pix] = st.cnt[s];
     }
     if (i == 0) {
