@@ -63,7 +63,7 @@ __device__ __forceinline__ uint32_t slice_any(unsigned ballot, int shift) { retu
 // FADD2, per-element round-to-nearest: bit-identical to scalar fmaf).
 struct Quad {
     float2 T[2], D[2], C[2][3];
-    int cnt[4];
+    float2 cnt[2];  // blends per pixel (exact in fp32 below 2^24)
 };
 
 __device__ __forceinline__ float2 f2(float v) { return make_float2(v, v); }
@@ -305,17 +305,20 @@ __global__ void __launch_bounds__(64, 8) k_raster_quad(Workspace ws, const uint3
         st.D[r] = f2(0.0f);
         st.C[r][0] = st.C[r][1] = st.C[r][2] = f2(0.0f);
     }
-#pragma unroll
-    for (int s = 0; s < 4; s++) st.cnt[s] = 0;
+    st.cnt[0] = st.cnt[1] = f2(0.0f);
     // CR group leader pixel (rasterize.py:235-246): top-left pixel of the w x w group
     const int lead_x = W == 4 ? ox + 4 * (bx >> 1) : x0, lead_y = W == 4 ? oy + 4 * (by >> 1) : y0;
     // Per pixel: number of tile splats it was live for (its death step); out-of-image pixels 0.
     // The reference charges a model-warp's alpha_eval (ref) / leader_eval (cr) once per splat while
     // any of its pixels is live, i.e. the max death step over its pixels.
-    uint32_t di[4];
+    __shared__ uint32_t s_di[64][4];  // per pixel: tile splats it was live for (written at its death)
+    uint32_t *di = s_di[tid];
 #pragma unroll
     for (int s = 0; s < 4; s++) di[s] = ((valid >> s) & 1u) ? 0xffffffffu : 0u;
     uint32_t c_alpha = 0, c_blend = 0, n_redecide = 0, n_tamb = 0, n_skip = 0;
+#ifdef SEELE_RASTER_PROFILE
+    uint32_t pr_steps = 0, pr_member = 0, pr_blend = 0, pr_near = 0, pr_hi = 0;
+#endif
     const uint2 rg = ws.ranges[tile];
 
     Staged *s_g = s_stage[warp];
@@ -381,6 +384,9 @@ __global__ void __launch_bounds__(64, 8) k_raster_quad(Workspace ws, const uint3
             jprev = j;
             const uint32_t step = b0 + (uint32_t)j - rg.x + 1u;  // tile splats processed including this one
             const Staged &sg = s_g[j];
+#ifdef SEELE_RASTER_PROFILE
+            pr_steps++;
+#endif
             float2 q[2], al[2], om[2], ef[2];
             quad_q(sg, lxp, lyp, q);
             uint32_t blend;
@@ -391,35 +397,35 @@ __global__ void __launch_bounds__(64, 8) k_raster_quad(Workspace ws, const uint3
                     c_alpha += slice_any(pb, shift);
                 }
             } else {
-                // leader phase: the leader pixel's alpha counts even if that pixel is done (rasterize.py:281)
+                // One alpha evaluation of all four pixels serves both phases (the member phase runs on ~95 % of
+                // steps): the leader pixel's alpha counts even if that pixel is done (rasterize.py:281), the
+                // members blend if live, their group's leader passed and their own alpha passes.
                 const bool glive = W == 2 ? live != 0u : (lb & gmask) != 0u;
-                bool lpass = false;
-                float al0 = 0.f, om0 = 1.f, ef0 = 0.f;
-                if (leader_thread && glive) lpass = pixel_alpha(sg, q[0].x, x0, y0, ws, th64, al0, om0, ef0, n_redecide);
+                const uint32_t lbit = (leader_thread && glive) ? 1u : 0u;
+                const uint32_t pass = quad_alphas(sg, q, x0, y0, live | lbit, ws, th64, al, om, ef, n_redecide);
+                const bool lpass = (pass & lbit) != 0u;
                 const unsigned pb = __ballot_sync(0xffffffffu, lpass);
                 c_alpha += slice_any(pb, shift);
-                blend = 0u;
-                if (pb != 0u) {  // member phase (rasterize.py:283-289), skipped when no leader of the warp passed
-                    const bool my_pass = (pb >> (W == 2 ? lane : leader_lane)) & 1u;
-                    const uint32_t mine = leader_thread ? 1u : 0u;  // slot 0 is this thread's leader pixel
-                    blend = quad_alphas(sg, q, x0, y0, my_pass ? (live & ~mine) : 0u, ws, th64, al, om, ef, n_redecide);
-                    if (leader_thread) {
-                        al[0].x = al0;
-                        om[0].x = om0;
-                        ef[0].x = ef0;
-                        blend |= (my_pass && (live & 1u)) ? 1u : 0u;  // leader pixel: lpass is its own alpha test
-                    }
-                }
+                const bool my_pass = (pb >> (W == 2 ? lane : leader_lane)) & 1u;
+                blend = my_pass ? (pass & live) : 0u;
             }
             const unsigned bb = __ballot_sync(0xffffffffu, blend != 0u);
             if (bb == 0u) continue;
+#ifdef SEELE_RASTER_PROFILE
+            pr_blend++;
+            pr_hi += __any_sync(0xffffffffu, (al[0].x > 0.5f) | (al[0].y > 0.5f) | (al[1].x > 0.5f) | (al[1].y > 0.5f)) ? 1 : 0;
+#endif
             c_blend += slice_any(bb, shift);
             uint32_t near = 0;
+            float2 m01[2];
 #pragma unroll
             for (int r = 0; r < 2; r++) {  // _blend (rasterize.py:169-177) on a pixel pair, masked by 0/1 factors
-                const bool b0 = (blend >> (2 * r)) & 1u, b1 = (blend >> (2 * r + 1)) & 1u;
-                const float2 m = make_float2(b0 ? 1.0f : 0.0f, b1 ? 1.0f : 0.0f);
-                const float2 nm = make_float2(b0 ? 0.0f : 1.0f, b1 ? 0.0f : 1.0f);
+                // 0/1 factors from the blend bits: (bit << 29) lands on the exponent of 1.0f (0x3f800000)
+                const uint32_t bl = blend >> (2 * r);
+                const float2 m = make_float2(__uint_as_float(0x3f800000u & (0u - (bl & 1u))),
+                                             __uint_as_float(0x3f800000u & (0u - ((bl >> 1) & 1u))));
+                const float2 nm = __ffma2_rn(m, f2(-1.0f), f2(1.0f));
+                m01[r] = m;
                 const float2 t0 = st.T[r];
                 const float2 wgt = __fmul2_rn(t0, __fmul2_rn(al[r], m));  // T alpha, or 0
                 st.C[r][0] = __ffma2_rn(wgt, f2(sg.r), st.C[r][0]);
@@ -434,9 +440,13 @@ __global__ void __launch_bounds__(64, 8) k_raster_quad(Workspace ws, const uint3
                 near |= ((lo.x < gm ? 1u : 0u) | (lo.y < gm ? 2u : 0u)) << (2 * r);
             }
 #pragma unroll
-            for (int s = 0; s < 4; s++) st.cnt[s] += (blend >> s) & 1u;
+            st.cnt[0] = __fadd2_rn(st.cnt[0], m01[0]);
+            st.cnt[1] = __fadd2_rn(st.cnt[1], m01[1]);
             near &= blend;  // T may be below gamma: decide below
             if (__any_sync(0xffffffffu, near != 0u)) {
+#ifdef SEELE_RASTER_PROFILE
+                pr_near++;
+#endif
                 uint32_t amb = 0;
 #pragma unroll
                 for (int s = 0; s < 4; s++) {
@@ -492,7 +502,7 @@ __global__ void __launch_bounds__(64, 8) k_raster_quad(Workspace ws, const uint3
     for (int s = 0; s < 4; s++) {
         if (di[s] == 0xffffffffu) di[s] = rg.y > rg.x ? rg.y - rg.x : 0u;
         n_live += di[s];
-        n_blend += (uint32_t)st.cnt[s];
+        n_blend += (uint32_t)lane_of(st.cnt[s >> 1], s & 1);
         mw_steps = max(mw_steps, di[s]);
     }
 #pragma unroll
@@ -504,6 +514,17 @@ __global__ void __launch_bounds__(64, 8) k_raster_quad(Workspace ws, const uint3
     const uint32_t w_live = __reduce_add_sync(0xffffffffu, n_live);
     const uint32_t w_blend = __reduce_add_sync(0xffffffffu, n_blend);
     const uint32_t w_skip = __reduce_add_sync(0xffffffffu, n_skip);
+#ifdef SEELE_RASTER_PROFILE
+    if (lane == 0) {  // debug build: warp-step counters in stats slots 11..15
+        unsigned long long *sp = (unsigned long long *)stats;
+        atomicAdd(sp + 11, (unsigned long long)pr_steps);
+        atomicAdd(sp + 12, (unsigned long long)pr_member);
+        atomicAdd(sp + 13, (unsigned long long)pr_blend);
+        atomicAdd(sp + 14, (unsigned long long)pr_near);
+        atomicAdd(sp + 15, (unsigned long long)pr_hi);
+    }
+    return;
+#endif
     if (lane == 0) {
         unsigned long long *sp = (unsigned long long *)stats;
         if (w_red) atomicAdd(sp + SEELE_STAT_ALPHA_REDECIDE, (unsigned long long)w_red);
@@ -521,7 +542,7 @@ __global__ void __launch_bounds__(64, 8) k_raster_quad(Workspace ws, const uint3
         image[3 * pix + 0] = fmaf(T, (float)cfg.bg[0], lane_of(st.C[r][0], c));  // background (rasterize.py:228-231)
         image[3 * pix + 1] = fmaf(T, (float)cfg.bg[1], lane_of(st.C[r][1], c));
         image[3 * pix + 2] = fmaf(T, (float)cfg.bg[2], lane_of(st.C[r][2], c));
-        if (contrib) contrib[pix] = st.cnt[s];
+        if (contrib) contrib[pix] = (int32_t)lane_of(st.cnt[r], c);
     }
     if (i == 0) {
         Counters k{c_alpha, c_blend, c_leader};

@@ -1,0 +1,89 @@
+"""Frame pipelining over CUDA streams for trajectory rendering.
+
+Frames of a camera trajectory are independent (the scene is read-only and
+every frame owns its workspace and outputs), so a trajectory renders with
+``depth`` frames in flight: slot ``k % depth`` issues frame ``k`` on its own
+stream with its own workspace, range table and output buffers.  The
+latency-bound stages of one frame (cluster lookup, radix passes, scans) then
+overlap the compute-bound raster of another on the same GPU, with no
+synchronisation between slots.  Each slot's stream orders reuse of its
+buffers; a slot's outputs stay valid until the slot is used again
+(``depth`` submissions later).
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import torch
+
+from . import _native
+from .model import CameraPose
+from .render import EngineConfig, FrameOutput, FrameRenderer
+from .residency import ResidentRenderer, _select_on_device
+
+
+@dataclass
+class _Slot:
+    renderer: FrameRenderer
+    stream: torch.cuda.Stream
+    sel_ids: torch.Tensor
+    ranges: torch.Tensor
+    image: torch.Tensor
+    contrib: torch.Tensor
+    stats: torch.Tensor
+    done: torch.cuda.Event
+
+
+class FramePipeline:
+    """Renders frames of a resident (clustered) scene ``depth`` at a time."""
+
+    def __init__(self, rr: ResidentRenderer, width: int, height: int, *, depth: int = 2,
+                 pair_capacity: int | None = None, contrib: bool = True):
+        if depth < 1:
+            raise ValueError("depth must be >= 1")
+        self.rr = rr
+        self.device = rr.device
+        self.size = (int(width), int(height))
+        self.slots: list[_Slot] = []
+        for _ in range(depth):
+            r = FrameRenderer(self.device)
+            r.reserve(rr.n_max, width, height, pair_capacity=pair_capacity)
+            self.slots.append(_Slot(
+                renderer=r,
+                stream=torch.cuda.Stream(self.device),
+                sel_ids=torch.empty(rr.m + 1, dtype=torch.int32, device=self.device),
+                ranges=torch.empty((rr.m + 2, 2), dtype=torch.int64, device=self.device),
+                image=torch.empty((height, width, 3), dtype=torch.float32, device=self.device),
+                contrib=torch.empty((height, width), dtype=torch.int32, device=self.device) if contrib else None,
+                stats=torch.zeros(_native.STAT_COUNT, dtype=torch.int64, device=self.device),
+                done=torch.cuda.Event()))
+        self._next = 0
+
+    @property
+    def depth(self) -> int:
+        return len(self.slots)
+
+    def wait_for(self, stream: torch.cuda.Stream) -> None:
+        """Make every slot stream wait for the work already queued on ``stream``."""
+        ev = torch.cuda.Event()
+        ev.record(stream)
+        for s in self.slots:
+            s.stream.wait_event(ev)
+
+    def join(self, stream: torch.cuda.Stream) -> None:
+        """Make ``stream`` wait for every frame submitted so far."""
+        for s in self.slots:
+            s.done.record(s.stream)
+            stream.wait_event(s.done)
+
+    def submit(self, cam: CameraPose, cfg: EngineConfig) -> FrameOutput:
+        """Queue one frame (cluster lookup + render) on the next slot; returns
+        its device outputs without synchronising."""
+        s = self.slots[self._next]
+        self._next = (self._next + 1) % len(self.slots)
+        rr = self.rr
+        _select_on_device(cam, rr.centroids, rr.m, rr.beta, rr.normalization, rr.chunks, s.sel_ids, s.ranges,
+                          s.stream)
+        return s.renderer.render(rr.scene, cam, cfg, ranges=s.ranges, n_ranges=rr.m + 2, n_max=rr.n_max,
+                                 image=s.image, contrib=s.contrib if s.contrib is not None else False,
+                                 stats=s.stats, stream=s.stream)
