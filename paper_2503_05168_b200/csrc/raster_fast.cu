@@ -267,7 +267,7 @@ __device__ __noinline__ double exact_transmittance(const Workspace &ws, const ui
 }
 
 template <int W>
-__global__ void __launch_bounds__(64, 8) k_raster_quad(Workspace ws, const uint32_t *__restrict__ pair_pos, CamK cam,
+__global__ void __launch_bounds__(64, 10) k_raster_quad(Workspace ws, const uint32_t *__restrict__ pair_pos, CamK cam,
                                                         CfgK cfg, float *image, int32_t *contrib, int64_t *stats) {
     __shared__ Staged s_stage[2][kBatch];  // per warp: each warp stages and walks the list on its own
     const int tile = blockIdx.x;
