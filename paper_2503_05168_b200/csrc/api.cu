@@ -143,6 +143,8 @@ Workspace carve_workspace(void *base, long long n_max, long long cap, int width,
     w.long_runs = c.take<uint2>(kLongRunsMax);
     w.dval[0] = c.take<uint32_t>(n);
     w.dval[1] = c.take<uint32_t>(n);
+    w.drect[0] = c.take<uint32_t>(n);
+    w.drect[1] = c.take<uint32_t>(n);
     w.poff = c.take<uint32_t>(n + 1);
     w.tile_r0 = c.take<uint32_t>(cap / kSortTile + 2);
     w.ent_x = c.take<uint32_t>(cap);

@@ -150,6 +150,7 @@ __global__ void __launch_bounds__(NT, 2) k_depth_pass(Workspace ws, int pass) {
     RankSmem &rs = *reinterpret_cast<RankSmem *>(smem);
     uint32_t *skey = reinterpret_cast<uint32_t *>(smem + sizeof(RankSmem));
     uint32_t *sval = skey + TILE;
+    uint32_t *srect = sval + TILE;
     __shared__ uint32_t s_base[RADIX];
 #ifdef SEELE_SORT_TRACE
     const unsigned long long t_enter = gtime();
@@ -163,7 +164,7 @@ __global__ void __launch_bounds__(NT, 2) k_depth_pass(Workspace ws, int pass) {
 #endif
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int shift = 8 * pass;
-    uint32_t key[IPT], val[IPT], dig[IPT], pos[IPT];
+    uint32_t key[IPT], val[IPT], rcv[IPT], dig[IPT], pos[IPT];
     const uint32_t ib = t0 + warp * 32 * IPT + lane;
     if (pass == 0) {
         const DepthKey dk = depth_key(ws);
@@ -179,15 +180,19 @@ __global__ void __launch_bounds__(NT, 2) k_depth_pass(Workspace ws, int pass) {
         for (int r = 0; r < IPT; r++) {
             key[r] = depth_quant(dk, tl[r], d[r]);
             val[r] = ib + r * 32;
+            rcv[r] = (uint32_t)(tl[r].x & 0xff) | ((uint32_t)(tl[r].y & 0xff) << 8) | ((uint32_t)(tl[r].z & 0xff) << 16) |
+                     ((uint32_t)(tl[r].w & 0xff) << 24);
         }
     } else {
         const uint32_t *kin = ws.dkey[(pass + 1) & 1];
         const uint32_t *vin = ws.dval[(pass + 1) & 1];
+        const uint32_t *rin = ws.drect[(pass + 1) & 1];
 #pragma unroll
         for (int r = 0; r < IPT; r++) {
             const uint32_t i = min(ib + r * 32, n - 1);
             key[r] = kin[i];
             val[r] = vin[i];
+            rcv[r] = rin[i];
         }
     }
 #pragma unroll
@@ -213,21 +218,32 @@ __global__ void __launch_bounds__(NT, 2) k_depth_pass(Workspace ws, int pass) {
         if (dig[r] == NO_DIGIT) continue;
         skey[pos[r]] = key[r];
         sval[pos[r]] = val[r];
+        srect[pos[r]] = rcv[r];
     }
     __syncthreads();
     const int nv = (int)min((uint32_t)TILE, n - t0);
     uint32_t *kout = ws.dkey[pass & 1];
     uint32_t *vout = ws.dval[pass & 1];
+    uint32_t *rout = ws.drect[pass & 1];
     for (int i = tid; i < nv; i += NT) {
         const uint32_t k = skey[i];
         const uint32_t dst = s_base[(k >> shift) & 0xffu] + (uint32_t)i;
         kout[dst] = k;
         vout[dst] = sval[i];
+        rout[dst] = srect[i];
     }
 #ifdef SEELE_SORT_TRACE
     __syncthreads();
     TRACE(pass, t, 4)
 #endif
+}
+
+__device__ __forceinline__ short4 unpack_rect(uint32_t v) {
+    return make_short4((short)(v & 0xff), (short)((v >> 8) & 0xff), (short)((v >> 16) & 0xff), (short)(v >> 24));
+}
+__device__ __forceinline__ uint32_t pack_rect(short4 r) {
+    return (uint32_t)(r.x & 0xff) | ((uint32_t)(r.y & 0xff) << 8) | ((uint32_t)(r.z & 0xff) << 16) |
+           ((uint32_t)(r.w & 0xff) << 24);
 }
 
 // (fp64 depth, position) order inside one run of equal quantised keys.
@@ -266,12 +282,16 @@ __global__ void __launch_bounds__(256) k_depth_fixup(Workspace ws, const int64_t
             continue;
         }
         const int m = (int)(e - i);
+        uint32_t *rs = ws.drect[kDepthFinal];
         if (m == 2) {  // the common case: one pair, in registers
             const uint32_t p0 = val[i], p1 = val[i + 1];
             const double d0 = ws.depth[p0], d1 = ws.depth[p1];
             if (depth_less(d1, p1, d0, p0)) {
+                const uint32_t r0 = rs[i];
                 val[i] = p1;
                 val[i + 1] = p0;
+                rs[i] = rs[i + 1];
+                rs[i + 1] = r0;
             }
             continue;
         }
@@ -296,7 +316,10 @@ __global__ void __launch_bounds__(256) k_depth_fixup(Workspace ws, const int64_t
             d[z + 1] = dq;
         }
         if (moved)
-            for (int q = 0; q < m; q++) val[i + q] = p[q];
+            for (int q = 0; q < m; q++) {
+                val[i + q] = p[q];
+                rs[i + q] = pack_rect(ws.rect[p[q]]);
+            }
     }
 }
 
@@ -327,6 +350,7 @@ __global__ void __launch_bounds__(512) k_depth_fix_long(Workspace ws) {
                 uint32_t r = 0;
                 for (uint32_t k = 0; k < m; k++) r += depth_less(s_d[k], s_p[k], dj, pj);
                 val[s + r] = pj;
+                ws.drect[kDepthFinal][s + r] = pack_rect(ws.rect[pj]);
             }
             __syncthreads();
         } else {
@@ -341,7 +365,10 @@ __global__ void __launch_bounds__(512) k_depth_fix_long(Workspace ws) {
                 spare[s + r] = pj;
             }
             __syncthreads();
-            for (uint32_t j = threadIdx.x; j < m; j += blockDim.x) val[s + j] = spare[s + j];
+            for (uint32_t j = threadIdx.x; j < m; j += blockDim.x) {
+                val[s + j] = spare[s + j];
+                ws.drect[kDepthFinal][s + j] = pack_rect(ws.rect[spare[s + j]]);
+            }
             __syncthreads();
         }
     }
@@ -378,21 +405,23 @@ __global__ void __launch_bounds__(NT) k_pair_scan(Workspace ws, int tiles_x, int
     if (tid == 0) s_pairs = 0ull;
     int32_t *diff = use_smem ? s_diff : ws.tile_diff;
     const uint32_t n = (uint32_t)stats[SEELE_STAT_BINNED];
-    const uint32_t *sorted = ws.dval[kDepthFinal];
+    const uint32_t *srect = ws.drect[kDepthFinal];
     const uint32_t n_etiles = (uint32_t)(cap / TILE) + 1u;  // tile_r0 entries kept (capacity)
     unsigned long long my_pairs = 0ull;
     while (true) {
         const uint32_t t = take_ticket(&ws.counters[CNT_TICKET + kLookScan]);
         if (t * TILE >= n) break;
         const uint32_t r0 = t * TILE + tid * IPT;
-        uint32_t h[IPT];
+        uint32_t h[IPT], rr[IPT];
         uint32_t sum = 0;
+#pragma unroll
+        for (int k = 0; k < IPT; k++) rr[k] = srect[min(r0 + k, n - 1)];  // coalesced: rects in rank order
 #pragma unroll
         for (int k = 0; k < IPT; k++) {
             h[k] = 0u;
             const uint32_t r = r0 + k;
             if (r < n) {
-                const short4 rc = ws.rect[sorted[r]];
+                const short4 rc = unpack_rect(rr[k]);
                 const int w = rc.y - rc.x + 1, hh = rc.w - rc.z + 1;
                 const int nseg = (w + kSegW - 1) / kSegW;  // row entries are split into <= kSegW columns
                 h[k] = (uint32_t)(hh * nseg);
@@ -558,10 +587,8 @@ __global__ void __launch_bounds__(NT, 2) k_row_pass(Workspace ws, int64_t *stats
     for (int k = tid; k <= nr; k += NT) {
         S.u.e.off[k] = ws.poff[r0 + k];
         if (k < nr) {
-            const uint32_t p = sorted[r0 + k];
-            const short4 rc = ws.rect[p];
-            S.u.e.pos[k] = p;
-            S.u.e.rect[k] = (uint32_t)rc.x | ((uint32_t)rc.y << 8) | ((uint32_t)rc.z << 16);
+            S.u.e.pos[k] = sorted[r0 + k];
+            S.u.e.rect[k] = ws.drect[kDepthFinal][r0 + k] & 0xffffffu;  // x0 | x1 << 8 | y0 << 16
         }
     }
     __syncthreads();
@@ -842,7 +869,7 @@ void launch_frame_begin(const Workspace &ws, const CamK &cam, int64_t *stats, cu
 void launch_depth_sort(const Workspace &ws, long long n_max, int64_t *stats, cudaStream_t st) {
     const int hist_grid = (int)std::min<long long>(ceil_div(n_max, 256 * 8), 4 * 148);
     k_depth_hist<<<hist_grid > 0 ? hist_grid : 1, 256, 0, st>>>(ws);
-    const size_t smem = sizeof(RankSmem) + 2 * sizeof(uint32_t) * TILE;
+    const size_t smem = sizeof(RankSmem) + 3 * sizeof(uint32_t) * TILE;
     set_smem(k_depth_pass, smem);
     const int grid = (int)ceil_div(n_max, TILE);
     for (int p = 0; p < kDepthPasses; p++) k_depth_pass<<<grid, NT, smem, st>>>(ws, p);

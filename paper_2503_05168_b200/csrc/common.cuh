@@ -82,6 +82,7 @@ struct Workspace {
     // value = assembled position; the sorted order ends in dkey/dval[kDepthFinal]
     uint32_t *dkey[2];
     uint32_t *dval[2];
+    uint32_t *drect[2];  // tile rect carried with each item: x0 | x1 << 8 | y0 << 16 | y1 << 24
     uint2 *long_runs;    // [kLongRunsMax] (start, length) of long equal-key runs
     // first row entry of each depth-ranked binned splat (+ sentinel) and first
     // rank of each 4096-entry tile of the row pass

@@ -69,7 +69,7 @@ int main(int argc, char **argv) {
     int64_t *stats;
     CK(cudaMalloc(&stats, sizeof(int64_t) * SEELE_STAT_COUNT));
     CK(cudaMemcpy(ws.depth, depth.data(), 8 * n, cudaMemcpyHostToDevice));
-    CK(cudaMemcpy(ws.tiles, tiles.data(), 4 * n, cudaMemcpyHostToDevice));
+
     CK(cudaMemcpy(ws.rect, rect.data(), 8 * n, cudaMemcpyHostToDevice));
     cudaStream_t st;
     CK(cudaStreamCreate(&st));
