@@ -76,6 +76,9 @@ class FramePipeline:
             s.done.record(s.stream)
             stream.wait_event(s.done)
 
+    def slot_of_next(self) -> int:
+        return self._next
+
     def submit(self, cam: CameraPose, cfg: EngineConfig) -> FrameOutput:
         """Queue one frame (cluster lookup + render) on the next slot; returns
         its device outputs without synchronising."""
@@ -87,3 +90,43 @@ class FramePipeline:
         return s.renderer.render(rr.scene, cam, cfg, ranges=s.ranges, n_ranges=rr.m + 2, n_max=rr.n_max,
                                  image=s.image, contrib=s.contrib if s.contrib is not None else False,
                                  stats=s.stats, stream=s.stream)
+
+
+class TrajectoryRenderer:
+    """Host-facing trajectory rendering: frames are pipelined on the device
+    (FramePipeline) and each frame's image, contributor counts and stats are
+    copied into pinned host buffers on its slot's stream, so the device->host
+    transfer of frame k overlaps the rendering of frames k+1 .. k+depth-1.
+    ``run`` yields ``(index, image, contrib, stats)`` numpy views into pinned
+    buffers; they stay valid until the next item is requested."""
+
+    def __init__(self, rr: ResidentRenderer, width: int, height: int, *, depth: int = 2,
+                 pair_capacity: int | None = None):
+        self.pipe = FramePipeline(rr, width, height, depth=depth, pair_capacity=pair_capacity)
+        self.host = [(torch.empty((height, width, 3), dtype=torch.float32, pin_memory=True),
+                      torch.empty((height, width), dtype=torch.int32, pin_memory=True),
+                      torch.empty(_native.STAT_COUNT, dtype=torch.int64, pin_memory=True),
+                      torch.cuda.Event()) for _ in range(depth)]
+
+    def run(self, cams, cfg: EngineConfig):
+        pending = []  # (index, slot)
+        for i, cam in enumerate(cams):
+            k = self.pipe.slot_of_next()
+            if len(pending) == self.pipe.depth:  # oldest frame must be consumed before its slot is reused
+                j, ks = pending.pop(0)
+                img, cnt, st, ev = self.host[ks]
+                ev.synchronize()
+                yield j, img.numpy(), cnt.numpy(), st.numpy()
+            out = self.pipe.submit(cam, cfg)
+            s = self.pipe.slots[k]
+            img, cnt, st, ev = self.host[k]
+            with torch.cuda.stream(s.stream):
+                st.copy_(out.stats, non_blocking=True)
+                img.copy_(out.image, non_blocking=True)
+                cnt.copy_(out.contrib, non_blocking=True)
+                ev.record(s.stream)
+            pending.append((i, k))
+        for j, ks in pending:
+            img, cnt, st, ev = self.host[ks]
+            ev.synchronize()
+            yield j, img.numpy(), cnt.numpy(), st.numpy()

@@ -131,6 +131,21 @@ class ResidentRenderer:
         res.stats.resident_bytes = self.resident_bytes
         return res
 
+    def render_trajectory(self, cams, cfg: EngineConfig, *, depth: int = 2, pair_capacity: int | None = None):
+        """Render a camera trajectory with ``depth`` frames in flight (B200
+        extension of render_frame for trajectories): yields ``(index, image
+        float32 (H,W,3), contributor counts int32 (H,W), stats int64)`` host
+        views, valid until the next item is requested.  Frames
+        whose tile pairs overflow ``pair_capacity`` are reported through
+        their stats (``SEELE_STAT_OVERFLOW``); size the capacity first."""
+        from .pipeline import TrajectoryRenderer
+        cams = list(cams)
+        if not cams:
+            return
+        w, h = int(cams[0].width), int(cams[0].height)
+        tr = TrajectoryRenderer(self, w, h, depth=depth, pair_capacity=pair_capacity)
+        yield from tr.run(cams, cfg)
+
     def close(self) -> None:
         pass
 
