@@ -366,7 +366,7 @@ def run_ours(args):
             "value_serial": value_serial, "frames_in_flight": args.depth,
             "vs_baseline": None, "dtype": "fp64+fp32", "data": "synthetic",
             "config": {**workload_config(args, container), "parallelism": f"frame-sharded x{size}"},
-            "roofline": {"kernel": "k_raster_quad + k_fixup (raster stage)", "bound": "fp32",
+            "roofline": {"kernel": "k_raster_quad (raster stage)", "bound": "fp32",
                          "achieved": round(r_tflops, 3), "peak": round(fp32_tflops, 1), "unit": "TFLOP/s",
                          "frac": round(r_tflops / fp32_tflops, 4),
                          "peak_source": f"nominal 148 SM x 128 FP32 lanes x 2 x {sm_mhz:.0f} MHz (no FP32 peak in "
