@@ -145,6 +145,16 @@ int seele_render(const seele_scene *scene, const int64_t *ranges_dev, int32_t n_
                  size_t workspace_bytes, int64_t n_max, int64_t pair_capacity, float *image_dev,
                  int32_t *contrib_dev, int64_t *stats_dev, void *stream);
 
+/* seele_render with the raster (the last stage) issued on raster_stream
+ * after the plan stages on `stream` (ordered by an event).  Lets a caller
+ * with several frames in flight give the latency-bound plan stages a
+ * higher stream priority than the issue-bound raster of another frame.
+ * raster_stream == NULL: same as seele_render. */
+int seele_render_split(const seele_scene *scene, const int64_t *ranges_dev, int32_t n_ranges,
+                       const seele_camera *cam, const seele_config *cfg, void *workspace,
+                       size_t workspace_bytes, int64_t n_max, int64_t pair_capacity, float *image_dev,
+                       int32_t *contrib_dev, int64_t *stats_dev, void *stream, void *raster_stream);
+
 /* select_clusters (residency.py:38-54) on device: nearest 1+m centroids
  * (fp64 squared distance in pose_feature space, compiler.py:113-121; ties
  * toward the smaller id) and the working-set range table for them:

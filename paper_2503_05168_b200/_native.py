@@ -43,6 +43,7 @@ MAX_RANGES = 64
 EXPORTED_SYMBOLS = (
     "seele_workspace_bytes",
     "seele_render",
+    "seele_render_split",
     "seele_select_clusters",
     "seele_plan_export",
     "seele_profile_enable",
@@ -118,6 +119,8 @@ def load(required: bool = True):
     lib.seele_workspace_bytes.restype = ctypes.c_size_t
     lib.seele_render.argtypes = [P, P, I32, P, P, P, ctypes.c_size_t, I64, I64, P, P, P, P]
     lib.seele_render.restype = ctypes.c_int
+    lib.seele_render_split.argtypes = [P, P, I32, P, P, P, ctypes.c_size_t, I64, I64, P, P, P, P, P]
+    lib.seele_render_split.restype = ctypes.c_int
     lib.seele_select_clusters.argtypes = [P, P, I32, I32, ctypes.c_double, P, ctypes.c_double, P, P, P, P]
     lib.seele_select_clusters.restype = ctypes.c_int
     lib.seele_plan_export.argtypes = [P, I64, I64, I32, I32, I64, I64, P, P]

@@ -23,6 +23,16 @@ inline void prof_mark(int i, cudaStream_t st) {
     if (g_prof) cudaEventRecord(g_ev[i], st);
 }
 
+// Small per-thread ring of events for cross-stream ordering (reuse is safe:
+// cudaStreamWaitEvent captures the event's state when it is called).
+cudaEvent_t next_event() {
+    thread_local cudaEvent_t ring[16] = {};
+    thread_local int at = 0;
+    at = (at + 1) & 15;
+    if (!ring[at] && cudaEventCreateWithFlags(&ring[at], cudaEventDisableTiming) != cudaSuccess) return nullptr;
+    return ring[at];
+}
+
 int fail(int code, const char *fmt, ...) {
     va_list ap;
     va_start(ap, fmt);
@@ -224,9 +234,10 @@ size_t seele_workspace_bytes(int64_t n_max, int64_t pair_capacity, int32_t width
     return carve_workspace(nullptr, n_max, pair_capacity, width, height).bytes;
 }
 
-int seele_render(const seele_scene *scene, const int64_t *ranges_dev, int32_t n_ranges, const seele_camera *cam,
-                 const seele_config *cfg, void *workspace, size_t workspace_bytes, int64_t n_max,
-                 int64_t pair_capacity, float *image_dev, int32_t *contrib_dev, int64_t *stats_dev, void *stream) {
+int seele_render_split(const seele_scene *scene, const int64_t *ranges_dev, int32_t n_ranges, const seele_camera *cam,
+                       const seele_config *cfg, void *workspace, size_t workspace_bytes, int64_t n_max,
+                       int64_t pair_capacity, float *image_dev, int32_t *contrib_dev, int64_t *stats_dev, void *stream,
+                       void *raster_stream) {
     g_err[0] = 0;
     int rc;
     if ((rc = check_camera(cam)) != SEELE_OK) return rc;
@@ -284,10 +295,25 @@ int seele_render(const seele_scene *scene, const int64_t *ranges_dev, int32_t n_
     prof_mark(2, st);
     launch_binning(ws, n_max, pair_capacity, ck, stats_dev, st);
     prof_mark(3, st);
-    launch_raster(ws, ws.pfinal, ck, cf, image_dev, contrib_dev, stats_dev, st);
-    prof_mark(4, st);
+    cudaStream_t rst = raster_stream ? static_cast<cudaStream_t>(raster_stream) : st;
+    if (rst != st) {  // raster on its own stream, after the plan
+        cudaEvent_t ev = next_event();
+        if (!ev) return fail(SEELE_ERR_CUDA, "could not create a CUDA event");
+        if ((e = cudaEventRecord(ev, st)) != cudaSuccess) return cuda_fail(e, "seele_render_split event");
+        if ((e = cudaStreamWaitEvent(rst, ev, 0)) != cudaSuccess) return cuda_fail(e, "seele_render_split wait");
+        prof_mark(3, rst);
+    }
+    launch_raster(ws, ws.pfinal, ck, cf, image_dev, contrib_dev, stats_dev, rst);
+    prof_mark(4, rst);
     if ((e = cudaGetLastError()) != cudaSuccess) return cuda_fail(e, "seele_render launch");
     return SEELE_OK;
+}
+
+int seele_render(const seele_scene *scene, const int64_t *ranges_dev, int32_t n_ranges, const seele_camera *cam,
+                 const seele_config *cfg, void *workspace, size_t workspace_bytes, int64_t n_max,
+                 int64_t pair_capacity, float *image_dev, int32_t *contrib_dev, int64_t *stats_dev, void *stream) {
+    return seele_render_split(scene, ranges_dev, n_ranges, cam, cfg, workspace, workspace_bytes, n_max, pair_capacity,
+                              image_dev, contrib_dev, stats_dev, stream, nullptr);
 }
 
 int seele_profile_enable(int32_t on) {

@@ -25,7 +25,9 @@ from .residency import ResidentRenderer, _select_on_device
 @dataclass
 class _Slot:
     renderer: FrameRenderer
-    stream: torch.cuda.Stream
+    stream: torch.cuda.Stream          # plan stages (high priority)
+    raster_stream: torch.cuda.Stream   # raster (low priority)
+    free: torch.cuda.Event             # the slot's last raster finished
     sel_ids: torch.Tensor
     ranges: torch.Tensor
     image: torch.Tensor
@@ -38,7 +40,7 @@ class FramePipeline:
     """Renders frames of a resident (clustered) scene ``depth`` at a time."""
 
     def __init__(self, rr: ResidentRenderer, width: int, height: int, *, depth: int = 2,
-                 pair_capacity: int | None = None, contrib: bool = True):
+                 pair_capacity: int | None = None, contrib: bool = True, split: bool = False):
         if depth < 1:
             raise ValueError("depth must be >= 1")
         self.rr = rr
@@ -48,9 +50,12 @@ class FramePipeline:
         for _ in range(depth):
             r = FrameRenderer(self.device)
             r.reserve(rr.n_max, width, height, pair_capacity=pair_capacity)
+            least, greatest = torch.cuda.Stream.priority_range()  # lower number = higher priority
             self.slots.append(_Slot(
                 renderer=r,
-                stream=torch.cuda.Stream(self.device),
+                stream=torch.cuda.Stream(self.device, priority=greatest if split else 0),
+                raster_stream=torch.cuda.Stream(self.device, priority=least if split else 0),
+                free=torch.cuda.Event(),
                 sel_ids=torch.empty(rr.m + 1, dtype=torch.int32, device=self.device),
                 ranges=torch.empty((rr.m + 2, 2), dtype=torch.int64, device=self.device),
                 image=torch.empty((height, width, 3), dtype=torch.float32, device=self.device),
@@ -58,6 +63,7 @@ class FramePipeline:
                 stats=torch.zeros(_native.STAT_COUNT, dtype=torch.int64, device=self.device),
                 done=torch.cuda.Event()))
         self._next = 0
+        self.split = split
 
     @property
     def depth(self) -> int:
@@ -69,12 +75,18 @@ class FramePipeline:
         ev.record(stream)
         for s in self.slots:
             s.stream.wait_event(ev)
+            s.raster_stream.wait_event(ev)
 
     def join(self, stream: torch.cuda.Stream) -> None:
         """Make ``stream`` wait for every frame submitted so far."""
         for s in self.slots:
-            s.done.record(s.stream)
+            s.done.record(s.raster_stream if self.split else s.stream)
             stream.wait_event(s.done)
+
+    def output_stream(self, k: int) -> torch.cuda.Stream:
+        """Stream on which slot k's outputs are complete."""
+        s = self.slots[k]
+        return s.raster_stream if self.split else s.stream
 
     def slot_of_next(self) -> int:
         return self._next
@@ -85,11 +97,17 @@ class FramePipeline:
         s = self.slots[self._next]
         self._next = (self._next + 1) % len(self.slots)
         rr = self.rr
+        if self.split:  # the slot's workspace and outputs are reused: wait for its previous raster
+            s.stream.wait_event(s.free)
         _select_on_device(cam, rr.centroids, rr.m, rr.beta, rr.normalization, rr.chunks, s.sel_ids, s.ranges,
                           s.stream)
-        return s.renderer.render(rr.scene, cam, cfg, ranges=s.ranges, n_ranges=rr.m + 2, n_max=rr.n_max,
-                                 image=s.image, contrib=s.contrib if s.contrib is not None else False,
-                                 stats=s.stats, stream=s.stream)
+        out = s.renderer.render(rr.scene, cam, cfg, ranges=s.ranges, n_ranges=rr.m + 2, n_max=rr.n_max,
+                                image=s.image, contrib=s.contrib if s.contrib is not None else False,
+                                stats=s.stats, stream=s.stream,
+                                raster_stream=s.raster_stream if self.split else None)
+        if self.split:
+            s.free.record(s.raster_stream)
+        return out
 
 
 class TrajectoryRenderer:
@@ -118,13 +136,13 @@ class TrajectoryRenderer:
                 ev.synchronize()
                 yield j, img.numpy(), cnt.numpy(), st.numpy()
             out = self.pipe.submit(cam, cfg)
-            s = self.pipe.slots[k]
             img, cnt, st, ev = self.host[k]
-            with torch.cuda.stream(s.stream):
+            ostream = self.pipe.output_stream(k)
+            with torch.cuda.stream(ostream):
                 st.copy_(out.stats, non_blocking=True)
                 img.copy_(out.image, non_blocking=True)
                 cnt.copy_(out.contrib, non_blocking=True)
-                ev.record(s.stream)
+                ev.record(ostream)
             pending.append((i, k))
         for j, ks in pending:
             img, cnt, st, ev = self.host[ks]

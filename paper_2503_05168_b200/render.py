@@ -211,8 +211,10 @@ class FrameRenderer:
     def render(self, scene: DeviceScene, cam: CameraPose, cfg: EngineConfig, *, ranges: torch.Tensor | None = None,
                n_ranges: int = 1, n_max: int | None = None, image: torch.Tensor | None = None,
                contrib: torch.Tensor | bool = True, stats: torch.Tensor | None = None,
-               stream: torch.cuda.Stream | None = None) -> FrameOutput:
-        """Asynchronous frame on ``stream`` (default: current stream)."""
+               stream: torch.cuda.Stream | None = None,
+               raster_stream: torch.cuda.Stream | None = None) -> FrameOutput:
+        """Asynchronous frame on ``stream`` (default: current stream); with
+        ``raster_stream`` the raster is issued there after the plan stages."""
         w, h = int(cam.width), int(cam.height)
         n_max = int(n_max or scene.n)
         self.reserve(n_max, w, h)
@@ -231,10 +233,11 @@ class FrameRenderer:
         sc = scene.struct()
         camc = _native.camera_struct(cam)
         cfgc = _native.config_struct(cfg)
-        _native.check(self.lib.seele_render(
+        _native.check(self.lib.seele_render_split(
             ctypes.byref(sc), ranges.data_ptr(), int(n_ranges), ctypes.byref(camc), ctypes.byref(cfgc),
             self.workspace.data_ptr(), self.workspace.numel(), self.n_max, self.pair_capacity, image.data_ptr(),
-            contrib.data_ptr() if contrib is not None else None, stats.data_ptr(), st.cuda_stream))
+            contrib.data_ptr() if contrib is not None else None, stats.data_ptr(), st.cuda_stream,
+            raster_stream.cuda_stream if raster_stream is not None else None))
         return FrameOutput(image=image, contrib=contrib, stats=stats)
 
     def render_checked(self, scene: DeviceScene, cam: CameraPose, cfg: EngineConfig, **kw) -> tuple[FrameOutput, np.ndarray]:

@@ -82,3 +82,26 @@ def test_working_set_is_reference_order(synthetic_container):
     sel = rr.select(poses[10])
     np.testing.assert_array_equal(rr.working_set_ids(sel), rr.assemble(sel).ids)
     assert len(sel) == 1 + c.m
+
+
+@pytest.mark.parametrize("depth", [1, 2, 3])
+def test_trajectory_pipeline_matches_serial(synthetic_container, depth):
+    """Frames in flight on separate streams (FramePipeline / render_trajectory)
+    give exactly the per-frame results of the serial path."""
+    d, poses = synthetic_container
+    rr = ResidentRenderer(str(d))
+    cfg = EngineConfig(engine="cr", group_w=2)
+    frames = [3, 17, 40, 41, 77, 100, 119]
+    want = {}
+    for f in frames:
+        res = rr.render_frame(poses[f], cfg, output="numpy32")
+        want[f] = (res.image.copy(), res.contrib_count.copy(), [getattr(res.stats, k) for k in STAT_KEYS])
+    got = 0
+    for i, img, cnt, st in rr.render_trajectory([poses[f] for f in frames], cfg, depth=depth,
+                                                pair_capacity=4_000_000):
+        w_img, w_cnt, w_st = want[frames[i]]
+        np.testing.assert_array_equal(img, w_img)
+        np.testing.assert_array_equal(cnt, w_cnt)
+        assert [int(st[k]) for k in range(len(STAT_KEYS))] == w_st
+        got += 1
+    assert got == len(frames)
