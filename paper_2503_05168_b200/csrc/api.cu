@@ -129,6 +129,7 @@ void note_launches(int n) { g_launches.fetch_add(n, std::memory_order_relaxed); 
 Workspace carve_workspace(void *base, long long n_max, long long cap, int width, int height) {
     Carver c{static_cast<char *>(base)};
     Workspace w;
+    w.stats_ptr = nullptr;
     const long long n = n_max > 0 ? n_max : 1;
     const int tiles_x = (width + kTile - 1) / kTile, tiles_y = (height + kTile - 1) / kTile;
     const long long tiles = (long long)tiles_x * tiles_y;
@@ -257,9 +258,10 @@ int seele_render_split(const seele_scene *scene, const int64_t *ranges_dev, int3
     if (n_max < 1 || n_max >= (1ll << 30) || pair_capacity < 1 || pair_capacity >= (1ll << 30))
         return fail(SEELE_ERR_INVALID_ARGUMENT, "n_max / pair_capacity out of range");
     if (!workspace || !image_dev || !stats_dev) return fail(SEELE_ERR_INVALID_ARGUMENT, "null output or workspace");
-    const Workspace ws = carve_workspace(workspace, n_max, pair_capacity, cam->width, cam->height);
+    Workspace ws = carve_workspace(workspace, n_max, pair_capacity, cam->width, cam->height);
     if (ws.bytes > workspace_bytes)
         return fail(SEELE_ERR_INVALID_ARGUMENT, "workspace too small (need %lld bytes)", (long long)ws.bytes);
+    ws.stats_ptr = stats_dev;
 
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     const CamK ck = make_cam(*cam);

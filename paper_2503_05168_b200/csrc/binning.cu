@@ -108,6 +108,7 @@ __global__ void __launch_bounds__(256) k_depth_hist(Workspace ws) {
 #pragma unroll
         for (int u = 0; u < U; u++) {
             if (i0 + u * 256 >= n) break;
+            if (tl[u].x > tl[u].y) continue;  // not binned: dropped by the sort
             const uint32_t key = depth_quant(k, tl[u], d[u]);
 #pragma unroll
             for (int p = 0; p < kDepthPasses; p++) atomicAdd(&h[p][(key >> (8 * p)) & 0xffu], 1u);
@@ -156,7 +157,8 @@ __global__ void __launch_bounds__(NT, 2) k_depth_pass(Workspace ws, int pass) {
     const unsigned long long t_enter = gtime();
 #endif
     const uint32_t t = take_ticket(&ws.counters[CNT_TICKET + kLookDepth + pass]);
-    const uint32_t n = ws.counters[CNT_WS];
+    // pass 0 reads every assembled splat and keeps the binned ones; later passes sort only those
+    const uint32_t n = pass == 0 ? ws.counters[CNT_WS] : (uint32_t)ws.counters_binned();
     const uint32_t t0 = t * TILE;
     if (t0 >= n) return;
 #ifdef SEELE_SORT_TRACE
@@ -196,7 +198,8 @@ __global__ void __launch_bounds__(NT, 2) k_depth_pass(Workspace ws, int pass) {
         }
     }
 #pragma unroll
-    for (int r = 0; r < IPT; r++) dig[r] = ib + r * 32 < n ? (key[r] >> shift) & 0xffu : NO_DIGIT;
+    for (int r = 0; r < IPT; r++)
+        dig[r] = ib + r * 32 < n && key[r] != 0xffffffu ? (key[r] >> shift) & 0xffu : NO_DIGIT;
 #ifdef SEELE_SORT_TRACE
     __syncthreads();
     TRACE(pass, t, 1)
@@ -221,7 +224,7 @@ __global__ void __launch_bounds__(NT, 2) k_depth_pass(Workspace ws, int pass) {
         srect[pos[r]] = rcv[r];
     }
     __syncthreads();
-    const int nv = (int)min((uint32_t)TILE, n - t0);
+    const int nv = (int)rs.total;  // ranked (binned) items of this tile
     uint32_t *kout = ws.dkey[pass & 1];
     uint32_t *vout = ws.dval[pass & 1];
     uint32_t *rout = ws.drect[pass & 1];

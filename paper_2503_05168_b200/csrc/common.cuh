@@ -108,6 +108,9 @@ struct Workspace {
     unsigned long long *pairs64;  // total tile pairs (u64)
     size_t bytes;
 
+    int64_t *stats_ptr;  // the frame's stats vector (set by seele_render)
+    __device__ __forceinline__ long long counters_binned() const { return stats_ptr[SEELE_STAT_BINNED]; }
+
     __device__ __forceinline__ unsigned long long *look_region(int pass) const {
         if (pass < kLookScan) return look + (size_t)pass * look_tiles_d * 256;
         if (pass == kLookScan) return look + (size_t)kDepthPasses * look_tiles_d * 256;

@@ -129,6 +129,7 @@ __device__ __forceinline__ T block_scan(T v, T &total) {
 struct RankSmem {
     uint32_t cnt[NT / 32][RADIX];  // per-warp digit counters -> per-warp exclusive offsets
     uint32_t start[RADIX];         // first slot of each digit in the sorted tile
+    uint32_t total;                // ranked items in the tile
 };
 
 // Stable in-tile ranking.  Item (warp w, round r, lane l) is tile item
@@ -167,6 +168,7 @@ __device__ __forceinline__ void block_rank(const uint32_t (&dig)[IPT], uint32_t 
     uint32_t all;
     const uint32_t st = block_scan<uint32_t>(tid < RADIX ? total : 0u, all);
     if (tid < RADIX) sm.start[tid] = st;
+    if (tid == 0) sm.total = all;
     __syncthreads();
 #pragma unroll
     for (int r = 0; r < IPT; r++)

@@ -65,9 +65,10 @@ int main(int argc, char **argv) {
     void *base;
     CK(cudaMalloc(&base, bytes));
     CK(cudaMemset(base, 0, bytes));
-    const Workspace ws = carve_workspace(base, n, cap, W, H);
+    Workspace ws = carve_workspace(base, n, cap, W, H);
     int64_t *stats;
     CK(cudaMalloc(&stats, sizeof(int64_t) * SEELE_STAT_COUNT));
+    ws.stats_ptr = stats;
     CK(cudaMemcpy(ws.depth, depth.data(), 8 * n, cudaMemcpyHostToDevice));
 
     CK(cudaMemcpy(ws.rect, rect.data(), 8 * n, cudaMemcpyHostToDevice));
