@@ -230,11 +230,21 @@ __device__ __forceinline__ void flush_block(const Workspace &ws, int64_t *stats,
     }
 }
 
+__device__ __forceinline__ void cp_async16(void *smem, const void *gmem) {
+    const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+
 template <int LAYOUT>
 __global__ void __launch_bounds__(256, 3) k_preprocess(SceneK sc, const int64_t *__restrict__ ranges,
                                                     int n_ranges, CamK cam, CfgK cfg, Workspace ws,
                                                     int64_t *stats) {
     __shared__ long long s_start[SEELE_MAX_RANGES], s_prefix[SEELE_MAX_RANGES + 1];
+    // SH planes of this thread's splat, copied asynchronously (cp.async / LDGSTS) at the top of each
+    // iteration so the transfer overlaps the fp64 projection; plane k of thread t at [k][t]
+    extern __shared__ float4 s_sh[];
     if (threadIdx.x == 0) {
         long long acc = 0;
         for (int r = 0; r < n_ranges; r++) {
@@ -262,6 +272,13 @@ __global__ void __launch_bounds__(256, 3) k_preprocess(SceneK sc, const int64_t 
             int r = 0;
             while (r + 1 < n_ranges && s_prefix[r + 1] <= p) r++;
             const long long i = s_start[r] + (p - s_prefix[r]);
+            if (LAYOUT == SEELE_LAYOUT_PLANES) {
+                for (int k = 0; k < 3 * sh_planes; k++) {
+                    const int plane = 3 + 4 * (k / sh_planes) + (k % sh_planes);
+                    cp_async16(&s_sh[k * 256 + threadIdx.x], sc.planes + plane * sc.plane_stride + i);
+                }
+                cp_async_commit();
+            }
             Splat g;
             load_splat<LAYOUT>(sc, i, sh_planes, g);
             double d[3] = {g.p[0] - cam.pos[0], g.p[1] - cam.pos[1], g.p[2] - cam.pos[2]};
@@ -318,13 +335,14 @@ __global__ void __launch_bounds__(256, 3) k_preprocess(SceneK sc, const int64_t 
                     if (LAYOUT == SEELE_LAYOUT_PLANES) {
                         // SH planes are read only for projected splats, one channel (4 x float4) at a time
                         float cc3[3];
+                        cp_async_wait_all();
 #pragma unroll
                         for (int ch = 0; ch < 3; ch++) {
                             float shc[16];
 #pragma unroll
                             for (int k = 0; k < 4; k++) {
                                 float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-                                if (k < sh_planes) v = __ldg(sc.planes + (3 + 4 * ch + k) * sc.plane_stride + i);
+                                if (k < sh_planes) v = s_sh[(ch * sh_planes + k) * 256 + threadIdx.x];
                                 shc[4 * k] = v.x;
                                 shc[4 * k + 1] = v.y;
                                 shc[4 * k + 2] = v.z;
@@ -372,6 +390,7 @@ __global__ void __launch_bounds__(256, 3) k_preprocess(SceneK sc, const int64_t 
             ws.status[p] = (uint8_t)status;
             ws.rect[p] = rect;
         }
+        if (LAYOUT == SEELE_LAYOUT_PLANES) cp_async_wait_all();  // slots are reused next iteration
         cnt[0] += status == 1;
         cnt[1] += status == 2;
         cnt[2] += status == 0;
@@ -428,8 +447,15 @@ __global__ void k_select(CamK cam, const double *__restrict__ centroids, int n, 
 
 void launch_preprocess(const SceneK &s, const int64_t *ranges, int n_ranges, const CamK &cam,
                        const CfgK &cfg, const Workspace &ws, int64_t *stats, int grid, cudaStream_t st) {
-    if (s.layout == SEELE_LAYOUT_PLANES)
-        k_preprocess<SEELE_LAYOUT_PLANES><<<grid, 256, 0, st>>>(s, ranges, n_ranges, cam, cfg, ws, stats);
+    if (s.layout == SEELE_LAYOUT_PLANES) {
+        constexpr int kShSmem = 12 * 256 * sizeof(float4);
+        static bool attr = false;
+        if (!attr) {
+            cudaFuncSetAttribute(k_preprocess<SEELE_LAYOUT_PLANES>, cudaFuncAttributeMaxDynamicSharedMemorySize, kShSmem);
+            attr = true;
+        }
+        k_preprocess<SEELE_LAYOUT_PLANES><<<grid, 256, kShSmem, st>>>(s, ranges, n_ranges, cam, cfg, ws, stats);
+    }
     else
         k_preprocess<SEELE_LAYOUT_F64><<<grid, 256, 0, st>>>(s, ranges, n_ranges, cam, cfg, ws, stats);
     note_launches(1);
