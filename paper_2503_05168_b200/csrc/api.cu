@@ -162,6 +162,7 @@ Workspace carve_workspace(void *base, long long n_max, long long cap, int width,
     w.ent_p = c.take<uint32_t>(cap);
     w.pfinal = c.take<uint32_t>(cap);
     w.ranges = c.take<uint2>(tiles);
+    w.tile_order = c.take<uint32_t>(tiles);
     w.dhist = c.take<uint32_t>(kDepthPasses * 256);
     w.row_start = c.take<uint32_t>(kMaxTileAxis + 2);
     w.chunk_first = c.take<uint32_t>(kMaxTileAxis + 2);

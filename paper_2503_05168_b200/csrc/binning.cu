@@ -521,10 +521,28 @@ __global__ void __launch_bounds__(NT) k_pair_scan(Workspace ws, int tiles_x, int
     for (int i = a0; i < a1; i++) part += (uint32_t)g[(i / tiles_x) * tx1 + i % tiles_x];
     uint32_t all;
     uint32_t acc = block_scan<uint32_t>(part, all);
+    __shared__ uint32_t s_bucket[33];
+    if (tid < 33) s_bucket[tid] = 0u;
+    __syncthreads();
     for (int i = a0; i < a1; i++) {
         const uint32_t c = (uint32_t)g[(i / tiles_x) * tx1 + i % tiles_x];
         ws.ranges[i] = over ? make_uint2(0u, 0u) : make_uint2(acc, acc + c);
         acc += c;
+        atomicAdd(&s_bucket[32 - (32 - __clz(c))], 1u);  // bucket 32 - bits(c): heavy tiles in low buckets
+    }
+    __syncthreads();
+    if (tid == 0) {  // exclusive scan over the 33 buckets
+        uint32_t run = 0;
+        for (int b = 0; b < 33; b++) {
+            const uint32_t v = s_bucket[b];
+            s_bucket[b] = run;
+            run += v;
+        }
+    }
+    __syncthreads();
+    for (int i = a0; i < a1; i++) {  // raster launch order (within a bucket arbitrary; results do not depend on it)
+        const uint32_t c = (uint32_t)g[(i / tiles_x) * tx1 + i % tiles_x];
+        ws.tile_order[atomicAdd(&s_bucket[32 - (32 - __clz(c))], 1u)] = (uint32_t)i;
     }
     // entries per row -> row bases (row pass digit bases) and column-pass chunks
     for (int i = tid; i <= tiles_y; i += NT) s_row[i] = *(volatile int32_t *)&ws.row_diff[i];

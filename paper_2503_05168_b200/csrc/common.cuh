@@ -94,6 +94,7 @@ struct Workspace {
     uint32_t *ent_p;
     uint32_t *pfinal;    // sorted pair -> assembled position (sort_intersections order)
     uint2 *ranges;       // per tile [start, end)
+    uint32_t *tile_order;  // raster launch order: tiles by descending pair count (heavy tiles first)
     // scratch
     unsigned long long *look;  // epoch-tagged look-back status words
     long long look_tiles_d, look_tiles_p;  // tiles per depth / pair pass region

@@ -270,7 +270,7 @@ template <int W>
 __global__ void __launch_bounds__(64, 10) k_raster_quad(Workspace ws, const uint32_t *__restrict__ pair_pos, CamK cam,
                                                         CfgK cfg, float *image, int32_t *contrib, int64_t *stats) {
     __shared__ Staged s_stage[2][kBatch];  // per warp: each warp stages and walks the list on its own
-    const int tile = blockIdx.x;
+    const int tile = (int)ws.tile_order[blockIdx.x];  // heavy tiles first (binning.cu k_pair_scan)
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int mw = tid >> 3, i = tid & 7;
     const int shift = lane & 24;  // byte of this model-warp in a warp ballot
