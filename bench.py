@@ -54,7 +54,7 @@ def parse():
     ap.add_argument("--flat", action="store_true", help="no cluster tables (whole scene every frame)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=60)
-    ap.add_argument("--depth", type=int, default=2, help="frames in flight (streams)")
+    ap.add_argument("--depth", type=int, default=3, help="frames in flight (streams)")
     return ap.parse_args()
 
 

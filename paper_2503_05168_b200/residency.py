@@ -143,8 +143,12 @@ class ResidentRenderer:
         if not cams:
             return
         w, h = int(cams[0].width), int(cams[0].height)
-        tr = TrajectoryRenderer(self, w, h, depth=depth, pair_capacity=pair_capacity)
-        yield from tr.run(cams, cfg)
+        key = (w, h, int(depth), pair_capacity)
+        tr = getattr(self, "_trajectory", None)
+        if tr is None or tr[0] != key:  # workspaces and pinned buffers are kept across calls
+            self._trajectory = None
+            tr = self._trajectory = (key, TrajectoryRenderer(self, w, h, depth=depth, pair_capacity=pair_capacity))
+        yield from tr[1].run(cams, cfg)
 
     def close(self) -> None:
         pass
