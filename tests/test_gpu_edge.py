@@ -1,0 +1,67 @@
+"""GPU edge cases of the sort / binning / raster path against the oracle:
+long runs of equal (and nearly equal) depths (the depth sort's exact fp64
+fix-up, including the CTA path for runs longer than 32), very wide splats
+(row entries split into 8-column segments), many tile rows and columns, and
+a frame with no binned splat."""
+import numpy as np
+import pytest
+
+from helpers import STAT_KEYS, psnr
+from oracle import oracle as O
+from paper_2503_05168_b200 import DeviceScene, EngineConfig, plan_frame, render_frame
+from paper_2503_05168_b200.model import SceneArrays
+from paper_2503_05168_b200.synthetic import make_camera, random_scene
+
+pytestmark = pytest.mark.gpu
+
+
+def _check(scene, cam, cfgs):
+    dscene = DeviceScene.from_arrays(scene)
+    for cfg in cfgs:
+        want = O.render(scene, cam, cfg)
+        res = render_frame(dscene, cam, cfg)
+        np.testing.assert_array_equal(res.contrib_count, want["contrib"])
+        assert [getattr(res.stats, k) for k in STAT_KEYS] == [want["stats"][k] for k in STAT_KEYS]
+        assert float(np.abs(res.image - want["image"]).max()) <= 1e-3
+        assert psnr(res.image, want["image"]) >= 50.0
+
+
+CFGS = (EngineConfig(engine="ref"), EngineConfig(engine="cr", group_w=2), EngineConfig(engine="cr", group_w=4))
+
+
+def _with_depths(scene, cam, depths):
+    """Move each splat along its view ray to the given camera depth."""
+    r = cam.rotation_matrix()
+    view = (r.T @ (scene.positions - cam.position).T).T
+    view = view * (depths / view[:, 2])[:, None]
+    pos = (r @ view.T).T + cam.position
+    return SceneArrays(pos, scene.log_scales, scene.rotations, scene.opacities, scene.sh, scene.ids)
+
+
+def test_equal_and_nearly_equal_depths():
+    cam = make_camera(160, 96)
+    rng = np.random.default_rng(21)
+    n = 6000
+    scene = random_scene(rng, n, sh_degree=2, camera=cam, opacity_range=(0.05, 0.7))
+    d = rng.uniform(2.0, 6.0, size=n)
+    d[:1500] = 3.0                                        # one long run of identical depths (> 32: CTA path)
+    d[1500:2500] = 4.0 + 1e-13 * rng.integers(0, 50, 1000)  # distinct depths inside one quantisation step
+    d[2500:2600] = d[2600:2700]                           # scattered pairs of exact ties
+    _check(_with_depths(scene, cam, d), cam, CFGS)
+
+
+def test_wide_splats_and_many_tiles():
+    cam = make_camera(1000, 720)  # 63 x 45 tiles
+    rng = np.random.default_rng(5)
+    scene = random_scene(rng, 4000, sh_degree=1, camera=cam, scale_range=(0.02, 0.9), opacity_range=(0.02, 0.8))
+    _check(scene, cam, CFGS[:2])
+    plan = plan_frame(DeviceScene.from_arrays(scene), cam, EngineConfig())
+    want = O.plan(scene, cam, EngineConfig())
+    np.testing.assert_array_equal(plan.sorted_pairs["tile_id"], want["pair_tile"])
+
+
+def test_no_binned_splat():
+    cam = make_camera(64, 48)
+    rng = np.random.default_rng(2)
+    scene = random_scene(rng, 50, camera=cam, opacity_range=(0.0005, 0.003))  # all below alpha_theta: r^2 = 0
+    _check(scene, cam, CFGS[:1])
