@@ -147,7 +147,9 @@ __global__ void __launch_bounds__(256) k_depth_hist(Workspace ws) {
 // One 8-bit pass of the depth sort.  Pass 0 builds its keys from the
 // preprocess outputs (value = assembled position).
 __global__ void __launch_bounds__(NT, 2) k_depth_pass(Workspace ws, int pass) {
-    extern __shared__ __align__(16) unsigned char smem[];
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    // every extern __shared__ array of this file aliases one symbol whose alignment may be 4: align here
+    unsigned char *smem = reinterpret_cast<unsigned char *>((reinterpret_cast<uintptr_t>(smem_raw) + 15) & ~uintptr_t(15));
     RankSmem &rs = *reinterpret_cast<RankSmem *>(smem);
     uint32_t *skey = reinterpret_cast<uint32_t *>(smem + sizeof(RankSmem));
     uint32_t *sval = skey + TILE;
@@ -890,7 +892,7 @@ void launch_frame_begin(const Workspace &ws, const CamK &cam, int64_t *stats, cu
 void launch_depth_sort(const Workspace &ws, long long n_max, int64_t *stats, cudaStream_t st) {
     const int hist_grid = (int)std::min<long long>(ceil_div(n_max, 256 * 8), 4 * 148);
     k_depth_hist<<<hist_grid > 0 ? hist_grid : 1, 256, 0, st>>>(ws);
-    const size_t smem = sizeof(RankSmem) + 3 * sizeof(uint32_t) * TILE;
+    const size_t smem = 16 + sizeof(RankSmem) + 3 * sizeof(uint32_t) * TILE;
     set_smem(k_depth_pass, smem);
     const int grid = (int)ceil_div(n_max, TILE);
     for (int p = 0; p < kDepthPasses; p++) k_depth_pass<<<grid, NT, smem, st>>>(ws, p);

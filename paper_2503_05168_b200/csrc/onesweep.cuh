@@ -126,7 +126,7 @@ __device__ __forceinline__ T block_scan(T v, T &total) {
 }
 
 // Per-CTA scratch of block_rank.
-struct RankSmem {
+struct __align__(16) RankSmem {
     uint32_t cnt[NT / 32][RADIX];  // per-warp digit counters -> per-warp exclusive offsets
     uint32_t start[RADIX];         // first slot of each digit in the sorted tile
     uint32_t total;                // ranked items in the tile
