@@ -300,30 +300,33 @@ __global__ void __launch_bounds__(256) k_depth_fixup(Workspace ws, const int64_t
             }
             continue;
         }
-        uint32_t p[32];
+        uint32_t p[32], rr[32];
         double d[32];
         for (int q = 0; q < m; q++) {
             p[q] = val[i + q];
-            d[q] = ws.depth[p[q]];
+            rr[q] = rs[i + q];
         }
+        for (int q = 0; q < m; q++) d[q] = ws.depth[p[q]];
         bool moved = false;
         for (int q = 1; q < m; q++) {
-            const uint32_t pq = p[q];
+            const uint32_t pq = p[q], rq = rr[q];
             const double dq = d[q];
             int z = q - 1;
             while (z >= 0 && depth_less(dq, pq, d[z], p[z])) {
                 p[z + 1] = p[z];
+                rr[z + 1] = rr[z];
                 d[z + 1] = d[z];
                 z--;
             }
             if (z + 1 != q) moved = true;
             p[z + 1] = pq;
+            rr[z + 1] = rq;
             d[z + 1] = dq;
         }
         if (moved)
             for (int q = 0; q < m; q++) {
                 val[i + q] = p[q];
-                rs[i + q] = pack_rect(ws.rect[p[q]]);
+                rs[i + q] = rr[q];
             }
     }
 }
@@ -890,7 +893,7 @@ void launch_frame_begin(const Workspace &ws, const CamK &cam, int64_t *stats, cu
 }
 
 void launch_depth_sort(const Workspace &ws, long long n_max, int64_t *stats, cudaStream_t st) {
-    const int hist_grid = (int)std::min<long long>(ceil_div(n_max, 256 * 8), 4 * 148);
+    const int hist_grid = (int)std::min<long long>(ceil_div(n_max, 256 * 8), 2 * 148);
     k_depth_hist<<<hist_grid > 0 ? hist_grid : 1, 256, 0, st>>>(ws);
     const size_t smem = 16 + sizeof(RankSmem) + 3 * sizeof(uint32_t) * TILE;
     set_smem(k_depth_pass, smem);
