@@ -387,7 +387,7 @@ __global__ void __launch_bounds__(512) k_depth_fix_long(Workspace ws) {
 // Row entries cover at most kSegW columns (wider ones are split; pieces of one
 // splat cover disjoint columns, so the per-column order is unaffected): the
 // column pass's per-entry loops stay short.
-constexpr uint32_t kSegW = 8;
+constexpr uint32_t kSegW = 4;
 
 // bin_tiles (preprocess.py:159-189) of splat rank r covers rect [x0,x1] x [y0,y1]
 // -> ceil(w / kSegW) row entries per covered tile row y and w * h pairs.
