@@ -52,17 +52,19 @@ def parse():
     ap.add_argument("--height", type=int, default=1080)
     ap.add_argument("--engine", default="cr2", choices=["ref", "cr1", "cr2", "cr4"])
     ap.add_argument("--flat", action="store_true", help="no cluster tables (whole scene every frame)")
+    ap.add_argument("--c1", action="store_true", help="BASELINE config 1 (100K random scene, one 256x256 view)")
+    ap.add_argument("--no-opacity-aware", action="store_true", help="plain 3-sigma binning (C5 'HP off')")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=60)
     ap.add_argument("--depth", type=int, default=3, help="frames in flight (streams)")
     return ap.parse_args()
 
 
-def engine_cfg(name: str, precision: str = "fast"):
+def engine_cfg(name: str, precision: str = "fast", opacity_aware: bool = True):
     from paper_2503_05168_b200.render import EngineConfig
     if name == "ref":
-        return EngineConfig(engine="ref", precision=precision)
-    return EngineConfig(engine="cr", group_w=int(name[2]), precision=precision)
+        return EngineConfig(engine="ref", precision=precision, opacity_aware_filter=opacity_aware)
+    return EngineConfig(engine="cr", group_w=int(name[2]), precision=precision, opacity_aware_filter=opacity_aware)
 
 
 def build_workload(args, device):
@@ -70,8 +72,14 @@ def build_workload(args, device):
     from paper_2503_05168_b200.container import container_from_table
     from paper_2503_05168_b200.synthetic import orbit, synth
     t0 = time.time()
-    scene = synth(args.n, 0)
-    poses = orbit(N_FRAMES, args.width, args.height)
+    if args.c1:  # BASELINE config 1: support.random_scene(default_rng(0), 100K, SH3) seen by make_camera(256, 256)
+        from paper_2503_05168_b200.synthetic import config1_scene
+        scene, cam = config1_scene()
+        args.n, args.width, args.height, args.flat = len(scene.positions), cam.width, cam.height, True
+        poses = [cam] * N_FRAMES
+    else:
+        scene = synth(args.n, 0)
+        poses = orbit(N_FRAMES, args.width, args.height)
     if args.flat:
         table = ClusterTable(shared_ids=np.arange(args.n), exclusive_ids=[np.zeros(0, np.int64)] * 2,
                              discarded_ids=np.zeros(0, np.int64), centroids=np.zeros((2, 6)), beta=1.0, neighbors=0,
@@ -163,7 +171,7 @@ def run_reference(args):
     from paper_2503_05168_b200.residency import ResidentRenderer
     device = torch.device("cuda", local) if torch.cuda.is_available() else None
     scene, poses, table, container, _ = build_workload(args, device)
-    cfg = engine_cfg(args.engine)
+    cfg = engine_cfg(args.engine, opacity_aware=not args.no_opacity_aware)
     # host-side cluster selection + assembly (residency.py:38-54, 217-220), no GPU involved
     from paper_2503_05168_b200.clusters import pose_feature
     norm = container.normalization
@@ -206,8 +214,10 @@ def workload_config(args, container) -> dict:
     return {
         "workload": ("C3: synthetic 3M-Gaussian scene (SURVEY App. C synth(3e6, 0)), 1920x1080, 120-frame orbit, "
                      "view-dependent cluster tables (24 clusters, M=4, beta=1), Seele engine (HP + CR w=2)")
-        if not args.flat and args.n == 3_000_000 else f"synth({args.n}) {args.width}x{args.height} "
-                                                       f"{'flat' if args.flat else 'clustered'}",
+        if not args.flat and args.n == 3_000_000 and not args.no_opacity_aware
+        else ("C1: support.random_scene(default_rng(0), 100K, SH3), one 256x256 view" if args.c1 else
+              f"synth({args.n}) {args.width}x{args.height} {'flat' if args.flat else 'clustered'}"
+              f"{' 3-sigma' if args.no_opacity_aware else ''}"),
         "gaussians": args.n, "width": args.width, "height": args.height, "engine": args.engine,
         "clusters": container.num_clusters, "neighbors": container.m,
         "shared_splats": int(container.chunks[0, 1]),
@@ -233,7 +243,7 @@ def run_ours(args):
     scene, poses, table, container, setup_s = build_workload(args, device)
     rr = ResidentRenderer(container, device=device)
     renderer = FrameRenderer(device)
-    cfg = engine_cfg(args.engine)
+    cfg = engine_cfg(args.engine, opacity_aware=not args.no_opacity_aware)
     lib = _native.load()
     my_frames = [(rank + size * k) % N_FRAMES for k in range(args.warmup + args.steps)]
 
