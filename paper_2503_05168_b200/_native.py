@@ -8,11 +8,13 @@ library is missing or no CUDA device is present, every render call raises
 from __future__ import annotations
 
 import ctypes
+import os
 from pathlib import Path
 
 from .errors import DeviceError, raise_for_status
 
-LIB_PATH = Path(__file__).resolve().parent / "libseele_b200.so"
+# SEELE_LIB: development override (A/B builds of the same library)
+LIB_PATH = Path(os.environ.get("SEELE_LIB") or Path(__file__).resolve().parent / "libseele_b200.so")
 ABI_VERSION = 1
 
 # enum indices of the device stats vector (seele_b200.h)

@@ -50,12 +50,14 @@ constexpr double kQ = 0.72134752044448170368;  // log2(e) / 2: q' = kQ q
 struct __align__(16) Staged {
     float mxh, mxl, myh, myl;  // tile-relative mean as hi + lo floats
     float l11, l21, l22, o;    // Cholesky factor of the conic in q' units; opacity
-    float q_lo, q_hi, e0, e1;  // alpha-test bracket in q'; alpha relative error model e0 + e1 q'
-    float r, g, b, om_o;       // colour; 1 - opacity
-    uint32_t p, pad[3];        // assembled position (fp64 re-decisions)
+    float q_lo, q_up, e0, e1;  // pass: q' < q_lo; fail: q' >= q_up (first float above the bracket); alpha error e0 + e1 q'
+    float r, g, b;             // colour
+    uint32_t p;                // assembled position (fp64 re-decisions)
 };
 
-__device__ __forceinline__ uint32_t slice_any(unsigned ballot, int shift) { return ((ballot >> shift) & 0xffu) != 0u; }
+__device__ __forceinline__ uint32_t fbits(float x) { return __float_as_uint(x); }
+// all-ones if the sign bit of x is set, else 0
+__device__ __forceinline__ uint32_t sign_mask(float x) { return (uint32_t)((int)__float_as_uint(x) >> 31); }
 
 // Quad state: four pixels, slot s = (x0 + (s & 1), y0 + (s >> 1)); the two
 // pixels of a quad row r = s >> 1 are one float2 (.x = left, .y = right) so
@@ -108,119 +110,6 @@ __device__ __forceinline__ bool rect_reaches(float mx, float my, float l11, floa
     return qmin <= qmax;
 }
 
-// alpha >= theta of the quad pixels in `need` (bit s); fills al / om / ef for
-// them: om = 1 - alpha, ef = bound on |om - (1 - alpha_ref)|.  Pixels inside
-// the bracket are re-decided with the reference formula in fp64 (rare).
-__device__ __forceinline__ uint32_t quad_alphas(const Staged &sg, const float2 q[2], int x0, int y0, uint32_t need,
-                                                const Workspace &ws, double th64, float2 al[2], float2 om[2],
-                                                float2 ef[2], uint32_t &n_redecide) {
-    uint32_t pass = 0, amb = 0, hi = 0;
-#pragma unroll
-    for (int r = 0; r < 2; r++) {
-        const float2 e = __fmul2_rn(f2(sg.o), make_float2(ex2_approx(-q[r].x), ex2_approx(-q[r].y)));
-        al[r] = make_float2(fminf(e.x, (float)kAlphaClamp), fminf(e.y, (float)kAlphaClamp));
-        om[r] = __ffma2_rn(al[r], f2(-1.0f), f2(1.0f));
-        ef[r] = __ffma2_rn(al[r], __ffma2_rn(f2(sg.e1), q[r], f2(sg.e0)), f2(6.0e-8f));
-#pragma unroll
-        for (int c = 0; c < 2; c++) {
-            const int s = 2 * r + c;
-            const float qs = lane_of(q[r], c);
-            hi |= (lane_of(e, c) > 0.5f ? 1u : 0u) << s;
-            pass |= (qs < sg.q_lo ? 1u : 0u) << s;
-            amb |= (qs >= sg.q_lo && qs <= sg.q_hi ? 1u : 0u) << s;
-        }
-    }
-    hi &= need;
-    if (__any_sync(0xffffffffu, hi != 0u)) {
-        // high alpha: 1 - alpha = (1 - o) + o (1 - 2^-q') keeps ~5e-7 relative accuracy (1 - alpha32
-        // would lose it by a factor alpha / (1 - alpha)); a surely clamped alpha is exactly 0.99
-#pragma unroll
-        for (int s = 0; s < 4; s++) {
-            if (!((hi >> s) & 1u)) continue;
-            const int r = s >> 1, c = s & 1;
-            const float qs = lane_of(q[r], c), als = lane_of(al[r], c);
-            const float e = sg.o * ex2_approx(-qs);
-            float oms = lane_of(om[r], c), efs = lane_of(ef[r], c);
-            if (e >= 0.99f * (1.0f + 4.0f * fmaf(sg.e1, qs, sg.e0))) {
-                oms = (float)(1.0 - kAlphaClamp);
-                efs = 1.0e-9f;
-            } else if (als < (float)kAlphaClamp) {
-                const float x = 0.69314718f * qs;  // 1 - e^-x, x < ln 2
-                float em = fmaf(-x, 1.0f / 362880.0f, 1.0f / 40320.0f);
-                em = fmaf(-x, em, 1.0f / 5040.0f);
-                em = fmaf(-x, em, 1.0f / 720.0f);
-                em = fmaf(-x, em, 1.0f / 120.0f);
-                em = fmaf(-x, em, 1.0f / 24.0f);
-                em = fmaf(-x, em, 1.0f / 6.0f);
-                em = fmaf(-x, em, 0.5f);
-                em = fmaf(-x, em, 1.0f);
-                em *= x;
-                oms = fmaf(sg.o, em, sg.om_o);
-                efs = fmaf(6.2e-7f, oms, als * fmaf(sg.e1, qs, sg.e0));
-            }
-            if (c) { om[r].y = oms; ef[r].y = efs; } else { om[r].x = oms; ef[r].x = efs; }
-        }
-    }
-    amb &= need;
-    if (amb) {  // inside the bracket: decide with the reference formula in fp64
-        const double2 m = ws.mean[sg.p];
-        const double4 co = ws.conic_op[sg.p];
-#pragma unroll
-        for (int s = 0; s < 4; s++) {
-            if (!((amb >> s) & 1u)) continue;
-            const int r = s >> 1, c = s & 1;
-            const double a64 = alpha64((double)(x0 + c) + 0.5, (double)(y0 + r) + 0.5, m.x, m.y, co.x, co.y, co.z,
-                                       co.w);
-            const float a32 = (float)a64, o32 = (float)(1.0 - a64);
-            if (c) { al[r].y = a32; om[r].y = o32; ef[r].y = 1.0e-9f; } else { al[r].x = a32; om[r].x = o32; ef[r].x = 1.0e-9f; }
-            pass |= (a64 >= th64 ? 1u : 0u) << s;
-            n_redecide++;
-        }
-    }
-    return pass & need;
-}
-
-// alpha >= theta of one pixel (the CR group leader, slot 0 of its quad),
-// same arithmetic as quad_alphas.
-__device__ __forceinline__ bool pixel_alpha(const Staged &sg, float q, int px, int py, const Workspace &ws,
-                                            double th64, float &al, float &om, float &ef, uint32_t &n_redecide) {
-    const float e = sg.o * ex2_approx(-q);
-    al = fminf(e, (float)kAlphaClamp);
-    om = 1.0f - al;
-    ef = fmaf(al, fmaf(sg.e1, q, sg.e0), 6.0e-8f);
-    bool pass = q < sg.q_lo;
-    if (e > 0.5f) {
-        if (e >= 0.99f * (1.0f + 4.0f * fmaf(sg.e1, q, sg.e0))) {
-            om = (float)(1.0 - kAlphaClamp);
-            ef = 1.0e-9f;
-        } else if (al < (float)kAlphaClamp) {
-            const float x = 0.69314718f * q;
-            float em = fmaf(-x, 1.0f / 362880.0f, 1.0f / 40320.0f);
-            em = fmaf(-x, em, 1.0f / 5040.0f);
-            em = fmaf(-x, em, 1.0f / 720.0f);
-            em = fmaf(-x, em, 1.0f / 120.0f);
-            em = fmaf(-x, em, 1.0f / 24.0f);
-            em = fmaf(-x, em, 1.0f / 6.0f);
-            em = fmaf(-x, em, 0.5f);
-            em = fmaf(-x, em, 1.0f);
-            em *= x;
-            om = fmaf(sg.o, em, sg.om_o);
-            ef = fmaf(6.2e-7f, om, al * fmaf(sg.e1, q, sg.e0));
-        }
-    }
-    if (!pass && q <= sg.q_hi) {
-        const double2 m = ws.mean[sg.p];
-        const double4 co = ws.conic_op[sg.p];
-        const double a64 = alpha64((double)px + 0.5, (double)py + 0.5, m.x, m.y, co.x, co.y, co.z, co.w);
-        al = (float)a64;
-        om = (float)(1.0 - a64);
-        ef = 1.0e-9f;
-        pass = a64 >= th64;
-        n_redecide++;
-    }
-    return pass;
-}
-
 // Exact fp64 transmittance of pixel (px, py) after the tile's splats k0..k1
 // (reference semantics, rasterize.py:146-177), for a pixel live throughout:
 // it blends splat k iff alpha_k >= theta and, for CR, its group leader's
@@ -266,14 +155,22 @@ __device__ __noinline__ double exact_transmittance(const Workspace &ws, const ui
     return T;
 }
 
+// Pixel slot s of a quad array (s = 2 * row + column).
+__device__ __forceinline__ float &slot(float2 (&v)[2], int s) { return (s & 1) ? v[s >> 1].y : v[s >> 1].x; }
+
+#ifndef SEELE_RASTER_MINB
+#define SEELE_RASTER_MINB 10
+#endif
 template <int W>
-__global__ void __launch_bounds__(64, 10) k_raster_quad(Workspace ws, const uint32_t *__restrict__ pair_pos, CamK cam,
+__global__ void __launch_bounds__(64, SEELE_RASTER_MINB) k_raster_quad(Workspace ws, const uint32_t *__restrict__ pair_pos, CamK cam,
                                                         CfgK cfg, float *image, int32_t *contrib, int64_t *stats) {
     __shared__ Staged s_stage[2][kBatch];  // per warp: each warp stages and walks the list on its own
+    // per pixel: tile splats it was live for (written at its death)
+    __shared__ uint32_t s_di[64][4];
     const int tile = (int)ws.tile_order[blockIdx.x];  // heavy tiles first (binning.cu k_pair_scan)
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int mw = tid >> 3, i = tid & 7;
-    const int shift = lane & 24;  // byte of this model-warp in a warp ballot
+    const unsigned bm = 0xffu << (lane & 24);  // this model-warp's byte of a warp ballot
     int bx, by;
     if (W == 4) {
         bx = 4 * (mw & 1) + (i & 3);
@@ -284,11 +181,19 @@ __global__ void __launch_bounds__(64, 10) k_raster_quad(Workspace ws, const uint
     }
     const int ox = (tile % cam.tiles_x) * kTile, oy = (tile / cam.tiles_x) * kTile;
     const int x0 = ox + 2 * bx, y0 = oy + 2 * by;
-    uint32_t valid = 0;
+    // Liveness as 0 / 1 float factors (1.0f = 0x3f800000): a pixel's blend factor is its pass sign mask & live
+    // & its group leader's verdict, one LOP3 per pixel.  Out-of-image pixels start dead.
+    float2 Lf[2];
+    uint32_t *di = s_di[tid];
 #pragma unroll
-    for (int s = 0; s < 4; s++)
-        if (x0 + (s & 1) < cam.width && y0 + (s >> 1) < cam.height) valid |= 1u << s;
-    uint32_t live = valid;  // bit s: pixel s not done (out-of-image pixels start done)
+    for (int s = 0; s < 4; s++) {
+        const bool v = x0 + (s & 1) < cam.width && y0 + (s >> 1) < cam.height;
+        slot(Lf, s) = v ? 1.0f : 0.0f;
+        di[s] = v ? 0xffffffffu : 0u;
+    }
+    int nlive = (Lf[0].x != 0.f) + (Lf[0].y != 0.f) + (Lf[1].x != 0.f) + (Lf[1].y != 0.f);
+    bool qlive = nlive != 0;
+    unsigned lb = __ballot_sync(0xffffffffu, qlive);
     const float lx0 = 2 * bx + 0.5f, ly0 = 2 * by + 0.5f;  // tile-relative centre of pixel 0
     const float2 lxp = make_float2(lx0, lx0 + 1.0f), lyp = make_float2(ly0, ly0 + 1.0f);
     // w = 4: the group is the 2x2 of quads whose top-left quad holds the leader pixel
@@ -298,33 +203,22 @@ __global__ void __launch_bounds__(64, 10) k_raster_quad(Workspace ws, const uint
     const bool leader_thread = W != 4 || (i == g_off);
     const double th64 = cfg.alpha_theta;
     const float gm = (float)cfg.gamma;
-    Quad st;
+    float2 T[2], D[2], C[2][3], cnt[2];
 #pragma unroll
     for (int r = 0; r < 2; r++) {
-        st.T[r] = f2(1.0f);
-        st.D[r] = f2(0.0f);
-        st.C[r][0] = st.C[r][1] = st.C[r][2] = f2(0.0f);
+        T[r] = f2(1.0f);
+        D[r] = f2(0.0f);
+        C[r][0] = C[r][1] = C[r][2] = f2(0.0f);
+        cnt[r] = f2(0.0f);
     }
-    st.cnt[0] = st.cnt[1] = f2(0.0f);
     // CR group leader pixel (rasterize.py:235-246): top-left pixel of the w x w group
     const int lead_x = W == 4 ? ox + 4 * (bx >> 1) : x0, lead_y = W == 4 ? oy + 4 * (by >> 1) : y0;
-    // Per pixel: number of tile splats it was live for (its death step); out-of-image pixels 0.
-    // The reference charges a model-warp's alpha_eval (ref) / leader_eval (cr) once per splat while
-    // any of its pixels is live, i.e. the max death step over its pixels.
-    __shared__ uint32_t s_di[64][4];  // per pixel: tile splats it was live for (written at its death)
-    uint32_t *di = s_di[tid];
-#pragma unroll
-    for (int s = 0; s < 4; s++) di[s] = ((valid >> s) & 1u) ? 0xffffffffu : 0u;
     uint32_t c_alpha = 0, c_blend = 0, n_redecide = 0, n_tamb = 0, n_skip = 0;
-#ifdef SEELE_RASTER_PROFILE
-    uint32_t pr_steps = 0, pr_member = 0, pr_blend = 0, pr_near = 0, pr_hi = 0;
-#endif
     const uint2 rg = ws.ranges[tile];
 
     Staged *s_g = s_stage[warp];
     const float ry0 = warp ? 8.5f : 0.5f, ry1 = ry0 + 7.0f;  // this warp's pixel-centre rows (tile-relative)
-    for (uint32_t b0 = rg.x; b0 < rg.y; b0 += kBatch) {
-        if (!__any_sync(0xffffffffu, live != 0u)) break;  // this warp's pixels are all done
+    for (uint32_t b0 = rg.x; b0 < rg.y && lb != 0u; b0 += kBatch) {
         const uint32_t idx = b0 + lane;
         bool rel = false;
         __syncwarp();
@@ -346,13 +240,13 @@ __global__ void __launch_bounds__(64, 10) k_raster_quad(Workspace ws, const uint
             sv.l22 = rc.z;
             sv.o = rc.w;
             sv.q_lo = rq.x;
-            sv.q_hi = rq.y;
+            sv.q_up = nextafterf(rq.y, INFINITY);
+            // 1 + 2^-10 covers the fp32 bound arithmetic (the products with T are rounded upward)
+            sv.e0 = rq.z * (1.0f + 1.0f / 1024.0f);
+            sv.e1 = rq.w * (1.0f + 1.0f / 1024.0f);
             sv.r = col.x;
             sv.g = col.y;
             sv.b = col.z;
-            sv.om_o = col.w;
-            sv.e0 = rq.z;
-            sv.e1 = rq.w;
             sv.p = p;
             s_g[lane] = sv;
             rel = bb.y >= ox + 0.5f && bb.x <= ox + 15.5f && bb.w >= oy + ry0 && bb.z <= oy + ry1;
@@ -369,131 +263,137 @@ __global__ void __launch_bounds__(64, 10) k_raster_quad(Workspace ws, const uint
         __syncwarp();
         const int nb = (int)min((uint32_t)kBatch, rg.y - b0);
         int jprev = -1;
-        unsigned lb = __ballot_sync(0xffffffffu, live != 0u);
-        while (lb != 0u) {
-            int j;
-            if (mlo) {
-                j = __ffs(mlo) - 1;
-                mlo &= mlo - 1u;
-            } else {
-                j = nb;  // no more relevant splats: charge the rest of the batch
-            }
-            const uint32_t gap = (uint32_t)(j - jprev - 1);  // skipped splats (charged via the death steps)
-            if (gap) n_skip += gap * __popc(live);
+        while (true) {
+            const int j = mlo ? __ffs(mlo) - 1 : nb;  // next relevant splat, or the end of the batch
+            mlo &= mlo - 1u;
+            n_skip += (uint32_t)(j - jprev - 1) * (uint32_t)nlive;  // skipped splats (charged via the death steps)
             if (j >= nb) break;
             jprev = j;
             const uint32_t step = b0 + (uint32_t)j - rg.x + 1u;  // tile splats processed including this one
             const Staged &sg = s_g[j];
-#ifdef SEELE_RASTER_PROFILE
-            pr_steps++;
-#endif
-            float2 q[2], al[2], om[2], ef[2];
+            float2 q[2], al[2], d[2], E[2];
             quad_q(sg, lxp, lyp, q);
-            uint32_t blend;
-            if (W == 0 || W == 1) {
-                blend = quad_alphas(sg, q, x0, y0, live, ws, th64, al, om, ef, n_redecide);
-                if (W == 1) {  // every pixel is its own group and leader
-                    const unsigned pb = __ballot_sync(0xffffffffu, blend != 0u);
-                    c_alpha += slice_any(pb, shift);
-                }
-            } else {
-                // One alpha evaluation of all four pixels serves both phases (the member phase runs on ~95 % of
-                // steps): the leader pixel's alpha counts even if that pixel is done (rasterize.py:281), the
-                // members blend if live, their group's leader passed and their own alpha passes.
-                const bool glive = W == 2 ? live != 0u : (lb & gmask) != 0u;
-                const uint32_t lbit = (leader_thread && glive) ? 1u : 0u;
-                const uint32_t pass = quad_alphas(sg, q, x0, y0, live | lbit, ws, th64, al, om, ef, n_redecide);
-                const bool lpass = (pass & lbit) != 0u;
-                const unsigned pb = __ballot_sync(0xffffffffu, lpass);
-                c_alpha += slice_any(pb, shift);
-                const bool my_pass = (pb >> (W == 2 ? lane : leader_lane)) & 1u;
-                blend = my_pass ? (pass & live) : 0u;
-            }
-            const unsigned bb = __ballot_sync(0xffffffffu, blend != 0u);
-            if (bb == 0u) continue;
-#ifdef SEELE_RASTER_PROFILE
-            pr_blend++;
-            pr_hi += __any_sync(0xffffffffu, (al[0].x > 0.5f) | (al[0].y > 0.5f) | (al[1].x > 0.5f) | (al[1].y > 0.5f)) ? 1 : 0;
-#endif
-            c_blend += slice_any(bb, shift);
-            uint32_t near = 0;
-            float2 m01[2];
+            uint32_t amb = 0;
 #pragma unroll
-            for (int r = 0; r < 2; r++) {  // _blend (rasterize.py:169-177) on a pixel pair, masked by 0/1 factors
-                // 0/1 factors from the blend bits: (bit << 29) lands on the exponent of 1.0f (0x3f800000)
-                const uint32_t bl = blend >> (2 * r);
-                const float2 m = make_float2(__uint_as_float(0x3f800000u & (0u - (bl & 1u))),
-                                             __uint_as_float(0x3f800000u & (0u - ((bl >> 1) & 1u))));
-                const float2 nm = __ffma2_rn(m, f2(-1.0f), f2(1.0f));
-                m01[r] = m;
-                const float2 t0 = st.T[r];
-                const float2 wgt = __fmul2_rn(t0, __fmul2_rn(al[r], m));  // T alpha, or 0
-                st.C[r][0] = __ffma2_rn(wgt, f2(sg.r), st.C[r][0]);
-                st.C[r][1] = __ffma2_rn(wgt, f2(sg.g), st.C[r][1]);
-                st.C[r][2] = __ffma2_rn(wgt, f2(sg.b), st.C[r][2]);
-                const float2 omm = __ffma2_rn(om[r], m, nm);  // 1 - alpha (exactly), or 1
-                const float2 t1 = __fmul2_rn(t0, omm);
-                const float2 d1 = __ffma2_rn(st.D[r], omm, __fmul2_rn(t0, __fmul2_rn(ef[r], m)));
-                st.T[r] = t1;
-                st.D[r] = d1;
-                const float2 lo = __fadd2_rn(t1, make_float2(-d1.x, -d1.y));
-                near |= ((lo.x < gm ? 1u : 0u) | (lo.y < gm ? 2u : 0u)) << (2 * r);
+            for (int r = 0; r < 2; r++) {
+                al[r] = __fmul2_rn(f2(sg.o), make_float2(ex2_approx(-q[r].x), ex2_approx(-q[r].y)));
+                d[r] = __fadd2_rn(q[r], f2(-sg.q_lo));  // sign set <=> q' < q_lo: surely passes
+                const float2 u = __fadd2_rn(q[r], f2(-sg.q_up));  // sign set <=> q' <= top of the bracket
+                E[r] = __ffma2_rn(f2(sg.e1), q[r], f2(sg.e0));
+                amb |= (fbits(u.x) & ~fbits(d[r].x)) | (fbits(u.y) & ~fbits(d[r].y));
             }
+            // alpha = min(o 2^-q', 0.99): the clamp can only bind for o > 0.99 (the error model covers
+            // 0.99f vs 0.99 and a clamp of the exact value)
+            if (sg.o > 0.99f) {
 #pragma unroll
-            st.cnt[0] = __fadd2_rn(st.cnt[0], m01[0]);
-            st.cnt[1] = __fadd2_rn(st.cnt[1], m01[1]);
-            near &= blend;  // T may be below gamma: decide below
-            if (__any_sync(0xffffffffu, near != 0u)) {
-#ifdef SEELE_RASTER_PROFILE
-                pr_near++;
-#endif
-                uint32_t amb = 0;
+                for (int r = 0; r < 2; r++) al[r] = make_float2(fminf(al[r].x, 0.99f), fminf(al[r].y, 0.99f));
+            }
+            if (__any_sync(0xffffffffu, (int)amb < 0)) {
+                // inside the bracket: decide with the reference formula in fp64 (rare); needed for live pixels
+                // and for the group leader pixel while its group is live
+                const bool glive = W == 4 ? (lb & gmask) != 0u : qlive;
 #pragma unroll
                 for (int s = 0; s < 4; s++) {
-                    if (!((near >> s) & 1u)) continue;
-                    if (lane_of(st.T[s >> 1], s & 1) + lane_of(st.D[s >> 1], s & 1) < gm) {  // surely below: done
-                        live &= ~(1u << s);
+                    const int r = s >> 1;
+                    const float qs = slot(q, s);
+                    const bool need = slot(Lf, s) != 0.0f || (W >= 2 && s == 0 && leader_thread && glive);
+                    if (!need || qs < sg.q_lo || qs >= sg.q_up) continue;
+                    const double2 m = ws.mean[sg.p];
+                    const double4 co = ws.conic_op[sg.p];
+                    const double a64 = alpha64((double)(x0 + (s & 1)) + 0.5, (double)(y0 + r) + 0.5, m.x, m.y, co.x,
+                                               co.y, co.z, co.w);
+                    slot(al, s) = (float)a64;
+                    slot(d, s) = a64 >= th64 ? -1.0f : 1.0f;
+                    slot(E, s) = 6.2e-8f;  // rounding of a64 to float
+                    n_redecide++;
+                }
+            }
+            uint32_t my = ~0u;  // all-ones if this thread's group leader passed (ref / w = 1: no leader test)
+            if (W == 2 || W == 4) {
+                // the leader's alpha counts even if the leader pixel is done (rasterize.py:281)
+                const bool glive = W == 4 ? (lb & gmask) != 0u : qlive;
+                const bool lp = leader_thread && glive && (int)fbits(d[0].x) < 0;
+                const unsigned pb = __ballot_sync(0xffffffffu, lp);
+                c_alpha += (pb & bm) != 0u;
+                my = 0u - ((pb >> (W == 2 ? lane : leader_lane)) & 1u);
+            }
+            float2 m[2];
+#pragma unroll
+            for (int r = 0; r < 2; r++)
+                m[r] = make_float2(__uint_as_float(sign_mask(d[r].x) & fbits(Lf[r].x) & my),
+                                   __uint_as_float(sign_mask(d[r].y) & fbits(Lf[r].y) & my));
+            const unsigned bb =
+                __ballot_sync(0xffffffffu, (fbits(m[0].x) | fbits(m[0].y) | fbits(m[1].x) | fbits(m[1].y)) != 0u);
+            if (bb == 0u) continue;
+            c_blend += (bb & bm) != 0u;
+            if (W == 1) c_alpha += (bb & bm) != 0u;  // each pixel is its own leader
+            float2 y[2];
+#pragma unroll
+            for (int r = 0; r < 2; r++) {  // _blend (rasterize.py:169-177) on a pixel pair, masked by 0/1 factors
+                const float2 am = __fmul2_rn(al[r], m[r]);
+                const float2 t0 = T[r];
+                const float2 wgt = __fmul2_rn(t0, am);  // T alpha, or 0
+                C[r][0] = __ffma2_rn(wgt, f2(sg.r), C[r][0]);
+                C[r][1] = __ffma2_rn(wgt, f2(sg.g), C[r][1]);
+                C[r][2] = __ffma2_rn(wgt, f2(sg.b), C[r][2]);
+                const float2 omm = __ffma2_rn(am, f2(-1.0f), f2(1.0f));  // 1 - alpha, or 1 (exact)
+                // |omm - (1 - alpha_ref)| <= alpha (e0 + e1 q') + 1e-7 (rounding of 1 - alpha and of T omm)
+                const float2 efm = __fmul2_rn(__ffma2_rn(al[r], E[r], f2(1.0e-7f)), m[r]);
+                const float2 t1 = __fmul2_rn(t0, omm);
+                const float2 d1 = __ffma2_ru(D[r], omm, __fmul2_ru(t0, efm));
+                T[r] = t1;
+                D[r] = d1;
+                // sign set <=> blended and T32 - D < gamma (rounded so that a clear sign proves T >= gamma)
+                y[r] = __ffma2_rn(m[r], __fadd2_rn(t1, __fmul2_rn(__fadd2_ru(d1, f2(gm)), f2(-1.0f))), f2(0.0f));
+                cnt[r] = __fadd2_rn(cnt[r], m[r]);
+            }
+            if (__any_sync(0xffffffffu, (int)(fbits(y[0].x) | fbits(y[0].y) | fbits(y[1].x) | fbits(y[1].y)) < 0)) {
+                uint32_t ambT = 0;
+#pragma unroll
+                for (int s = 0; s < 4; s++) {
+                    if ((int)fbits(slot(y, s)) >= 0) continue;
+                    if (__fadd_ru(slot(T, s), slot(D, s)) < gm) {  // surely below: done
+                        slot(Lf, s) = 0.0f;
                         di[s] = step;
+                        nlive--;
                     } else {
-                        amb |= 1u << s;
+                        ambT |= 1u << s;
                     }
                 }
-                unsigned ambw = __ballot_sync(0xffffffffu, amb != 0u);
+                unsigned ambw = __ballot_sync(0xffffffffu, ambT != 0u);
                 while (ambw) {
                     // T < gamma undecidable in fp32: recompute that pixel's transmittance exactly (fp64,
                     // reference formula) over every splat of the tile up to this one, all 32 lanes together,
                     // then decide.  A live pixel's blends depend only on its own alphas (and its group
                     // leader's for CR).
                     const int src = __ffs(ambw) - 1;
-                    const uint32_t am = __shfl_sync(0xffffffffu, amb, src);
+                    const uint32_t am = __shfl_sync(0xffffffffu, ambT, src);
                     const int s = __ffs(am) - 1;
                     const int px = __shfl_sync(0xffffffffu, x0, src) + (s & 1);
                     const int py = __shfl_sync(0xffffffffu, y0, src) + (s >> 1);
                     const int gx = __shfl_sync(0xffffffffu, lead_x, src), gy = __shfl_sync(0xffffffffu, lead_y, src);
-                    const double T = exact_transmittance<W>(ws, pair_pos, rg.x, b0 + (uint32_t)j, px, py, gx, gy, th64);
+                    const double Tx = exact_transmittance<W>(ws, pair_pos, rg.x, b0 + (uint32_t)j, px, py, gx, gy, th64);
                     if (lane == src) {
                         n_tamb++;
 #pragma unroll
                         for (int ss = 0; ss < 4; ss++) {
                             if (ss != s) continue;
-                            if (ss & 1) {
-                                st.T[ss >> 1].y = (float)T;
-                                st.D[ss >> 1].y = 6.0e-8f * (float)T;
-                            } else {
-                                st.T[ss >> 1].x = (float)T;
-                                st.D[ss >> 1].x = 6.0e-8f * (float)T;
-                            }
-                            if (T < cfg.gamma) {
-                                live &= ~(1u << ss);
+                            slot(T, ss) = (float)Tx;
+                            slot(D, ss) = 6.0e-8f * (float)Tx;
+                            if (Tx < cfg.gamma) {
+                                slot(Lf, ss) = 0.0f;
                                 di[ss] = step;
+                                nlive--;
                             }
                         }
-                        amb &= ~(1u << s);
+                        ambT &= ~(1u << s);
                     }
-                    ambw = __ballot_sync(0xffffffffu, amb != 0u);
+                    ambw = __ballot_sync(0xffffffffu, ambT != 0u);
                 }
+                qlive = nlive != 0;
+                lb = __ballot_sync(0xffffffffu, qlive);
+                if (lb == 0u) break;
             }
-            lb = __ballot_sync(0xffffffffu, live != 0u);
         }
     }
     // pixels still live at the end took every splat of the list
@@ -502,7 +402,7 @@ __global__ void __launch_bounds__(64, 10) k_raster_quad(Workspace ws, const uint
     for (int s = 0; s < 4; s++) {
         if (di[s] == 0xffffffffu) di[s] = rg.y > rg.x ? rg.y - rg.x : 0u;
         n_live += di[s];
-        n_blend += (uint32_t)lane_of(st.cnt[s >> 1], s & 1);
+        n_blend += (uint32_t)slot(cnt, s);
         mw_steps = max(mw_steps, di[s]);
     }
 #pragma unroll
@@ -514,17 +414,6 @@ __global__ void __launch_bounds__(64, 10) k_raster_quad(Workspace ws, const uint
     const uint32_t w_live = __reduce_add_sync(0xffffffffu, n_live);
     const uint32_t w_blend = __reduce_add_sync(0xffffffffu, n_blend);
     const uint32_t w_skip = __reduce_add_sync(0xffffffffu, n_skip);
-#ifdef SEELE_RASTER_PROFILE
-    if (lane == 0) {  // debug build: warp-step counters in stats slots 11..15
-        unsigned long long *sp = (unsigned long long *)stats;
-        atomicAdd(sp + 11, (unsigned long long)pr_steps);
-        atomicAdd(sp + 12, (unsigned long long)pr_member);
-        atomicAdd(sp + 13, (unsigned long long)pr_blend);
-        atomicAdd(sp + 14, (unsigned long long)pr_near);
-        atomicAdd(sp + 15, (unsigned long long)pr_hi);
-    }
-    return;
-#endif
     if (lane == 0) {
         unsigned long long *sp = (unsigned long long *)stats;
         if (w_red) atomicAdd(sp + SEELE_STAT_ALPHA_REDECIDE, (unsigned long long)w_red);
@@ -535,21 +424,20 @@ __global__ void __launch_bounds__(64, 10) k_raster_quad(Workspace ws, const uint
     }
 #pragma unroll
     for (int s = 0; s < 4; s++) {
-        if (!((valid >> s) & 1u)) continue;
+        if (x0 + (s & 1) >= cam.width || y0 + (s >> 1) >= cam.height) continue;
         const long long pix = (long long)(y0 + (s >> 1)) * cam.width + x0 + (s & 1);
         const int r = s >> 1, c = s & 1;
-        const float T = lane_of(st.T[r], c);
-        image[3 * pix + 0] = fmaf(T, (float)cfg.bg[0], lane_of(st.C[r][0], c));  // background (rasterize.py:228-231)
-        image[3 * pix + 1] = fmaf(T, (float)cfg.bg[1], lane_of(st.C[r][1], c));
-        image[3 * pix + 2] = fmaf(T, (float)cfg.bg[2], lane_of(st.C[r][2], c));
-        if (contrib) contrib[pix] = (int32_t)lane_of(st.cnt[r], c);
+        const float Ts = slot(T, s);
+        image[3 * pix + 0] = fmaf(Ts, (float)cfg.bg[0], lane_of(C[r][0], c));  // background (rasterize.py:228-231)
+        image[3 * pix + 1] = fmaf(Ts, (float)cfg.bg[1], lane_of(C[r][1], c));
+        image[3 * pix + 2] = fmaf(Ts, (float)cfg.bg[2], lane_of(C[r][2], c));
+        if (contrib) contrib[pix] = (int32_t)slot(cnt, s);
     }
     if (i == 0) {
         Counters k{c_alpha, c_blend, c_leader};
         add_counters<W>(stats, k);
     }
 }
-
 }  // namespace
 
 void launch_raster_fast(int W, const Workspace &ws, const uint32_t *pair_pos, const CamK &cam, const CfgK &cfg,
