@@ -145,9 +145,7 @@ Workspace carve_workspace(void *base, long long n_max, long long cap, int width,
     w.rect = c.take<short4>(n);
     w.mean = c.take<double2>(n);
     w.conic_op = c.take<double4>(n);
-    w.color = c.take<float4>(n);
-    w.rc = c.take<float4>(n);
-    w.rq = c.take<float4>(n);
+    w.rec = c.take<RasterRec>(n);
     w.bbox = c.take<float4>(n);
     w.dkey[0] = c.take<uint32_t>(n);
     w.dkey[1] = c.take<uint32_t>(n);
@@ -203,10 +201,10 @@ __global__ void k_export_splats(Workspace ws, long long n, int8_t *status, doubl
         }
         if (opacity) opacity[p] = co.w;
         if (color) {
-            const float4 c = ok ? ws.color[p] : make_float4(0, 0, 0, 0);
-            color[3 * p] = c.x;
-            color[3 * p + 1] = c.y;
-            color[3 * p + 2] = c.z;
+            const RasterRec r = ok ? ws.rec[p] : RasterRec{};
+            color[3 * p] = r.r;
+            color[3 * p + 1] = r.g;
+            color[3 * p + 2] = r.b;
         }
     }
 }

@@ -65,6 +65,17 @@ constexpr int kLookScan = 3;
 constexpr int kLookRows = 4;
 constexpr int kLookCols = 5;
 
+// FAST raster record of one splat (raster_fast.cu), written by preprocess.
+// q' = q log2(e) / 2, so alpha = o 2^-q'; one 64-byte line, staged into
+// shared memory by four 16-byte cp.async per splat.
+struct __align__(16) RasterRec {
+    float mxh, mxl, myh, myl;  // mean in pixel coordinates as hi + lo floats
+    float l11, l21, l22, o;    // Cholesky factor of the conic in q' units; opacity
+    float q_lo, q_up, e0, e1;  // pass: q' < q_lo; fail: q' >= q_up; alpha relative error <= e0 + e1 q'
+    float r, g, b;             // colour
+    uint32_t p;                // assembled position (fp64 re-decisions)
+};
+
 // Workspace carve-up; identical on every call for the same (n_max, cap, w, h).
 struct Workspace {
     // per assembled splat (preprocess)
@@ -73,11 +84,8 @@ struct Workspace {
     short4 *rect;
     double2 *mean;
     double4 *conic_op;   // (a, b, c, opacity)
-    float4 *color;       // (r, g, b, 1 - opacity)
-    // FAST raster records (raster_fast.cu); q' = q log2(e) / 2 so alpha = o 2^-q'
-    float4 *rc;          // (l11, l21, l22, opacity): Cholesky factor of the conic in q' units, fp32
-    float4 *rq;          // (q_lo', q_hi', e0, e1): alpha-test bracket, alpha error |da/a| <= e0 + e1 q'
-    float4 *bbox;        // (x_min, x_max, y_min, y_max) of {q' <= q_hi'} in pixel coordinates
+    RasterRec *rec;      // FAST raster records (also the colour of the exact engine)
+    float4 *bbox;        // (x_min, x_max, y_min, y_max) of {q' < q_up} in pixel coordinates
     // depth sort (ping-pong): key = depth quantised monotonically to 24 bits,
     // value = assembled position; the sorted order ends in dkey/dval[kDepthFinal]
     uint32_t *dkey[2];

@@ -151,7 +151,7 @@ __device__ __forceinline__ void load_splat(const SceneK &sc, long long i, int sh
 // bbox = axis-aligned box of {q' <= q_hi'}; the raster refines it with the
 // exact minimum of q' over each warp's pixel rectangle.
 __device__ __forceinline__ void write_raster_record(const Workspace &ws, long long p, double m0, double m1, double ca,
-                                                    double cb, double cc, double o, double qth) {
+                                                    double cb, double cc, double o, double qth, float4 col) {
     const double K = 0.72134752044448170368;  // log2(e) / 2
     const double u = 5.9604644775390625e-08;  // 2^-24
     const double tr = ca + cc, disc = sqrt(0.25 * (ca - cc) * (ca - cc) + cb * cb);
@@ -184,8 +184,16 @@ __device__ __forceinline__ void write_raster_record(const Workspace &ws, long lo
     const double l11 = sqrt(K * ca);
     const double l21 = K * cb / l11;
     const double l22 = sqrt(fmax(K * det / ca, 0.0));
-    ws.rc[p] = make_float4((float)l11, (float)l21, (float)l22, (float)o);
-    ws.rq[p] = rq;
+    // raster record: the mean as hi + lo floats (|m - hi - lo| ~ 2^-48 |m|); q_up = the first float above
+    // the bracket top, so q' <= q_hi' <=> q' < q_up; the error model is widened by 2^-10 for the fp32
+    // bound arithmetic of the raster (products with T rounded upward)
+    const float mxh = (float)m0, myh = (float)m1;
+    float4 *rec = reinterpret_cast<float4 *>(ws.rec + p);
+    rec[0] = make_float4(mxh, (float)(m0 - (double)mxh), myh, (float)(m1 - (double)myh));
+    rec[1] = make_float4((float)l11, (float)l21, (float)l22, (float)o);
+    rec[2] = make_float4(rq.x, nextafterf(rq.y, INFINITY), rq.z * (1.0f + 1.0f / 1024.0f),
+                         rq.w * (1.0f + 1.0f / 1024.0f));
+    rec[3] = make_float4(col.x, col.y, col.z, __uint_as_float((uint32_t)p));
     ws.bbox[p] = bb;
 }
 
@@ -359,7 +367,6 @@ __global__ void __launch_bounds__(256, 3) k_preprocess(SceneK sc, const int64_t 
                         col.y = sh_channel([&](int k) { return (float)shp[16 + k]; }, vx, vy, vz, cfg.sh_degree);
                         col.z = sh_channel([&](int k) { return (float)shp[32 + k]; }, vx, vy, vz, cfg.sh_degree);
                     }
-                    col.w = (float)(1.0 - g.o);
                     const double qth = 2.0 * log(g.o / cfg.alpha_theta);  // alpha >= theta <=> q <= qth
                     double r2 = 9.0;  // MAX_RADIUS_SQ
                     if (cfg.opacity_aware) {
@@ -383,8 +390,7 @@ __global__ void __launch_bounds__(256, 3) k_preprocess(SceneK sc, const int64_t 
                     zbits = (unsigned long long)__double_as_longlong(z);
                     ws.mean[p] = make_double2(m0, m1);
                     ws.conic_op[p] = make_double4(ca, cb, cc, g.o);
-                    ws.color[p] = col;
-                    write_raster_record(ws, p, m0, m1, ca, cb, cc, g.o, qth);
+                    write_raster_record(ws, p, m0, m1, ca, cb, cc, g.o, qth, col);
                 }
             }
             ws.status[p] = (uint8_t)status;

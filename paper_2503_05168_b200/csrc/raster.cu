@@ -59,7 +59,8 @@ __global__ void __launch_bounds__(256) k_raster_exact(Workspace ws, const uint32
             s_b[tid] = co.y;
             s_c[tid] = co.z;
             s_o[tid] = co.w;
-            s_col[tid] = ws.color[p];
+            const RasterRec &rr = ws.rec[p];
+            s_col[tid] = make_float4(rr.r, rr.g, rr.b, 0.f);
         }
         __syncthreads();
         const int nb = min(256u, rg.y - b0);

@@ -47,32 +47,35 @@ namespace {
 constexpr int kBatch = 32;  // splats staged per warp batch
 constexpr double kQ = 0.72134752044448170368;  // log2(e) / 2: q' = kQ q
 
-struct __align__(16) Staged {
-    float mxh, mxl, myh, myl;  // tile-relative mean as hi + lo floats
-    float l11, l21, l22, o;    // Cholesky factor of the conic in q' units; opacity
-    float q_lo, q_up, e0, e1;  // pass: q' < q_lo; fail: q' >= q_up (first float above the bracket); alpha error e0 + e1 q'
-    float r, g, b;             // colour
-    uint32_t p;                // assembled position (fp64 re-decisions)
-};
+using Staged = RasterRec;
+
+__device__ __forceinline__ void cp_async16(void *smem, const void *gmem) {
+    const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
 __device__ __forceinline__ uint32_t fbits(float x) { return __float_as_uint(x); }
+// c += (ballot & mask) != 0, as one predicated add
+__device__ __forceinline__ void count_any(uint32_t &c, unsigned ballot, unsigned mask) {
+    asm("{\n\t.reg .pred p;\n\t.reg .b32 t;\n\tand.b32 t, %1, %2;\n\tsetp.ne.u32 p, t, 0;\n\t@p add.u32 %0, %0, 1;\n\t}"
+        : "+r"(c)
+        : "r"(ballot), "r"(mask));
+}
 // all-ones if the sign bit of x is set, else 0
 __device__ __forceinline__ uint32_t sign_mask(float x) { return (uint32_t)((int)__float_as_uint(x) >> 31); }
 
-// Quad state: four pixels, slot s = (x0 + (s & 1), y0 + (s >> 1)); the two
-// pixels of a quad row r = s >> 1 are one float2 (.x = left, .y = right) so
-// the per-pixel math runs as packed fp32x2 instructions (FFMA2 / FMUL2 /
-// FADD2, per-element round-to-nearest: bit-identical to scalar fmaf).
-struct Quad {
-    float2 T[2], D[2], C[2][3];
-    float2 cnt[2];  // blends per pixel (exact in fp32 below 2^24)
-};
-
+// The two pixels of a quad row are one float2 (.x = left, .y = right) so the
+// per-pixel math runs as packed fp32x2 instructions (FFMA2 / FMUL2 / FADD2,
+// per-element rounding: bit-identical to scalar fmaf).
 __device__ __forceinline__ float2 f2(float v) { return make_float2(v, v); }
 __device__ __forceinline__ float lane_of(const float2 &v, int c) { return c ? v.y : v.x; }
 
 // q' of the four quad pixels (fp32 Cholesky form, error model at
-// preprocess.cu write_raster_record): q[r] = (q of (x0, y0 + r), q of (x0 + 1, y0 + r)).
+// preprocess.cu write_raster_record), pixel centres and mean in absolute
+// pixel coordinates: q[r] = (q of (x0, y0 + r), q of (x0 + 1, y0 + r)).
 __device__ __forceinline__ void quad_q(const Staged &sg, float2 lxp, float2 lyp, float2 q[2]) {
     const float2 dx = __fadd2_rn(__fadd2_rn(lxp, f2(-sg.mxh)), f2(-sg.mxl));
     const float2 dy = __fadd2_rn(__fadd2_rn(lyp, f2(-sg.myh)), f2(-sg.myl));
@@ -117,11 +120,11 @@ __device__ __forceinline__ bool rect_reaches(float mx, float my, float l11, floa
 // decided from fp64 q against the fp32 bracket (valid a fortiori), with the
 // reference formula inside it.
 __device__ __forceinline__ bool exact_test(double px, double py, const double2 &m, const double4 &co, float q_lo,
-                                           float q_hi, double th, double &a) {
+                                           float q_up, double th, double &a) {
     const double dx = px - m.x, dy = py - m.y;
     const double q = fma(co.x * dx, dx, fma(2.0 * co.y * dx, dy, (co.z * dy) * dy));
     const double qp = kQ * q;
-    if (qp > (double)q_hi) return false;
+    if (qp >= (double)q_up) return false;
     if (qp < (double)q_lo) {
         a = fmin(co.w * exp(-0.5 * q), kAlphaClamp);
         return true;
@@ -144,7 +147,7 @@ __device__ __noinline__ double exact_transmittance(const Workspace &ws, const ui
         const uint32_t p = pair_pos[k];
         const double2 m = ws.mean[p];
         const double4 co = ws.conic_op[p];
-        const float4 f = ws.rq[p];
+        const float4 f = reinterpret_cast<const float4 *>(ws.rec + p)[2];  // (q_lo, q_up, e0, e1)
         double a;
         if (W >= 2 && !exact_test(lx + 0.5, ly + 0.5, m, co, f.x, f.y, th, a)) continue;
         if (!exact_test(px + 0.5, py + 0.5, m, co, f.x, f.y, th, a)) continue;
@@ -159,12 +162,15 @@ __device__ __noinline__ double exact_transmittance(const Workspace &ws, const ui
 __device__ __forceinline__ float &slot(float2 (&v)[2], int s) { return (s & 1) ? v[s >> 1].y : v[s >> 1].x; }
 
 #ifndef SEELE_RASTER_MINB
-#define SEELE_RASTER_MINB 10
+#define SEELE_RASTER_MINB 8
 #endif
 template <int W>
 __global__ void __launch_bounds__(64, SEELE_RASTER_MINB) k_raster_quad(Workspace ws, const uint32_t *__restrict__ pair_pos, CamK cam,
                                                         CfgK cfg, float *image, int32_t *contrib, int64_t *stats) {
-    __shared__ Staged s_stage[2][kBatch];  // per warp: each warp stages and walks the list on its own
+    // per warp, double-buffered: each warp stages and walks the list on its own; batch b + 1 is in flight
+    // (cp.async) while batch b is rasterized
+    __shared__ Staged s_stage[2][2][kBatch];
+    __shared__ float4 s_box[2][2][kBatch];
     // per pixel: tile splats it was live for (written at its death)
     __shared__ uint32_t s_di[64][4];
     const int tile = (int)ws.tile_order[blockIdx.x];  // heavy tiles first (binning.cu k_pair_scan)
@@ -194,7 +200,7 @@ __global__ void __launch_bounds__(64, SEELE_RASTER_MINB) k_raster_quad(Workspace
     int nlive = (Lf[0].x != 0.f) + (Lf[0].y != 0.f) + (Lf[1].x != 0.f) + (Lf[1].y != 0.f);
     bool qlive = nlive != 0;
     unsigned lb = __ballot_sync(0xffffffffu, qlive);
-    const float lx0 = 2 * bx + 0.5f, ly0 = 2 * by + 0.5f;  // tile-relative centre of pixel 0
+    const float lx0 = (float)x0 + 0.5f, ly0 = (float)y0 + 0.5f;  // centre of pixel 0 (exact in fp32)
     const float2 lxp = make_float2(lx0, lx0 + 1.0f), lyp = make_float2(ly0, ly0 + 1.0f);
     // w = 4: the group is the 2x2 of quads whose top-left quad holds the leader pixel
     const int g_off = (i & 2);
@@ -216,59 +222,58 @@ __global__ void __launch_bounds__(64, SEELE_RASTER_MINB) k_raster_quad(Workspace
     uint32_t c_alpha = 0, c_blend = 0, n_redecide = 0, n_tamb = 0, n_skip = 0;
     const uint2 rg = ws.ranges[tile];
 
-    Staged *s_g = s_stage[warp];
     const float ry0 = warp ? 8.5f : 0.5f, ry1 = ry0 + 7.0f;  // this warp's pixel-centre rows (tile-relative)
-    for (uint32_t b0 = rg.x; b0 < rg.y && lb != 0u; b0 += kBatch) {
-        const uint32_t idx = b0 + lane;
-        bool rel = false;
-        __syncwarp();
+    // cp.async of one splat's record + box into buffer `buf` (idx past the list: nothing)
+    auto stage = [&](uint32_t idx, uint32_t p, int buf) {
         if (idx < rg.y) {
-            const uint32_t p = pair_pos[idx];
-            const double2 m = ws.mean[p];
-            const float4 rc = ws.rc[p];
-            const float4 rq = ws.rq[p];
-            const float4 col = ws.color[p];
-            const float4 bb = ws.bbox[p];
-            Staged sv;
-            const double mxr = m.x - (double)ox, myr = m.y - (double)oy;
-            sv.mxh = (float)mxr;
-            sv.mxl = (float)(mxr - (double)sv.mxh);
-            sv.myh = (float)myr;
-            sv.myl = (float)(myr - (double)sv.myh);
-            sv.l11 = rc.x;
-            sv.l21 = rc.y;
-            sv.l22 = rc.z;
-            sv.o = rc.w;
-            sv.q_lo = rq.x;
-            sv.q_up = nextafterf(rq.y, INFINITY);
-            // 1 + 2^-10 covers the fp32 bound arithmetic (the products with T are rounded upward)
-            sv.e0 = rq.z * (1.0f + 1.0f / 1024.0f);
-            sv.e1 = rq.w * (1.0f + 1.0f / 1024.0f);
-            sv.r = col.x;
-            sv.g = col.y;
-            sv.b = col.z;
-            sv.p = p;
-            s_g[lane] = sv;
+            const float4 *src = reinterpret_cast<const float4 *>(ws.rec + p);
+            float4 *dst = reinterpret_cast<float4 *>(&s_stage[warp][buf][lane]);
+#pragma unroll
+            for (int k = 0; k < 4; k++) cp_async16(dst + k, src + k);
+            cp_async16(&s_box[warp][buf][lane], ws.bbox + p);
+        }
+        cp_async_commit();
+    };
+    uint32_t p_next = rg.x + lane < rg.y ? pair_pos[rg.x + lane] : 0u;
+    stage(rg.x + lane, p_next, 0);
+    p_next = rg.x + kBatch + lane < rg.y ? pair_pos[rg.x + kBatch + lane] : 0u;
+    int buf = 0;
+    for (uint32_t b0 = rg.x; b0 < rg.y && lb != 0u; b0 += kBatch, buf ^= 1) {
+        __syncwarp();  // every lane is done with buffer buf ^ 1 (batch b - 1)
+        stage(b0 + kBatch + lane, p_next, buf ^ 1);
+        const uint32_t i2 = b0 + 2 * kBatch + lane;
+        p_next = i2 < rg.y ? pair_pos[i2] : 0u;
+        cp_async_wait<1>();  // this lane's part of batch b has landed
+        __syncwarp();
+        const Staged *s_g = s_stage[warp][buf];
+        bool rel = false;
+        if (b0 + lane < rg.y) {
+            const Staged &sv = s_g[lane];
+            const float4 bb = s_box[warp][buf][lane];
             rel = bb.y >= ox + 0.5f && bb.x <= ox + 15.5f && bb.w >= oy + ry0 && bb.z <= oy + ry1;
             if (rel) {
-                // exact refinement; the margin covers the fp32 evaluation (twice the bracket width) and the
-                // plain-float mean (|error| <= 2^-24 (|d| + 23) px, times |grad q'| <= 2 P sqrt(q'))
-                const float P = sqrtf(fmaf(rc.x, rc.x, fmaf(rc.y, rc.y, rc.z * rc.z)));
-                const float qm = rq.y + 2.0f * (rq.y - rq.x) + 1e-6f * rq.y + 1e-5f * P * sqrtf(fmaxf(rq.y, 0.f)) +
-                                 1e-6f;
-                rel = rect_reaches((float)mxr, (float)myr, rc.x, rc.y, rc.z, qm, 0.5f, 15.5f, ry0, ry1);
+                // exact refinement in tile-relative floats; the margin covers the fp32 evaluation (twice the
+                // bracket width) and the float mean, |error| <= ep = 2^-23 (|d| + 32) px, times
+                // |grad q'| <= 2 P sqrt(q')
+                const float mx = (sv.mxh - (float)ox) + sv.mxl, my = (sv.myh - (float)oy) + sv.myl;
+                const float P = sqrtf(fmaf(sv.l11, sv.l11, fmaf(sv.l21, sv.l21, sv.l22 * sv.l22)));
+                const float ep = 1.2e-7f * (fabsf(mx) + fabsf(my) + 32.0f);
+                const float qh = sv.q_up, pe = P * ep;
+                const float qm = qh + 2.0f * (qh - sv.q_lo) + 1e-6f * qh + 2.2f * pe * sqrtf(fmaxf(qh, 0.f)) +
+                                 1.1f * pe * pe + 1e-6f;
+                rel = rect_reaches(mx, my, sv.l11, sv.l21, sv.l22, qm, 0.5f, 15.5f, ry0, ry1);
             }
         }
         uint32_t mlo = __ballot_sync(0xffffffffu, rel);
         __syncwarp();
         const int nb = (int)min((uint32_t)kBatch, rg.y - b0);
-        int jprev = -1;
-        while (true) {
-            const int j = mlo ? __ffs(mlo) - 1 : nb;  // next relevant splat, or the end of the batch
+        // skipped splats of the batch (charged to the live pixels via the death steps); a pixel that dies in
+        // the batch takes back the skipped splats after its death
+        const uint32_t skipped = ~mlo & (nb == kBatch ? ~0u : (1u << nb) - 1u);
+        n_skip += (uint32_t)__popc(skipped) * (uint32_t)nlive;
+        while (mlo) {
+            const int j = __ffs(mlo) - 1;  // next relevant splat
             mlo &= mlo - 1u;
-            n_skip += (uint32_t)(j - jprev - 1) * (uint32_t)nlive;  // skipped splats (charged via the death steps)
-            if (j >= nb) break;
-            jprev = j;
             const uint32_t step = b0 + (uint32_t)j - rg.x + 1u;  // tile splats processed including this one
             const Staged &sg = s_g[j];
             float2 q[2], al[2], d[2], E[2];
@@ -314,8 +319,9 @@ __global__ void __launch_bounds__(64, SEELE_RASTER_MINB) k_raster_quad(Workspace
                 const bool glive = W == 4 ? (lb & gmask) != 0u : qlive;
                 const bool lp = leader_thread && glive && (int)fbits(d[0].x) < 0;
                 const unsigned pb = __ballot_sync(0xffffffffu, lp);
-                c_alpha += (pb & bm) != 0u;
-                my = 0u - ((pb >> (W == 2 ? lane : leader_lane)) & 1u);
+                count_any(c_alpha, pb, bm);
+                // w = 2: the group is the thread's own quad, its leader verdict is lp itself
+                my = W == 2 ? (lp ? ~0u : 0u) : 0u - ((pb >> leader_lane) & 1u);
             }
             float2 m[2];
 #pragma unroll
@@ -325,8 +331,8 @@ __global__ void __launch_bounds__(64, SEELE_RASTER_MINB) k_raster_quad(Workspace
             const unsigned bb =
                 __ballot_sync(0xffffffffu, (fbits(m[0].x) | fbits(m[0].y) | fbits(m[1].x) | fbits(m[1].y)) != 0u);
             if (bb == 0u) continue;
-            c_blend += (bb & bm) != 0u;
-            if (W == 1) c_alpha += (bb & bm) != 0u;  // each pixel is its own leader
+            count_any(c_blend, bb, bm);
+            if (W == 1) count_any(c_alpha, bb, bm);  // each pixel is its own leader
             float2 y[2];
 #pragma unroll
             for (int r = 0; r < 2; r++) {  // _blend (rasterize.py:169-177) on a pixel pair, masked by 0/1 factors
@@ -356,6 +362,7 @@ __global__ void __launch_bounds__(64, SEELE_RASTER_MINB) k_raster_quad(Workspace
                         slot(Lf, s) = 0.0f;
                         di[s] = step;
                         nlive--;
+                        n_skip -= (uint32_t)__popc(skipped >> j >> 1);
                     } else {
                         ambT |= 1u << s;
                     }
@@ -384,6 +391,7 @@ __global__ void __launch_bounds__(64, SEELE_RASTER_MINB) k_raster_quad(Workspace
                                 slot(Lf, ss) = 0.0f;
                                 di[ss] = step;
                                 nlive--;
+                                n_skip -= (uint32_t)__popc(skipped >> j >> 1);
                             }
                         }
                         ambT &= ~(1u << s);
@@ -396,6 +404,7 @@ __global__ void __launch_bounds__(64, SEELE_RASTER_MINB) k_raster_quad(Workspace
             }
         }
     }
+    cp_async_wait<0>();  // no copy outlives the kernel
     // pixels still live at the end took every splat of the list
     uint32_t n_live = 0, n_blend = 0, mw_steps = 0;
 #pragma unroll
