@@ -259,96 +259,83 @@ __device__ __forceinline__ bool depth_less(double da, uint32_t pa, double db, ui
 // Exact order inside runs of equal 32-bit keys among the binned splats:
 // short runs by the thread at the run start (insertion sort, already sorted
 // by position), runs longer than 32 are queued for k_depth_fix_long.
+// Exact order inside runs of equal quantised keys, out of place (last pass
+// buffers -> kDepthFinal): one thread per position.  A position outside a run
+// is copied; inside a run of <= 32 (found in a shared-memory window of keys
+// with a 32-key halo) its rank among the run's members in (fp64 depth,
+// position) order -- independent loads, no serial chain -- gives its slot.
+// Longer runs are queued by their first position for k_depth_fix_long.
+constexpr int kFixHalo = 32;
+
 __global__ void __launch_bounds__(256) k_depth_fixup(Workspace ws, const int64_t *stats) {
-    constexpr int U = 8;  // positions per thread, keys loaded up front
+    __shared__ uint32_t sk[256 + 2 * kFixHalo];
     const uint32_t n = (uint32_t)stats[SEELE_STAT_BINNED];
-    const uint32_t *key = ws.dkey[kDepthFinal];
-    uint32_t *val = ws.dval[kDepthFinal];
-    const uint32_t i0 = (blockIdx.x * blockDim.x + threadIdx.x) * U;
-    if (i0 + 1 >= n) return;
-    uint32_t k[U + 2];  // k[j + 1] = key[i0 + j], j = -1 .. U
-#pragma unroll
-    for (int j = 0; j < U + 2; j++) {
-        const long long i = (long long)i0 + j - 1;
-        k[j] = (i >= 0 && i < (long long)n) ? key[i] : (j == 0 ? 0xfffffffeu : 0xffffffffu);
+    const uint32_t *key = ws.dkey[kDepthSorted];
+    const uint32_t *src = ws.dval[kDepthSorted];
+    const uint32_t *rsrc = ws.drect[kDepthSorted];
+    uint32_t *dst = ws.dval[kDepthFinal];
+    uint32_t *rdst = ws.drect[kDepthFinal];
+    const long long b0 = (long long)blockIdx.x * 256;
+    if (b0 >= n) return;
+    const int tid = threadIdx.x;
+    for (int k = tid; k < 256 + 2 * kFixHalo; k += 256) {
+        const long long g = b0 - kFixHalo + k;
+        sk[k] = (g >= 0 && g < (long long)n) ? key[g] : 0xffffffffu;  // keys are 24-bit: never equal
     }
-    if (i0 == 0) k[0] = ~k[1];
-#pragma unroll
-    for (int j = 0; j < U; j++) {
-        const uint32_t i = i0 + j;
-        if (i + 1 >= n || k[j + 2] != k[j + 1] || k[j] == k[j + 1]) continue;  // not the start of a run >= 2
-        const uint32_t kk = k[j + 1];
-        uint32_t e = i + 2;
-        while (e < n && e - i < 32 && key[e] == kk) e++;
-        if (e < n && key[e] == kk) {  // long run: queue it
-            while (e < n && key[e] == kk) e++;
+    __syncthreads();
+    const long long i = b0 + tid;
+    if (i >= n) return;
+    const int c = tid + kFixHalo;
+    const uint32_t k = sk[c];
+    const uint32_t p = src[i];
+    if (sk[c - 1] != k && sk[c + 1] != k) {  // not in a run
+        dst[i] = p;
+        rdst[i] = rsrc[i];
+        return;
+    }
+    int s = c, e = c + 1;
+    while (s > 0 && sk[s - 1] == k) s--;
+    while (e < 256 + 2 * kFixHalo && sk[e] == k) e++;
+    if (s == 0 || e == 256 + 2 * kFixHalo || e - s > 32) {  // long run (> 32, or beyond the window)
+        if (sk[c - 1] != k) {  // its first position queues it
+            uint32_t end = (uint32_t)i + 1;
+            while (end < n && key[end] == k) end++;
             const uint32_t slot = atomicAdd(&ws.counters[CNT_LONG_RUNS], 1u);
-            if (slot < kLongRunsMax) ws.long_runs[slot] = make_uint2(i, e - i);
-            continue;
+            if (slot < kLongRunsMax) ws.long_runs[slot] = make_uint2((uint32_t)i, end - (uint32_t)i);
         }
-        const int m = (int)(e - i);
-        uint32_t *rs = ws.drect[kDepthFinal];
-        if (m == 2) {  // the common case: one pair, in registers
-            const uint32_t p0 = val[i], p1 = val[i + 1];
-            const double d0 = ws.depth[p0], d1 = ws.depth[p1];
-            if (depth_less(d1, p1, d0, p0)) {
-                const uint32_t r0 = rs[i];
-                val[i] = p1;
-                val[i + 1] = p0;
-                rs[i] = rs[i + 1];
-                rs[i + 1] = r0;
-            }
-            continue;
-        }
-        uint32_t p[32], rr[32];
-        double d[32];
-        for (int q = 0; q < m; q++) {
-            p[q] = val[i + q];
-            rr[q] = rs[i + q];
-        }
-        for (int q = 0; q < m; q++) d[q] = ws.depth[p[q]];
-        bool moved = false;
-        for (int q = 1; q < m; q++) {
-            const uint32_t pq = p[q], rq = rr[q];
-            const double dq = d[q];
-            int z = q - 1;
-            while (z >= 0 && depth_less(dq, pq, d[z], p[z])) {
-                p[z + 1] = p[z];
-                rr[z + 1] = rr[z];
-                d[z + 1] = d[z];
-                z--;
-            }
-            if (z + 1 != q) moved = true;
-            p[z + 1] = pq;
-            rr[z + 1] = rq;
-            d[z + 1] = dq;
-        }
-        if (moved)
-            for (int q = 0; q < m; q++) {
-                val[i + q] = p[q];
-                rs[i + q] = rr[q];
-            }
+        return;
     }
+    const double d = ws.depth[p];
+    uint32_t rank = 0;
+    for (int q = s; q < e; q++) {
+        if (q == c) continue;
+        const uint32_t pq = src[b0 - kFixHalo + q];
+        rank += depth_less(ws.depth[pq], pq, d, p);
+    }
+    const long long o = b0 - kFixHalo + s + rank;
+    dst[o] = p;
+    rdst[o] = rsrc[i];
 }
 
 // Long equal-key runs (rare: > 32 splats within one quantisation step): one
 // CTA per run, each item's rank = number of run items before it in
-// (depth, position) order.  Runs up to kFixSmem items are staged in shared
-// memory; longer ones are ranked from global memory into the spare buffer.
+// (depth, position) order, read from the last pass's buffer and written to
+// its slot in kDepthFinal.  Runs up to kFixSmem items are staged in shared
+// memory; longer ones are ranked from global memory.
 constexpr int kFixSmem = 4096;
 
 __global__ void __launch_bounds__(512) k_depth_fix_long(Workspace ws) {
     __shared__ double s_d[kFixSmem];
     __shared__ uint32_t s_p[kFixSmem];
     const uint32_t nq = min(ws.counters[CNT_LONG_RUNS], (uint32_t)kLongRunsMax);
-    uint32_t *val = ws.dval[kDepthFinal];
-    uint32_t *spare = ws.dval[kDepthFinal ^ 1];
+    const uint32_t *src = ws.dval[kDepthSorted];
+    uint32_t *dst = ws.dval[kDepthFinal];
     for (uint32_t q = blockIdx.x; q < nq; q += gridDim.x) {
         const uint2 run = ws.long_runs[q];
         const uint32_t s = run.x, m = run.y;
         if (m <= (uint32_t)kFixSmem) {
             for (uint32_t j = threadIdx.x; j < m; j += blockDim.x) {
-                s_p[j] = val[s + j];
+                s_p[j] = src[s + j];
                 s_d[j] = ws.depth[s_p[j]];
             }
             __syncthreads();
@@ -357,27 +344,22 @@ __global__ void __launch_bounds__(512) k_depth_fix_long(Workspace ws) {
                 const uint32_t pj = s_p[j];
                 uint32_t r = 0;
                 for (uint32_t k = 0; k < m; k++) r += depth_less(s_d[k], s_p[k], dj, pj);
-                val[s + r] = pj;
+                dst[s + r] = pj;
                 ws.drect[kDepthFinal][s + r] = pack_rect(ws.rect[pj]);
             }
             __syncthreads();
         } else {
             for (uint32_t j = threadIdx.x; j < m; j += blockDim.x) {
-                const uint32_t pj = val[s + j];
+                const uint32_t pj = src[s + j];
                 const double dj = ws.depth[pj];
                 uint32_t r = 0;
                 for (uint32_t k = 0; k < m; k++) {
-                    const uint32_t pk = val[s + k];
+                    const uint32_t pk = src[s + k];
                     r += depth_less(ws.depth[pk], pk, dj, pj);
                 }
-                spare[s + r] = pj;
+                dst[s + r] = pj;
+                ws.drect[kDepthFinal][s + r] = pack_rect(ws.rect[pj]);
             }
-            __syncthreads();
-            for (uint32_t j = threadIdx.x; j < m; j += blockDim.x) {
-                val[s + j] = spare[s + j];
-                ws.drect[kDepthFinal][s + j] = pack_rect(ws.rect[spare[s + j]]);
-            }
-            __syncthreads();
         }
     }
 }
@@ -596,13 +578,12 @@ struct RowSmem {
 // Emits the row entries of 4096 consecutive entry slots in depth-rank order
 // (ty-major inside a splat, like bin_tiles) and scatters them stably by row:
 // one onesweep pass whose digit is the tile row.
-__global__ void __launch_bounds__(NT, 2) k_row_pass(Workspace ws, int64_t *stats) {
-    extern __shared__ __align__(16) unsigned char smem[];
-    RowSmem &S = *reinterpret_cast<RowSmem *>(smem);
+// One ticket of the row pass; false once the tickets run past the entries.
+__device__ __forceinline__ bool row_tile(const Workspace &ws, int64_t *stats, RowSmem &S) {
     const uint32_t E = ws.counters[CNT_ENTRIES];
     const uint32_t t = take_ticket(&ws.counters[CNT_TICKET + kLookRows]);
     const uint32_t base = t * TILE;
-    if (base >= E) return;
+    if (base >= E) return false;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const uint32_t n = (uint32_t)stats[SEELE_STAT_BINNED];
     const uint32_t *sorted = ws.dval[kDepthFinal];
@@ -687,6 +668,16 @@ __global__ void __launch_bounds__(NT, 2) k_row_pass(Workspace ws, int64_t *stats
         ws.ent_x[dst] = x;
         ws.ent_p[dst] = S.u.g.p[i];
     }
+    return true;
+}
+
+// Persistent: each CTA takes tickets (in order over the grid) until none is left,
+// so the grid is sized to the machine, not to the pair capacity.
+__global__ void __launch_bounds__(NT, 2) k_row_pass(Workspace ws, int64_t *stats) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    RowSmem &S = *reinterpret_cast<RowSmem *>(smem);
+    while (row_tile(ws, stats, S)) __syncthreads();
+
 }
 
 // ---- column pass ---------------------------------------------------------------------
@@ -718,12 +709,11 @@ struct ColSmem {
 // popc(mask_v & lanes_below) -- work proportional to the entry's width.
 // Pairs are staged by column in shared memory and copied out as contiguous
 // runs.
-__global__ void __launch_bounds__(NT, 2) k_col_pass(Workspace ws, int tiles_x, int tiles_y) {
-    extern __shared__ __align__(16) unsigned char smem[];
-    ColSmem &S = *reinterpret_cast<ColSmem *>(smem);
+// One ticket (row chunk) of the column pass; false once the tickets run past the chunks.
+__device__ __forceinline__ bool col_tile(const Workspace &ws, int tiles_x, int tiles_y, ColSmem &S) {
     const uint32_t C = ws.counters[CNT_CHUNKS];
     const uint32_t t = take_ticket(&ws.counters[CNT_TICKET + kLookCols]);
-    if (t >= C) return;
+    if (t >= C) return false;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     for (int y = tid; y < tiles_y; y += NT) S.chunk_first[y] = ws.chunk_first[y];
     __syncthreads();
@@ -856,6 +846,15 @@ __global__ void __launch_bounds__(NT, 2) k_col_pass(Workspace ws, int tiles_x, i
         }
         __syncthreads();
     }
+    return true;
+}
+
+// Persistent, like k_row_pass.
+__global__ void __launch_bounds__(NT, 2) k_col_pass(Workspace ws, int tiles_x, int tiles_y) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    ColSmem &S = *reinterpret_cast<ColSmem *>(smem);
+    while (col_tile(ws, tiles_x, tiles_y, S)) __syncthreads();
+
 }
 
 __global__ void k_fill_pair_tiles(const uint2 *ranges, int n_tiles, int32_t *pair_tile) {
@@ -899,7 +898,7 @@ void launch_depth_sort(const Workspace &ws, long long n_max, int64_t *stats, cud
     set_smem(k_depth_pass, smem);
     const int grid = (int)ceil_div(n_max, TILE);
     for (int p = 0; p < kDepthPasses; p++) k_depth_pass<<<grid, NT, smem, st>>>(ws, p);
-    const int fix_grid = (int)ceil_div(n_max, 256 * 8);
+    const int fix_grid = (int)ceil_div(n_max, 256);
     k_depth_fixup<<<fix_grid > 0 ? fix_grid : 1, 256, 0, st>>>(ws, stats);
     k_depth_fix_long<<<64, 512, 0, st>>>(ws);
     note_launches(3 + kDepthPasses);
@@ -922,9 +921,11 @@ void launch_binning(const Workspace &ws, long long n_max, long long cap, const C
     k_pair_scan<<<scan_grid > 0 ? scan_grid : 1, NT, scan_smem, st>>>(ws, cam.tiles_x, cam.tiles_y, cap, use_smem,
                                                                       stats);
     set_smem(k_row_pass, sizeof(RowSmem));
-    k_row_pass<<<(int)ceil_div(cap, TILE), NT, sizeof(RowSmem), st>>>(ws, stats);
+    const int persist = 2 * sms;  // two CTAs per SM (launch bounds)
+    k_row_pass<<<(int)std::min<long long>(ceil_div(cap, TILE), persist), NT, sizeof(RowSmem), st>>>(ws, stats);
     set_smem(k_col_pass, sizeof(ColSmem));
-    k_col_pass<<<(int)(ceil_div(cap, TILE) + cam.tiles_y), NT, sizeof(ColSmem), st>>>(ws, cam.tiles_x, cam.tiles_y);
+    k_col_pass<<<(int)std::min<long long>(ceil_div(cap, TILE) + cam.tiles_y, persist), NT, sizeof(ColSmem), st>>>(
+        ws, cam.tiles_x, cam.tiles_y);
     note_launches(3);
 }
 
