@@ -146,7 +146,10 @@ __global__ void __launch_bounds__(256) k_depth_hist(Workspace ws) {
 
 // One 8-bit pass of the depth sort.  Pass 0 builds its keys from the
 // preprocess outputs (value = assembled position).
-__global__ void __launch_bounds__(NT, 2) k_depth_pass(Workspace ws, int pass) {
+#ifndef SEELE_DEPTH_MINB
+#define SEELE_DEPTH_MINB 2
+#endif
+__global__ void __launch_bounds__(NT, SEELE_DEPTH_MINB) k_depth_pass(Workspace ws, int pass) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     // every extern __shared__ array of this file aliases one symbol whose alignment may be 4: align here
     unsigned char *smem = reinterpret_cast<unsigned char *>((reinterpret_cast<uintptr_t>(smem_raw) + 15) & ~uintptr_t(15));
@@ -207,7 +210,10 @@ __global__ void __launch_bounds__(NT, 2) k_depth_pass(Workspace ws, int pass) {
     TRACE(pass, t, 1)
 #endif
     uint32_t count;
-    block_rank(dig, pos, rs, count);
+#ifndef SEELE_DEPTH_BALLOT
+#define SEELE_DEPTH_BALLOT 1
+#endif
+    block_rank<SEELE_DEPTH_BALLOT>(dig, pos, rs, count);
     TRACE(pass, t, 2)
     if (tid < RADIX) {
         const uint32_t ex = lookback(ws.look_region(kLookDepth + pass) + tid, RADIX, t,
@@ -579,9 +585,8 @@ struct RowSmem {
 // (ty-major inside a splat, like bin_tiles) and scatters them stably by row:
 // one onesweep pass whose digit is the tile row.
 // One ticket of the row pass; false once the tickets run past the entries.
-__device__ __forceinline__ bool row_tile(const Workspace &ws, int64_t *stats, RowSmem &S) {
+__device__ __forceinline__ bool row_tile(const Workspace &ws, int64_t *stats, RowSmem &S, uint32_t t) {
     const uint32_t E = ws.counters[CNT_ENTRIES];
-    const uint32_t t = take_ticket(&ws.counters[CNT_TICKET + kLookRows]);
     const uint32_t base = t * TILE;
     if (base >= E) return false;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -649,7 +654,10 @@ __device__ __forceinline__ bool row_tile(const Workspace &ws, int64_t *stats, Ro
         }
     }
     uint32_t count;
-    block_rank(dig, pos, S.rs, count);
+#ifndef SEELE_ROW_BALLOT
+#define SEELE_ROW_BALLOT 1
+#endif
+    block_rank<SEELE_ROW_BALLOT>(dig, pos, S.rs, count);
     if (tid < RADIX) {
         const uint32_t ex =
             lookback(ws.look_region(kLookRows) + tid, RADIX, t, *ws.epoch * 16u + kLookRows, count, t == 0);
@@ -676,7 +684,7 @@ __device__ __forceinline__ bool row_tile(const Workspace &ws, int64_t *stats, Ro
 __global__ void __launch_bounds__(NT, 2) k_row_pass(Workspace ws, int64_t *stats) {
     extern __shared__ __align__(16) unsigned char smem[];
     RowSmem &S = *reinterpret_cast<RowSmem *>(smem);
-    while (row_tile(ws, stats, S)) __syncthreads();
+    ticket_loop(&ws.counters[CNT_TICKET + kLookRows], [&](uint32_t t) { return row_tile(ws, stats, S, t); });
 
 }
 
@@ -710,9 +718,8 @@ struct ColSmem {
 // Pairs are staged by column in shared memory and copied out as contiguous
 // runs.
 // One ticket (row chunk) of the column pass; false once the tickets run past the chunks.
-__device__ __forceinline__ bool col_tile(const Workspace &ws, int tiles_x, int tiles_y, ColSmem &S) {
+__device__ __forceinline__ bool col_tile(const Workspace &ws, int tiles_x, int tiles_y, ColSmem &S, uint32_t t) {
     const uint32_t C = ws.counters[CNT_CHUNKS];
-    const uint32_t t = take_ticket(&ws.counters[CNT_TICKET + kLookCols]);
     if (t >= C) return false;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     for (int y = tid; y < tiles_y; y += NT) S.chunk_first[y] = ws.chunk_first[y];
@@ -853,7 +860,8 @@ __device__ __forceinline__ bool col_tile(const Workspace &ws, int tiles_x, int t
 __global__ void __launch_bounds__(NT, 2) k_col_pass(Workspace ws, int tiles_x, int tiles_y) {
     extern __shared__ __align__(16) unsigned char smem[];
     ColSmem &S = *reinterpret_cast<ColSmem *>(smem);
-    while (col_tile(ws, tiles_x, tiles_y, S)) __syncthreads();
+    ticket_loop(&ws.counters[CNT_TICKET + kLookCols],
+                [&](uint32_t t) { return col_tile(ws, tiles_x, tiles_y, S, t); });
 
 }
 

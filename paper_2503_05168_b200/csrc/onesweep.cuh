@@ -3,7 +3,7 @@
 //
 // A pass is ONE kernel: every CTA takes a ticket (dynamic tile id, so every
 // lower tile is already resident when it looks back), ranks its NT * IPT items by
-// digit inside the CTA (warp __match_any_sync + per-warp digit counters in
+// digit inside the CTA (per-bit warp ballots + per-warp digit counters in
 // shared memory, stable in input order), publishes its per-digit counts and
 // resolves their exclusive prefix over the lower tiles by decoupled look-back,
 // then scatters the digit-sorted tile with coalesced runs.  Loads are issued
@@ -132,11 +132,13 @@ struct __align__(16) RankSmem {
     uint32_t total;                // ranked items in the tile
 };
 
-// Stable in-tile ranking.  Item (warp w, round r, lane l) is tile item
+// Stable in-tile ranking; kBallot: peers by per-bit ballots instead of
+// __match_any_sync (faster on sm_100: depth sort 186 -> 165 us).  Item (warp w, round r, lane l) is tile item
 // w * 32 * IPT + r * 32 + l; dig[r] = NO_DIGIT marks an absent item.  On
 // return pos[r] is the item's slot in the digit-sorted tile, sm.start[d] the
 // first slot of digit d, and thread d (< RADIX) holds the tile's count of
 // digit d in `count`.
+template <bool kBallot>
 __device__ __forceinline__ void block_rank(const uint32_t (&dig)[IPT], uint32_t (&pos)[IPT], RankSmem &sm,
                                            uint32_t &count) {
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -147,7 +149,19 @@ __device__ __forceinline__ void block_rank(const uint32_t (&dig)[IPT], uint32_t 
 #pragma unroll
     for (int r = 0; r < IPT; r++) {
         const uint32_t d = dig[r];
-        const unsigned peers = __match_any_sync(0xffffffffu, d);
+        unsigned peers;
+        if (kBallot) {
+            // lanes with the same 8-bit digit: one ballot per bit (absent items excluded)
+            peers = __ballot_sync(0xffffffffu, d != NO_DIGIT);
+#pragma unroll
+            for (int b = 0; b < 8; b++) {
+                const uint32_t bit = (d >> b) & 1u;
+                const unsigned bb = __ballot_sync(0xffffffffu, bit);
+                peers &= bb ^ (bit - 1u);  // bit set: lanes with the bit; clear: lanes without
+            }
+        } else {
+            peers = __match_any_sync(0xffffffffu, d);
+        }
         const uint32_t base = d != NO_DIGIT ? sm.cnt[warp][d] : 0u;
         const uint32_t rk = __popc(peers & lt);
         __syncwarp();
@@ -174,6 +188,20 @@ __device__ __forceinline__ void block_rank(const uint32_t (&dig)[IPT], uint32_t 
     for (int r = 0; r < IPT; r++)
         if (dig[r] != NO_DIGIT) pos[r] += sm.start[dig[r]] + sm.cnt[warp][dig[r]];
     count = total;
+}
+
+// Persistent ticket loop (one ticket at a time: prefetching the next ticket
+// made the look-back chains wait on CTAs still busy with their current one).
+template <typename F>
+__device__ __forceinline__ void ticket_loop(uint32_t *counter, F &&body) {
+    __shared__ uint32_t s_t;
+    while (true) {
+        if (threadIdx.x == 0) s_t = atomicAdd(counter, 1u);
+        __syncthreads();
+        const uint32_t t = s_t;
+        if (!body(t)) break;
+        __syncthreads();
+    }
 }
 
 __device__ __forceinline__ uint32_t take_ticket(uint32_t *counter) {
