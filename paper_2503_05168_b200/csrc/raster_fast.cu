@@ -173,6 +173,7 @@ __global__ void __launch_bounds__(64, SEELE_RASTER_MINB) k_raster_quad(Workspace
     __shared__ float4 s_box[2][2][kBatch];
     // per pixel: tile splats it was live for (written at its death)
     __shared__ uint32_t s_di[64][4];
+    __shared__ float s_T[64][4];  // per pixel: transmittance at its death
     const int tile = (int)ws.tile_order[blockIdx.x];  // heavy tiles first (binning.cu k_pair_scan)
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int mw = tid >> 3, i = tid & 7;
@@ -349,8 +350,9 @@ __global__ void __launch_bounds__(64, SEELE_RASTER_MINB) k_raster_quad(Workspace
                 const float2 d1 = __ffma2_ru(D[r], omm, __fmul2_ru(t0, efm));
                 T[r] = t1;
                 D[r] = d1;
-                // sign set <=> blended and T32 - D < gamma (rounded so that a clear sign proves T >= gamma)
-                y[r] = __ffma2_rn(m[r], __fadd2_rn(t1, __fmul2_rn(__fadd2_ru(d1, f2(gm)), f2(-1.0f))), f2(0.0f));
+                // sign set <=> T32 - D < gamma (rounded so that a clear sign proves T >= gamma); done pixels carry
+                // T = 1e30 (their transmittance is parked in s_T) and never test positive
+                y[r] = __fadd2_rn(t1, __fmul2_rn(__fadd2_ru(d1, f2(gm)), f2(-1.0f)));
                 cnt[r] = __fadd2_rn(cnt[r], m[r]);
             }
             if (__any_sync(0xffffffffu, (int)(fbits(y[0].x) | fbits(y[0].y) | fbits(y[1].x) | fbits(y[1].y)) < 0)) {
@@ -360,6 +362,8 @@ __global__ void __launch_bounds__(64, SEELE_RASTER_MINB) k_raster_quad(Workspace
                     if ((int)fbits(slot(y, s)) >= 0) continue;
                     if (__fadd_ru(slot(T, s), slot(D, s)) < gm) {  // surely below: done
                         slot(Lf, s) = 0.0f;
+                        s_T[tid][s] = slot(T, s);
+                        slot(T, s) = 1e30f;
                         di[s] = step;
                         nlive--;
                         n_skip -= (uint32_t)__popc(skipped >> j >> 1);
@@ -389,6 +393,8 @@ __global__ void __launch_bounds__(64, SEELE_RASTER_MINB) k_raster_quad(Workspace
                             slot(D, ss) = 6.0e-8f * (float)Tx;
                             if (Tx < cfg.gamma) {
                                 slot(Lf, ss) = 0.0f;
+                                s_T[tid][ss] = slot(T, ss);
+                                slot(T, ss) = 1e30f;
                                 di[ss] = step;
                                 nlive--;
                                 n_skip -= (uint32_t)__popc(skipped >> j >> 1);
@@ -436,7 +442,7 @@ __global__ void __launch_bounds__(64, SEELE_RASTER_MINB) k_raster_quad(Workspace
         if (x0 + (s & 1) >= cam.width || y0 + (s >> 1) >= cam.height) continue;
         const long long pix = (long long)(y0 + (s >> 1)) * cam.width + x0 + (s & 1);
         const int r = s >> 1, c = s & 1;
-        const float Ts = slot(T, s);
+        const float Ts = slot(Lf, s) != 0.0f ? slot(T, s) : s_T[tid][s];
         image[3 * pix + 0] = fmaf(Ts, (float)cfg.bg[0], lane_of(C[r][0], c));  // background (rasterize.py:228-231)
         image[3 * pix + 1] = fmaf(Ts, (float)cfg.bg[1], lane_of(C[r][1], c));
         image[3 * pix + 2] = fmaf(Ts, (float)cfg.bg[2], lane_of(C[r][2], c));
