@@ -375,7 +375,10 @@ __global__ void __launch_bounds__(512) k_depth_fix_long(Workspace ws) {
 // Row entries cover at most kSegW columns (wider ones are split; pieces of one
 // splat cover disjoint columns, so the per-column order is unaffected): the
 // column pass's per-entry loops stay short.
-constexpr uint32_t kSegW = 4;
+#ifndef SEELE_SEGW
+#define SEELE_SEGW 3
+#endif
+constexpr uint32_t kSegW = SEELE_SEGW;
 
 // bin_tiles (preprocess.py:159-189) of splat rank r covers rect [x0,x1] x [y0,y1]
 // -> ceil(w / kSegW) row entries per covered tile row y and w * h pairs.
@@ -900,7 +903,10 @@ void launch_frame_begin(const Workspace &ws, const CamK &cam, int64_t *stats, cu
 }
 
 void launch_depth_sort(const Workspace &ws, long long n_max, int64_t *stats, cudaStream_t st) {
-    const int hist_grid = (int)std::min<long long>(ceil_div(n_max, 256 * 8), 2 * 148);
+#ifndef SEELE_HIST_PER_SM
+#define SEELE_HIST_PER_SM 2
+#endif
+    const int hist_grid = (int)std::min<long long>(ceil_div(n_max, 256 * 8), SEELE_HIST_PER_SM * 148);
     k_depth_hist<<<hist_grid > 0 ? hist_grid : 1, 256, 0, st>>>(ws);
     const size_t smem = 16 + sizeof(RankSmem) + 3 * sizeof(uint32_t) * TILE;
     set_smem(k_depth_pass, smem);
