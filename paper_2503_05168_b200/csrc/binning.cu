@@ -931,7 +931,10 @@ void launch_binning(const Workspace &ws, long long n_max, long long cap, const C
     const int use_smem = diff_bytes <= 160 * 1024;
     const size_t scan_smem = use_smem ? diff_bytes : 0;
     set_smem(k_pair_scan, 160 * 1024);
-    const int scan_grid = (int)std::min<long long>(ceil_div(n_max, TILE), 2 * sms);
+#ifndef SEELE_SCAN_PER_SM2
+#define SEELE_SCAN_PER_SM2 4
+#endif
+    const int scan_grid = (int)std::min<long long>(ceil_div(n_max, TILE), SEELE_SCAN_PER_SM2 * sms / 2);
     k_pair_scan<<<scan_grid > 0 ? scan_grid : 1, NT, scan_smem, st>>>(ws, cam.tiles_x, cam.tiles_y, cap, use_smem,
                                                                       stats);
     set_smem(k_row_pass, sizeof(RowSmem));

@@ -153,28 +153,37 @@ __device__ __forceinline__ void load_splat(const SceneK &sc, long long i, int sh
 __device__ __forceinline__ void write_raster_record(const Workspace &ws, long long p, double m0, double m1, double ca,
                                                     double cb, double cc, double o, double qth, float4 col) {
     const double K = 0.72134752044448170368;  // log2(e) / 2
-    const double u = 5.9604644775390625e-08;  // 2^-24
-    const double tr = ca + cc, disc = sqrt(0.25 * (ca - cc) * (ca - cc) + cb * cb);
-    const double lmin = fmax(0.5 * tr - disc, 1e-300);
     const double det = ca * cc - cb * cb;
     float4 rq = make_float4(-INFINITY, -INFINITY, 0.f, 0.f);
     float4 bb = make_float4(INFINITY, -INFINITY, INFINITY, -INFINITY);
     if (qth >= 0.0) {
+        // The error-model terms are upper bounds, so they are evaluated in fp32 and widened by 1.001
+        // (several fp32 roundings); lmin = det / lmax has no cancellation.  Any s > 0 is a valid
+        // linearisation point (AM-GM), so sq needs no rounding care.
+        constexpr float u = 5.9604644775390625e-08f;  // 2^-24
+        constexpr float W = 1.001f;
+        const float caf = (float)ca, cbf = (float)cb, ccf = (float)cc, trf = caf + ccf;
+        const float hd = 0.5f * (caf - ccf);
+        const float lmax = 0.5f * trf + sqrtf(fmaf(hd, hd, cbf * cbf));
+        const float kap = W * trf * lmax / fmaxf((float)det, 1e-30f);  // tr / lmin >= 1
         const double qt = K * qth;
-        const double P = sqrt(K * tr);
-        const double sq = fmax(sqrt(qt), 1e-3);
-        const double e0q = 1.25 * 3.0 * u * P * sq;
-        const double e1q = 1.25 * (u * (4.0 + 10.0 * sqrt(tr / lmin)) + 3.0 * u * P / sq);
-        const double delta = e0q + e1q * qt + qt * (1e-15 * 2.0 * tr / lmin + 2.0 * u) + 1e-30;
-        rq.x = __double2float_rd(qt - delta);
-        rq.y = delta < 1e6 ? __double2float_ru(qt + delta) : INFINITY;
-        rq.z = (float)(4.7e-7 + 0.6931471805599453 * e0q);
-        rq.w = (float)(0.6931471805599453 * e1q);
+        const float qtf = (float)qt;
+        const float P = W * sqrtf((float)K * trf);
+        const float sq = fmaxf(sqrtf(qtf), 1e-3f);
+        const float e0q = W * 1.25f * 3.0f * u * P * sq;
+        const float e1q = W * 1.25f * (u * (4.0f + 10.0f * sqrtf(kap)) + 3.0f * u * P / sq);
+        const float delta = W * (e0q + e1q * qtf + qtf * (1e-15f * 2.0f * kap + 2.0f * u)) + 1e-30f;
+        rq.x = __double2float_rd(qt - (double)delta);
+        rq.y = delta < 1e6f ? __double2float_ru(qt + (double)delta) : INFINITY;
+        rq.z = W * (4.7e-7f + 0.6931471805599453f * e0q);
+        rq.w = W * 0.6931471805599453f * e1q;
         // bounding box of {q <= q_hi' / k}: half extents sqrt(Q Sigma_xx), sqrt(Q Sigma_yy), Sigma = conic^-1
-        const double Q = (double)rq.y / K;
+        // (fp32, widened by 1e-6 relative + 1e-4 px, rounded outward)
+        const float Q = rq.y / (float)K * W;
         if (isfinite(Q) && det > 0.0) {
-            const double hx = sqrt(Q * (cc / det)) * (1.0 + 1e-6) + 1e-4;
-            const double hy = sqrt(Q * (ca / det)) * (1.0 + 1e-6) + 1e-4;
+            const float rdet = 1.0f / (float)det;
+            const double hx = (double)(sqrtf(Q * (ccf * rdet)) * (1.0f + 1e-6f) + 1e-4f);
+            const double hy = (double)(sqrtf(Q * (caf * rdet)) * (1.0f + 1e-6f) + 1e-4f);
             bb = make_float4(__double2float_rd(m0 - hx), __double2float_ru(m0 + hx), __double2float_rd(m1 - hy),
                              __double2float_ru(m1 + hy));
         } else {
@@ -245,8 +254,11 @@ __device__ __forceinline__ void cp_async16(void *smem, const void *gmem) {
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 
+#ifndef SEELE_PRE_MINB
+#define SEELE_PRE_MINB 3
+#endif
 template <int LAYOUT>
-__global__ void __launch_bounds__(256, 3) k_preprocess(SceneK sc, const int64_t *__restrict__ ranges,
+__global__ void __launch_bounds__(256, SEELE_PRE_MINB) k_preprocess(SceneK sc, const int64_t *__restrict__ ranges,
                                                     int n_ranges, CamK cam, CfgK cfg, Workspace ws,
                                                     int64_t *stats) {
     __shared__ long long s_start[SEELE_MAX_RANGES], s_prefix[SEELE_MAX_RANGES + 1];
