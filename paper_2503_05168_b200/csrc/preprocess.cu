@@ -293,9 +293,16 @@ __global__ void __launch_bounds__(256, SEELE_PRE_MINB) k_preprocess(SceneK sc, c
             while (r + 1 < n_ranges && s_prefix[r + 1] <= p) r++;
             const long long i = s_start[r] + (p - s_prefix[r]);
             if (LAYOUT == SEELE_LAYOUT_PLANES) {
-                for (int k = 0; k < 3 * sh_planes; k++) {
-                    const int plane = 3 + 4 * (k / sh_planes) + (k % sh_planes);
-                    cp_async16(&s_sh[k * 256 + threadIdx.x], sc.planes + plane * sc.plane_stride + i);
+                // slot ch * sh_planes + k <- plane 3 + 4 ch + k (no runtime division: the full SH3 case unrolled)
+                const float4 *src = sc.planes + 3 * sc.plane_stride + i;
+                float4 *dst = s_sh + threadIdx.x;
+                if (sh_planes == 4) {
+#pragma unroll
+                    for (int k = 0; k < 12; k++) cp_async16(dst + k * 256, src + k * sc.plane_stride);
+                } else {
+                    for (int ch = 0; ch < 3; ch++)
+                        for (int k = 0; k < sh_planes; k++)
+                            cp_async16(dst + (ch * sh_planes + k) * 256, src + (4 * ch + k) * sc.plane_stride);
                 }
                 cp_async_commit();
             }
