@@ -84,14 +84,11 @@ struct Splat {
 };
 
 __device__ __forceinline__ double sigmoid_clip(double x) {
-    // io.py:33-34 _decode_opacity = clip(sigmoid(x), 1e-12, 1 - 1e-12); sigmoid model.py:44-54
-    double v;
-    if (x >= 0.0) {
-        v = 1.0 / (1.0 + exp(-x));
-    } else {
-        double e = exp(x);
-        v = e / (1.0 + e);
-    }
+    // io.py:33-34 _decode_opacity = clip(sigmoid(x), 1e-12, 1 - 1e-12); sigmoid model.py:44-54:
+    // x >= 0: 1 / (1 + exp(-x)), else exp(x) / (1 + exp(x)) -- the same two formulas with one exp and one
+    // division (a divergent if / else would run both exps in every warp)
+    const double e = exp(-fabs(x));
+    double v = (x >= 0.0 ? 1.0 : e) / (1.0 + e);
     v = v < 1e-12 ? 1e-12 : v;
     v = v > 1.0 - 1e-12 ? 1.0 - 1e-12 : v;
     return v;
@@ -151,7 +148,8 @@ __device__ __forceinline__ void load_splat(const SceneK &sc, long long i, int sh
 // bbox = axis-aligned box of {q' <= q_hi'}; the raster refines it with the
 // exact minimum of q' over each warp's pixel rectangle.
 __device__ __forceinline__ void write_raster_record(const Workspace &ws, long long p, double m0, double m1, double ca,
-                                                    double cb, double cc, double o, double qth, float4 col) {
+                                                    double cb, double cc, double o, double qth, float qth_err,
+                                                    float4 col) {
     const double K = 0.72134752044448170368;  // log2(e) / 2
     const double det = ca * cc - cb * cb;
     float4 rq = make_float4(-INFINITY, -INFINITY, 0.f, 0.f);
@@ -172,7 +170,7 @@ __device__ __forceinline__ void write_raster_record(const Workspace &ws, long lo
         const float sq = fmaxf(sqrtf(qtf), 1e-3f);
         const float e0q = W * 1.25f * 3.0f * u * P * sq;
         const float e1q = W * 1.25f * (u * (4.0f + 10.0f * sqrtf(kap)) + 3.0f * u * P / sq);
-        const float delta = W * (e0q + e1q * qtf + qtf * (1e-15f * 2.0f * kap + 2.0f * u)) + 1e-30f;
+        const float delta = W * (e0q + e1q * qtf + qtf * (1e-15f * 2.0f * kap + 2.0f * u) + (float)K * qth_err) + 1e-30f;
         rq.x = __double2float_rd(qt - (double)delta);
         rq.y = delta < 1e6f ? __double2float_ru(qt + (double)delta) : INFINITY;
         rq.z = W * (4.7e-7f + 0.6931471805599453f * e0q);
@@ -386,9 +384,19 @@ __global__ void __launch_bounds__(256, SEELE_PRE_MINB) k_preprocess(SceneK sc, c
                         col.y = sh_channel([&](int k) { return (float)shp[16 + k]; }, vx, vy, vz, cfg.sh_degree);
                         col.z = sh_channel([&](int k) { return (float)shp[32 + k]; }, vx, vy, vz, cfg.sh_degree);
                     }
-                    const double qth = 2.0 * log(g.o / cfg.alpha_theta);  // alpha >= theta <=> q <= qth
+                    // alpha >= theta <=> q <= qth = 2 ln(o / theta).  qth >= 9 (o >= theta e^4.5) only feeds the
+                    // alpha bracket (r2 clips at 9), which tolerates an fp32 log with its error added to the
+                    // bracket; below that qth sets the opacity-aware radius and is taken in fp64.
+                    double qth;
+                    float qth_err = 0.0f;
+                    if (g.o >= cfg.alpha_theta * (90.0171313005218 * (1.0 + 1e-12))) {
+                        qth = 2.0 * (double)logf((float)g.o / (float)cfg.alpha_theta);
+                        qth_err = 2.0e-6f;  // 2 (two fp32 roundings of the ratio + 1 ulp of logf at <= ~7)
+                    } else {
+                        qth = 2.0 * log(g.o / cfg.alpha_theta);
+                    }
                     double r2 = 9.0;  // MAX_RADIUS_SQ
-                    if (cfg.opacity_aware) {
+                    if (cfg.opacity_aware && qth_err == 0.0f) {  // (fp32 log branch: the true qth >= 9, r2 = 9)
                         r2 = qth;
                         r2 = r2 > 9.0 ? 9.0 : r2;
                         r2 = r2 < 0.0 ? 0.0 : r2;
@@ -409,7 +417,7 @@ __global__ void __launch_bounds__(256, SEELE_PRE_MINB) k_preprocess(SceneK sc, c
                     zbits = (unsigned long long)__double_as_longlong(z);
                     ws.mean[p] = make_double2(m0, m1);
                     ws.conic_op[p] = make_double4(ca, cb, cc, g.o);
-                    write_raster_record(ws, p, m0, m1, ca, cb, cc, g.o, qth, col);
+                    write_raster_record(ws, p, m0, m1, ca, cb, cc, g.o, qth, qth_err, col);
                 }
             }
             ws.status[p] = (uint8_t)status;
