@@ -287,7 +287,11 @@ int seele_render_split(const seele_scene *scene, const int64_t *ranges_dev, int3
     cudaError_t e;
     const int sms = sm_count();
     long long pre_blocks = (n_max + 255) / 256;
-    const int pre_grid = (int)(pre_blocks < 16LL * sms ? (pre_blocks > 0 ? pre_blocks : 1) : 16LL * sms);
+#ifndef SEELE_PRE_GRID_PER_SM
+#define SEELE_PRE_GRID_PER_SM 3  // persistent: the resident CTAs of k_preprocess (launch bounds 256, 3)
+#endif
+    const long long pre_cap = (long long)SEELE_PRE_GRID_PER_SM * sms;
+    const int pre_grid = (int)(pre_blocks < pre_cap ? (pre_blocks > 0 ? pre_blocks : 1) : pre_cap);
     launch_frame_begin(ws, ck, stats_dev, st);
     prof_mark(0, st);
     launch_preprocess(sk, ranges_dev, n_ranges, ck, cf, ws, stats_dev, pre_grid, st);
