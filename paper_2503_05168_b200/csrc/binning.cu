@@ -265,83 +265,91 @@ __device__ __forceinline__ bool depth_less(double da, uint32_t pa, double db, ui
 // Exact order inside runs of equal 32-bit keys among the binned splats:
 // short runs by the thread at the run start (insertion sort, already sorted
 // by position), runs longer than 32 are queued for k_depth_fix_long.
-// Exact order inside runs of equal quantised keys, out of place (last pass
-// buffers -> kDepthFinal): one thread per position.  A position outside a run
-// is copied; inside a run of <= 32 (found in a shared-memory window of keys
-// with a 32-key halo) its rank among the run's members in (fp64 depth,
-// position) order -- independent loads, no serial chain -- gives its slot.
-// Longer runs are queued by their first position for k_depth_fix_long.
-constexpr int kFixHalo = 32;
+// Exact order inside runs of equal quantised keys, in place: a run's members
+// are ranked among themselves in (fp64 depth, position) order -- independent
+// loads, no serial chain -- and written to s + rank after a CTA barrier.  A
+// CTA owns the runs that START in its 256 positions; its 32 extra threads
+// cover the tail of a run that crosses into the next CTA's range (which skips
+// runs started before it), so every run is read and written by one CTA only.
+// Positions outside runs are untouched.  Runs longer than 32 are queued by
+// their first position for k_depth_fix_long.
+constexpr int kFixOwn = 256, kFixHalo = 32, kFixThreads = kFixOwn + kFixHalo;
 
-__global__ void __launch_bounds__(256) k_depth_fixup(Workspace ws, const int64_t *stats) {
-    __shared__ uint32_t sk[256 + 2 * kFixHalo];
+__global__ void __launch_bounds__(kFixThreads) k_depth_fixup(Workspace ws, const int64_t *stats) {
+    __shared__ uint32_t sk[kFixHalo + kFixOwn + 2 * kFixHalo];  // keys [b0 - 32, b0 + 256 + 64)
     const uint32_t n = (uint32_t)stats[SEELE_STAT_BINNED];
-    const uint32_t *key = ws.dkey[kDepthSorted];
-    const uint32_t *src = ws.dval[kDepthSorted];
-    const uint32_t *rsrc = ws.drect[kDepthSorted];
-    uint32_t *dst = ws.dval[kDepthFinal];
-    uint32_t *rdst = ws.drect[kDepthFinal];
-    const long long b0 = (long long)blockIdx.x * 256;
+    const uint32_t *key = ws.dkey[kDepthFinal];
+    uint32_t *val = ws.dval[kDepthFinal];
+    uint32_t *rs = ws.drect[kDepthFinal];
+    const long long b0 = (long long)blockIdx.x * kFixOwn;
     if (b0 >= n) return;
     const int tid = threadIdx.x;
-    for (int k = tid; k < 256 + 2 * kFixHalo; k += 256) {
+    constexpr int kWin = kFixHalo + kFixOwn + 2 * kFixHalo;
+    for (int k = tid; k < kWin; k += kFixThreads) {
         const long long g = b0 - kFixHalo + k;
         sk[k] = (g >= 0 && g < (long long)n) ? key[g] : 0xffffffffu;  // keys are 24-bit: never equal
     }
     __syncthreads();
     const long long i = b0 + tid;
-    if (i >= n) return;
     const int c = tid + kFixHalo;
-    const uint32_t k = sk[c];
-    const uint32_t p = src[i];
-    if (sk[c - 1] != k && sk[c + 1] != k) {  // not in a run
-        dst[i] = p;
-        rdst[i] = rsrc[i];
-        return;
-    }
-    int s = c, e = c + 1;
-    while (s > 0 && sk[s - 1] == k) s--;
-    while (e < 256 + 2 * kFixHalo && sk[e] == k) e++;
-    if (s == 0 || e == 256 + 2 * kFixHalo || e - s > 32) {  // long run (> 32, or beyond the window)
-        if (sk[c - 1] != k) {  // its first position queues it
-            uint32_t end = (uint32_t)i + 1;
-            while (end < n && key[end] == k) end++;
-            const uint32_t slot = atomicAdd(&ws.counters[CNT_LONG_RUNS], 1u);
-            if (slot < kLongRunsMax) ws.long_runs[slot] = make_uint2((uint32_t)i, end - (uint32_t)i);
+    long long out = -1;
+    uint32_t p = 0, rr = 0;
+    if (i < n) {
+        const uint32_t k = sk[c];
+        if (sk[c - 1] == k || sk[c + 1] == k) {  // in a run
+            int s = c, e = c + 1;
+            while (s > 0 && sk[s - 1] == k) s--;
+            while (e < kWin && sk[e] == k) e++;
+            // owned: the run starts in [b0, b0 + 256) (s == 0 means it starts before the window: not ours)
+            if (s >= kFixHalo && s < kFixHalo + kFixOwn) {
+                if (e == kWin || e - s > 32) {  // long run
+                    if (c == s) {
+                        uint32_t end = (uint32_t)i + 1;
+                        while (end < n && key[end] == k) end++;
+                        const uint32_t slot = atomicAdd(&ws.counters[CNT_LONG_RUNS], 1u);
+                        if (slot < kLongRunsMax) ws.long_runs[slot] = make_uint2((uint32_t)i, end - (uint32_t)i);
+                    }
+                } else {
+                    p = val[i];
+                    rr = rs[i];
+                    const double d = ws.depth[p];
+                    uint32_t rank = 0;
+                    for (int q = s; q < e; q++) {
+                        if (q == c) continue;
+                        const uint32_t pq = val[b0 - kFixHalo + q];
+                        rank += depth_less(ws.depth[pq], pq, d, p);
+                    }
+                    out = b0 - kFixHalo + s + rank;
+                }
+            }
         }
-        return;
     }
-    const double d = ws.depth[p];
-    uint32_t rank = 0;
-    for (int q = s; q < e; q++) {
-        if (q == c) continue;
-        const uint32_t pq = src[b0 - kFixHalo + q];
-        rank += depth_less(ws.depth[pq], pq, d, p);
+    __syncthreads();  // every member of every owned run has been read
+    if (out >= 0) {
+        val[out] = p;
+        rs[out] = rr;
     }
-    const long long o = b0 - kFixHalo + s + rank;
-    dst[o] = p;
-    rdst[o] = rsrc[i];
 }
 
 // Long equal-key runs (rare: > 32 splats within one quantisation step): one
 // CTA per run, each item's rank = number of run items before it in
 // (depth, position) order, read from the last pass's buffer and written to
-// its slot in kDepthFinal.  Runs up to kFixSmem items are staged in shared
-// memory; longer ones are ranked from global memory.
+// its slot, in place.  Runs up to kFixSmem items are staged in shared
+// memory; longer ones are ranked from global memory through the spare buffer.
 constexpr int kFixSmem = 4096;
 
 __global__ void __launch_bounds__(512) k_depth_fix_long(Workspace ws) {
     __shared__ double s_d[kFixSmem];
     __shared__ uint32_t s_p[kFixSmem];
     const uint32_t nq = min(ws.counters[CNT_LONG_RUNS], (uint32_t)kLongRunsMax);
-    const uint32_t *src = ws.dval[kDepthSorted];
-    uint32_t *dst = ws.dval[kDepthFinal];
+    uint32_t *val = ws.dval[kDepthFinal];
+    uint32_t *spare = ws.dval[kDepthFinal ^ 1];
     for (uint32_t q = blockIdx.x; q < nq; q += gridDim.x) {
         const uint2 run = ws.long_runs[q];
         const uint32_t s = run.x, m = run.y;
         if (m <= (uint32_t)kFixSmem) {
             for (uint32_t j = threadIdx.x; j < m; j += blockDim.x) {
-                s_p[j] = src[s + j];
+                s_p[j] = val[s + j];
                 s_d[j] = ws.depth[s_p[j]];
             }
             __syncthreads();
@@ -350,22 +358,27 @@ __global__ void __launch_bounds__(512) k_depth_fix_long(Workspace ws) {
                 const uint32_t pj = s_p[j];
                 uint32_t r = 0;
                 for (uint32_t k = 0; k < m; k++) r += depth_less(s_d[k], s_p[k], dj, pj);
-                dst[s + r] = pj;
+                val[s + r] = pj;
                 ws.drect[kDepthFinal][s + r] = pack_rect(ws.rect[pj]);
             }
             __syncthreads();
-        } else {
+        } else {  // ranked from global memory into the other ping-pong buffer, then copied back
             for (uint32_t j = threadIdx.x; j < m; j += blockDim.x) {
-                const uint32_t pj = src[s + j];
+                const uint32_t pj = val[s + j];
                 const double dj = ws.depth[pj];
                 uint32_t r = 0;
                 for (uint32_t k = 0; k < m; k++) {
-                    const uint32_t pk = src[s + k];
+                    const uint32_t pk = val[s + k];
                     r += depth_less(ws.depth[pk], pk, dj, pj);
                 }
-                dst[s + r] = pj;
-                ws.drect[kDepthFinal][s + r] = pack_rect(ws.rect[pj]);
+                spare[s + r] = pj;
             }
+            __syncthreads();
+            for (uint32_t j = threadIdx.x; j < m; j += blockDim.x) {
+                val[s + j] = spare[s + j];
+                ws.drect[kDepthFinal][s + j] = pack_rect(ws.rect[spare[s + j]]);
+            }
+            __syncthreads();
         }
     }
 }
@@ -912,8 +925,8 @@ void launch_depth_sort(const Workspace &ws, long long n_max, int64_t *stats, cud
     set_smem(k_depth_pass, smem);
     const int grid = (int)ceil_div(n_max, TILE);
     for (int p = 0; p < kDepthPasses; p++) k_depth_pass<<<grid, NT, smem, st>>>(ws, p);
-    const int fix_grid = (int)ceil_div(n_max, 256);
-    k_depth_fixup<<<fix_grid > 0 ? fix_grid : 1, 256, 0, st>>>(ws, stats);
+    const int fix_grid = (int)ceil_div(n_max, kFixOwn);
+    k_depth_fixup<<<fix_grid > 0 ? fix_grid : 1, kFixThreads, 0, st>>>(ws, stats);
     k_depth_fix_long<<<64, 512, 0, st>>>(ws);
     note_launches(3 + kDepthPasses);
 }

@@ -57,8 +57,7 @@ enum {
 #endif
 constexpr int kSortTile = SEELE_SORT_NT * SEELE_SORT_IPT;  // items per onesweep CTA tile (onesweep.cuh TILE)
 constexpr int kDepthPasses = 3;   // 8-bit passes of the 24-bit depth key
-constexpr int kDepthSorted = (kDepthPasses - 1) & 1;  // ping-pong buffer the last radix pass writes
-constexpr int kDepthFinal = kDepthSorted ^ 1;          // the exact order (ties fixed), written by the fix-up
+constexpr int kDepthFinal = (kDepthPasses - 1) & 1;  // ping-pong buffer holding the sorted order (ties fixed in place)
 constexpr int kLongRunsMax = 4096; // equal-key runs longer than this many go to the CTA fix-up
 constexpr int kMaxTileAxis = 256;  // tiles per image axis (row / column digits fit one pass)
 constexpr int kLookDepth = 0;     // look-back regions (pass ids)
@@ -88,8 +87,7 @@ struct Workspace {
     RasterRec *rec;      // FAST raster records (also the colour of the exact engine)
     float4 *bbox;        // (x_min, x_max, y_min, y_max) of {q' < q_up} in pixel coordinates
     // depth sort (ping-pong): key = depth quantised monotonically to 24 bits,
-    // value = assembled position; the radix passes end in dkey/dval[kDepthSorted], the
-    // exact order (ties fixed) in dval/drect[kDepthFinal]
+    // value = assembled position; the sorted order ends in dkey/dval[kDepthFinal]
     uint32_t *dkey[2];
     uint32_t *dval[2];
     uint32_t *drect[2];  // tile rect carried with each item: x0 | x1 << 8 | y0 << 16 | y1 << 24
