@@ -697,7 +697,10 @@ __device__ __forceinline__ bool row_tile(const Workspace &ws, int64_t *stats, Ro
 
 // Persistent: each CTA takes tickets (in order over the grid) until none is left,
 // so the grid is sized to the machine, not to the pair capacity.
-__global__ void __launch_bounds__(NT, 2) k_row_pass(Workspace ws, int64_t *stats) {
+#ifndef SEELE_ROW_MINB
+#define SEELE_ROW_MINB 2
+#endif
+__global__ void __launch_bounds__(NT, SEELE_ROW_MINB) k_row_pass(Workspace ws, int64_t *stats) {
     extern __shared__ __align__(16) unsigned char smem[];
     RowSmem &S = *reinterpret_cast<RowSmem *>(smem);
     ticket_loop(&ws.counters[CNT_TICKET + kLookRows], [&](uint32_t t) { return row_tile(ws, stats, S, t); });
@@ -873,7 +876,10 @@ __device__ __forceinline__ bool col_tile(const Workspace &ws, int tiles_x, int t
 }
 
 // Persistent, like k_row_pass.
-__global__ void __launch_bounds__(NT, 2) k_col_pass(Workspace ws, int tiles_x, int tiles_y) {
+#ifndef SEELE_COL_MINB
+#define SEELE_COL_MINB 2
+#endif
+__global__ void __launch_bounds__(NT, SEELE_COL_MINB) k_col_pass(Workspace ws, int tiles_x, int tiles_y) {
     extern __shared__ __align__(16) unsigned char smem[];
     ColSmem &S = *reinterpret_cast<ColSmem *>(smem);
     ticket_loop(&ws.counters[CNT_TICKET + kLookCols],
