@@ -64,6 +64,14 @@ __device__ __forceinline__ void count_any(uint32_t &c, unsigned ballot, unsigned
         : "+r"(c)
         : "r"(ballot), "r"(mask));
 }
+// lf & (sign of d ? ~0 : 0) & g as a shift + one LOP3 (kept out of predicate/select form)
+__device__ __forceinline__ uint32_t sign_and(float d, uint32_t lf, uint32_t g) {
+    uint32_t r;
+    asm("{\n\t.reg .b32 t;\n\tshr.s32 t, %1, 31;\n\tlop3.b32 %0, t, %2, %3, 0x80;\n\t}"
+        : "=r"(r)
+        : "r"(__float_as_uint(d)), "r"(lf), "r"(g));
+    return r;
+}
 // all-ones if the sign bit of x is set, else 0
 __device__ __forceinline__ uint32_t sign_mask(float x) { return (uint32_t)((int)__float_as_uint(x) >> 31); }
 
@@ -327,8 +335,8 @@ __global__ void __launch_bounds__(64, SEELE_RASTER_MINB) k_raster_quad(Workspace
             float2 m[2];
 #pragma unroll
             for (int r = 0; r < 2; r++)
-                m[r] = make_float2(__uint_as_float(sign_mask(d[r].x) & fbits(Lf[r].x) & my),
-                                   __uint_as_float(sign_mask(d[r].y) & fbits(Lf[r].y) & my));
+                m[r] = make_float2(__uint_as_float(sign_and(d[r].x, fbits(Lf[r].x), my)),
+                                   __uint_as_float(sign_and(d[r].y, fbits(Lf[r].y), my)));
             const unsigned bb =
                 __ballot_sync(0xffffffffu, (fbits(m[0].x) | fbits(m[0].y) | fbits(m[1].x) | fbits(m[1].y)) != 0u);
             if (bb == 0u) continue;
