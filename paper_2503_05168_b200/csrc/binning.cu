@@ -449,7 +449,10 @@ __global__ void __launch_bounds__(NT) k_pair_scan(Workspace ws, int tiles_x, int
         }
         uint32_t agg;
         const uint32_t ex = block_scan<uint32_t>(sum, agg);
-        if (tid == 0) s_prev = lookback(ws.look_region(kLookScan), 1, t, *ws.epoch * 16u + kLookScan, agg, t == 0);
+        if (tid < 32) {  // one warp: 32 predecessors per round trip
+            const uint32_t pv = lookback_warp(ws.look_region(kLookScan), t, *ws.epoch * 16u + kLookScan, agg, t == 0);
+            if (tid == 0) s_prev = pv;
+        }
         __syncthreads();
         uint32_t run = s_prev + ex;
 #pragma unroll

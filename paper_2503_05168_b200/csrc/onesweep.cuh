@@ -101,6 +101,40 @@ __device__ __forceinline__ uint32_t lookback(unsigned long long *col, int stride
     return sum;
 }
 
+// Look-back of a single column (stride 1) by one whole warp: the 32 lanes
+// read 32 predecessors per round trip (coalesced), the warp consumes them in
+// order up to the first one not yet published or the first inclusive prefix.
+// Returns the exclusive prefix in every lane.
+__device__ __forceinline__ uint32_t lookback_warp(unsigned long long *col, uint32_t tile, uint32_t epoch,
+                                                  uint32_t mine, bool start) {
+    const int lane = threadIdx.x & 31;
+    if (start) {
+        if (lane == 0) publish(col + tile, epoch, FLAG_INC, mine);
+        return 0u;
+    }
+    if (lane == 0) publish(col + tile, epoch, FLAG_AGG, mine);
+    uint32_t sum = 0;
+    long long j = (long long)tile - 1;
+    while (true) {
+        const long long jj = j - lane;
+        const unsigned long long x = jj >= 0 ? peek(col + jj) : 0ull;
+        const bool valid = jj >= 0 && (uint32_t)(x >> 32) == epoch;
+        const unsigned vb = __ballot_sync(0xffffffffu, valid);
+        const unsigned ib = __ballot_sync(0xffffffffu, valid && ((uint32_t)x & FLAG_INC) != 0u);
+        const int gap = ~vb ? __ffs(~vb) - 1 : 32;
+        const int inc = ib ? __ffs(ib) - 1 : 32;
+        const bool done = inc < gap;
+        const int take = done ? inc + 1 : gap;
+        sum += __reduce_add_sync(0xffffffffu, lane < take ? ((uint32_t)x & VAL_MASK) : 0u);
+        if (sum > VAL_MASK) sum = VAL_MASK;
+        if (done) break;
+        j -= take;
+        if (take == 0) __nanosleep(32);  // predecessor still counting
+    }
+    if (lane == 0) publish(col + tile, epoch, FLAG_INC, sum + mine);
+    return sum;
+}
+
 // 256-thread block exclusive scan of one value per thread (uses its own smem).
 template <typename T>
 __device__ __forceinline__ T block_scan(T v, T &total) {
