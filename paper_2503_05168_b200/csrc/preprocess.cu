@@ -252,11 +252,15 @@ __device__ __forceinline__ void cp_async16(void *smem, const void *gmem) {
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 
-#ifndef SEELE_PRE_MINB
-#define SEELE_PRE_MINB 3
+#ifndef SEELE_PRE_THREADS
+#define SEELE_PRE_THREADS 256
 #endif
+#ifndef SEELE_PRE_MINB
+#define SEELE_PRE_MINB (768 / SEELE_PRE_THREADS)
+#endif
+constexpr int kPre = SEELE_PRE_THREADS;  // threads per CTA
 template <int LAYOUT>
-__global__ void __launch_bounds__(256, SEELE_PRE_MINB) k_preprocess(SceneK sc, const int64_t *__restrict__ ranges,
+__global__ void __launch_bounds__(kPre, SEELE_PRE_MINB) k_preprocess(SceneK sc, const int64_t *__restrict__ ranges,
                                                     int n_ranges, CamK cam, CfgK cfg, Workspace ws,
                                                     int64_t *stats) {
     __shared__ long long s_start[SEELE_MAX_RANGES], s_prefix[SEELE_MAX_RANGES + 1];
@@ -296,11 +300,11 @@ __global__ void __launch_bounds__(256, SEELE_PRE_MINB) k_preprocess(SceneK sc, c
                 float4 *dst = s_sh + threadIdx.x;
                 if (sh_planes == 4) {
 #pragma unroll
-                    for (int k = 0; k < 12; k++) cp_async16(dst + k * 256, src + k * sc.plane_stride);
+                    for (int k = 0; k < 12; k++) cp_async16(dst + k * kPre, src + k * sc.plane_stride);
                 } else {
                     for (int ch = 0; ch < 3; ch++)
                         for (int k = 0; k < sh_planes; k++)
-                            cp_async16(dst + (ch * sh_planes + k) * 256, src + (4 * ch + k) * sc.plane_stride);
+                            cp_async16(dst + (ch * sh_planes + k) * kPre, src + (4 * ch + k) * sc.plane_stride);
                 }
                 cp_async_commit();
             }
@@ -367,7 +371,7 @@ __global__ void __launch_bounds__(256, SEELE_PRE_MINB) k_preprocess(SceneK sc, c
 #pragma unroll
                             for (int k = 0; k < 4; k++) {
                                 float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-                                if (k < sh_planes) v = s_sh[(ch * sh_planes + k) * 256 + threadIdx.x];
+                                if (k < sh_planes) v = s_sh[(ch * sh_planes + k) * kPre + threadIdx.x];
                                 shc[4 * k] = v.x;
                                 shc[4 * k + 1] = v.y;
                                 shc[4 * k + 2] = v.z;
@@ -480,17 +484,18 @@ __global__ void k_select(CamK cam, const double *__restrict__ centroids, int n, 
 
 void launch_preprocess(const SceneK &s, const int64_t *ranges, int n_ranges, const CamK &cam,
                        const CfgK &cfg, const Workspace &ws, int64_t *stats, int grid, cudaStream_t st) {
+    grid *= 256 / kPre;  // the caller sizes the grid in 256-thread CTAs
     if (s.layout == SEELE_LAYOUT_PLANES) {
-        constexpr int kShSmem = 12 * 256 * sizeof(float4);
+        constexpr int kShSmem = 12 * kPre * sizeof(float4);
         static bool attr = false;
         if (!attr) {
             cudaFuncSetAttribute(k_preprocess<SEELE_LAYOUT_PLANES>, cudaFuncAttributeMaxDynamicSharedMemorySize, kShSmem);
             attr = true;
         }
-        k_preprocess<SEELE_LAYOUT_PLANES><<<grid, 256, kShSmem, st>>>(s, ranges, n_ranges, cam, cfg, ws, stats);
+        k_preprocess<SEELE_LAYOUT_PLANES><<<grid, kPre, kShSmem, st>>>(s, ranges, n_ranges, cam, cfg, ws, stats);
     }
     else
-        k_preprocess<SEELE_LAYOUT_F64><<<grid, 256, 0, st>>>(s, ranges, n_ranges, cam, cfg, ws, stats);
+        k_preprocess<SEELE_LAYOUT_F64><<<grid, kPre, 0, st>>>(s, ranges, n_ranges, cam, cfg, ws, stats);
     note_launches(1);
 }
 

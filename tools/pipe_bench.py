@@ -25,7 +25,7 @@ for f in range(0, 120, 3):
 del probe
 cap = int(need * 1.05) + 4096
 main = torch.cuda.current_stream(dev)
-for depth, split in ((1, False), (2, False), (3, False), (4, False), (3, True)):
+for depth, split in ((1, False), (3, False), (2, True), (3, True), (4, True)):
     pipe = FramePipeline(rr, args.width, args.height, depth=depth, pair_capacity=cap, split=split)
     for k in range(6):
         pipe.submit(poses[k], cfg)
