@@ -99,6 +99,9 @@ __device__ __forceinline__ void quad_q(const Staged &sg, float2 lxp, float2 lyp,
 // [x0, x1] x [y0, y1] (tile-relative) can have q' <= qmax: the minimum of q'
 // over the rectangle is 0 if the mean lies inside, else it lies on an edge,
 // where it is a 1D quadratic minimised in closed form (Cholesky coordinates).
+// The minimiser may be computed approximately (fast division): q' is evaluated
+// exactly at the point taken, and at an interior minimum an error e in its
+// position changes q' only by O(e^2), far inside the margin.
 __device__ __forceinline__ bool rect_reaches(float mx, float my, float l11, float l21, float l22, float qmax, float x0,
                                              float x1, float y0, float y1) {
     if (mx >= x0 && mx <= x1 && my >= y0 && my <= y1) return true;
@@ -107,14 +110,14 @@ __device__ __forceinline__ bool rect_reaches(float mx, float my, float l11, floa
 #pragma unroll
     for (int e = 0; e < 2; e++) {  // horizontal edges y = y0, y1: minimiser dx = -l21 dy / l11
         const float dy = (e ? y1 : y0) - my;
-        const float dx = fminf(fmaxf(-l21 * dy / l11, x0 - mx), x1 - mx);
+        const float dx = fminf(fmaxf(__fdividef(-l21 * dy, l11), x0 - mx), x1 - mx);
         const float u1 = fmaf(l11, dx, l21 * dy), u2 = l22 * dy;
         qmin = fminf(qmin, fmaf(u1, u1, u2 * u2));
     }
 #pragma unroll
     for (int e = 0; e < 2; e++) {  // vertical edges x = x0, x1: minimiser dy = -l11 l21 dx / (l21^2 + l22^2)
         const float dx = (e ? x1 : x0) - mx;
-        const float dy = fminf(fmaxf(-l11 * l21 * dx / cyy, y0 - my), y1 - my);
+        const float dy = fminf(fmaxf(__fdividef(-l11 * l21 * dx, cyy), y0 - my), y1 - my);
         const float u1 = fmaf(l11, dx, l21 * dy), u2 = l22 * dy;
         qmin = fminf(qmin, fmaf(u1, u1, u2 * u2));
     }
