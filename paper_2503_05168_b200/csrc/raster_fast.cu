@@ -72,6 +72,12 @@ __device__ __forceinline__ uint32_t sign_and(float d, uint32_t lf, uint32_t g) {
         : "r"(__float_as_uint(d)), "r"(lf), "r"(g));
     return r;
 }
+// sqrt within a few ulp (MUFU), for bounds that are widened anyway
+__device__ __forceinline__ float sqrt_approx(float x) {
+    float y;
+    asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
 // all-ones if the sign bit of x is set, else 0
 __device__ __forceinline__ uint32_t sign_mask(float x) { return (uint32_t)((int)__float_as_uint(x) >> 31); }
 
@@ -268,10 +274,11 @@ __global__ void __launch_bounds__(64, SEELE_RASTER_MINB) k_raster_quad(Workspace
                 // bracket width) and the float mean, |error| <= ep = 2^-23 (|d| + 32) px, times
                 // |grad q'| <= 2 P sqrt(q')
                 const float mx = (sv.mxh - (float)ox) + sv.mxl, my = (sv.myh - (float)oy) + sv.myl;
-                const float P = sqrtf(fmaf(sv.l11, sv.l11, fmaf(sv.l21, sv.l21, sv.l22 * sv.l22)));
+                // (margin terms only need upper bounds: approximate square roots, widened by 1e-4)
+                const float P = 1.0001f * sqrt_approx(fmaf(sv.l11, sv.l11, fmaf(sv.l21, sv.l21, sv.l22 * sv.l22)));
                 const float ep = 1.2e-7f * (fabsf(mx) + fabsf(my) + 32.0f);
                 const float qh = sv.q_up, pe = P * ep;
-                const float qm = qh + 2.0f * (qh - sv.q_lo) + 1e-6f * qh + 2.2f * pe * sqrtf(fmaxf(qh, 0.f)) +
+                const float qm = qh + 2.0f * (qh - sv.q_lo) + 1e-6f * qh + 2.2f * pe * (1.0001f * sqrt_approx(fmaxf(qh, 0.f))) +
                                  1.1f * pe * pe + 1e-6f;
                 rel = rect_reaches(mx, my, sv.l11, sv.l21, sv.l22, qm, 0.5f, 15.5f, ry0, ry1);
             }
