@@ -149,14 +149,19 @@ __global__ void __launch_bounds__(256) k_depth_hist(Workspace ws) {
 #ifndef SEELE_DEPTH_MINB
 #define SEELE_DEPTH_MINB 2
 #endif
+#ifndef SEELE_DEPTH_IPT
+#define SEELE_DEPTH_IPT 8
+#endif
+constexpr int DIPT = SEELE_DEPTH_IPT;  // items per thread of the depth passes
+constexpr int DTILE = NT * DIPT;
 __global__ void __launch_bounds__(NT, SEELE_DEPTH_MINB) k_depth_pass(Workspace ws, int pass) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     // every extern __shared__ array of this file aliases one symbol whose alignment may be 4: align here
     unsigned char *smem = reinterpret_cast<unsigned char *>((reinterpret_cast<uintptr_t>(smem_raw) + 15) & ~uintptr_t(15));
     RankSmem &rs = *reinterpret_cast<RankSmem *>(smem);
     uint32_t *skey = reinterpret_cast<uint32_t *>(smem + sizeof(RankSmem));
-    uint32_t *sval = skey + TILE;
-    uint32_t *srect = sval + TILE;
+    uint32_t *sval = skey + DTILE;
+    uint32_t *srect = sval + DTILE;
     __shared__ uint32_t s_base[RADIX];
 #ifdef SEELE_SORT_TRACE
     const unsigned long long t_enter = gtime();
@@ -164,27 +169,27 @@ __global__ void __launch_bounds__(NT, SEELE_DEPTH_MINB) k_depth_pass(Workspace w
     const uint32_t t = take_ticket(&ws.counters[CNT_TICKET + kLookDepth + pass]);
     // pass 0 reads every assembled splat and keeps the binned ones; later passes sort only those
     const uint32_t n = pass == 0 ? ws.counters[CNT_WS] : (uint32_t)ws.counters_binned();
-    const uint32_t t0 = t * TILE;
+    const uint32_t t0 = t * DTILE;
     if (t0 >= n) return;
 #ifdef SEELE_SORT_TRACE
     if (threadIdx.x == 0 && t < 4096) g_trace[pass][t][0] = t_enter;
 #endif
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int shift = 8 * pass;
-    uint32_t key[IPT], val[IPT], rcv[IPT], dig[IPT], pos[IPT];
-    const uint32_t ib = t0 + warp * 32 * IPT + lane;
+    uint32_t key[DIPT], val[DIPT], rcv[DIPT], dig[DIPT], pos[DIPT];
+    const uint32_t ib = t0 + warp * 32 * DIPT + lane;
     if (pass == 0) {
         const DepthKey dk = depth_key(ws);
-        short4 tl[IPT];
-        double d[IPT];
+        short4 tl[DIPT];
+        double d[DIPT];
 #pragma unroll
-        for (int r = 0; r < IPT; r++) {
+        for (int r = 0; r < DIPT; r++) {
             const uint32_t i = min(ib + r * 32, n - 1);
             tl[r] = ws.rect[i];
             d[r] = ws.depth[i];
         }
 #pragma unroll
-        for (int r = 0; r < IPT; r++) {
+        for (int r = 0; r < DIPT; r++) {
             key[r] = depth_quant(dk, tl[r], d[r]);
             val[r] = ib + r * 32;
             rcv[r] = (uint32_t)(tl[r].x & 0xff) | ((uint32_t)(tl[r].y & 0xff) << 8) | ((uint32_t)(tl[r].z & 0xff) << 16) |
@@ -195,7 +200,7 @@ __global__ void __launch_bounds__(NT, SEELE_DEPTH_MINB) k_depth_pass(Workspace w
         const uint32_t *vin = ws.dval[(pass + 1) & 1];
         const uint32_t *rin = ws.drect[(pass + 1) & 1];
 #pragma unroll
-        for (int r = 0; r < IPT; r++) {
+        for (int r = 0; r < DIPT; r++) {
             const uint32_t i = min(ib + r * 32, n - 1);
             key[r] = kin[i];
             val[r] = vin[i];
@@ -203,7 +208,7 @@ __global__ void __launch_bounds__(NT, SEELE_DEPTH_MINB) k_depth_pass(Workspace w
         }
     }
 #pragma unroll
-    for (int r = 0; r < IPT; r++)
+    for (int r = 0; r < DIPT; r++)
         dig[r] = ib + r * 32 < n && key[r] != 0xffffffu ? (key[r] >> shift) & 0xffu : NO_DIGIT;
 #ifdef SEELE_SORT_TRACE
     __syncthreads();
@@ -213,7 +218,7 @@ __global__ void __launch_bounds__(NT, SEELE_DEPTH_MINB) k_depth_pass(Workspace w
 #ifndef SEELE_DEPTH_BALLOT
 #define SEELE_DEPTH_BALLOT 1
 #endif
-    block_rank<SEELE_DEPTH_BALLOT>(dig, pos, rs, count);
+    block_rank<SEELE_DEPTH_BALLOT, DIPT>(dig, pos, rs, count);
     TRACE(pass, t, 2)
     if (tid < RADIX) {
         const uint32_t ex = lookback(ws.look_region(kLookDepth + pass) + tid, RADIX, t,
@@ -225,7 +230,7 @@ __global__ void __launch_bounds__(NT, SEELE_DEPTH_MINB) k_depth_pass(Workspace w
     TRACE(pass, t, 3)
 #endif
 #pragma unroll
-    for (int r = 0; r < IPT; r++) {
+    for (int r = 0; r < DIPT; r++) {
         if (dig[r] == NO_DIGIT) continue;
         skey[pos[r]] = key[r];
         sval[pos[r]] = val[r];
@@ -930,9 +935,9 @@ void launch_depth_sort(const Workspace &ws, long long n_max, int64_t *stats, cud
 #endif
     const int hist_grid = (int)std::min<long long>(ceil_div(n_max, 256 * 8), SEELE_HIST_PER_SM * 148);
     k_depth_hist<<<hist_grid > 0 ? hist_grid : 1, 256, 0, st>>>(ws);
-    const size_t smem = 16 + sizeof(RankSmem) + 3 * sizeof(uint32_t) * TILE;
+    const size_t smem = 16 + sizeof(RankSmem) + 3 * sizeof(uint32_t) * DTILE;
     set_smem(k_depth_pass, smem);
-    const int grid = (int)ceil_div(n_max, TILE);
+    const int grid = (int)ceil_div(n_max, DTILE);
     for (int p = 0; p < kDepthPasses; p++) k_depth_pass<<<grid, NT, smem, st>>>(ws, p);
     const int fix_grid = (int)ceil_div(n_max, kFixOwn);
     k_depth_fixup<<<fix_grid > 0 ? fix_grid : 1, kFixThreads, 0, st>>>(ws, stats);

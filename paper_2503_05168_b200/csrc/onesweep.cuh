@@ -177,8 +177,8 @@ struct __align__(16) RankSmem {
 // return pos[r] is the item's slot in the digit-sorted tile, sm.start[d] the
 // first slot of digit d, and thread d (< RADIX) holds the tile's count of
 // digit d in `count`.
-template <bool kBallot>
-__device__ __forceinline__ void block_rank(const uint32_t (&dig)[IPT], uint32_t (&pos)[IPT], RankSmem &sm,
+template <bool kBallot, int IPT_ = IPT>
+__device__ __forceinline__ void block_rank(const uint32_t (&dig)[IPT_], uint32_t (&pos)[IPT_], RankSmem &sm,
                                            uint32_t &count) {
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
 #pragma unroll
@@ -186,7 +186,7 @@ __device__ __forceinline__ void block_rank(const uint32_t (&dig)[IPT], uint32_t 
     __syncwarp();
     const unsigned lt = (1u << lane) - 1u;
 #pragma unroll
-    for (int r = 0; r < IPT; r++) {
+    for (int r = 0; r < IPT_; r++) {
         const uint32_t d = dig[r];
         unsigned peers;
         if (kBallot) {
@@ -224,7 +224,7 @@ __device__ __forceinline__ void block_rank(const uint32_t (&dig)[IPT], uint32_t 
     if (tid == 0) sm.total = all;
     __syncthreads();
 #pragma unroll
-    for (int r = 0; r < IPT; r++)
+    for (int r = 0; r < IPT_; r++)
         if (dig[r] != NO_DIGIT) pos[r] += sm.start[dig[r]] + sm.cnt[warp][dig[r]];
     count = total;
 }
