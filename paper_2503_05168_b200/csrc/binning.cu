@@ -406,6 +406,13 @@ constexpr uint32_t kSegW = SEELE_SEGW;
 // 2D difference array of per-tile pair counts and the 1D one of per-row entry
 // counts.  The last CTA turns those into the tile ranges (sorting.py:46-53),
 // the row bases of the row pass and the chunk table of the column pass.
+// raster launch order bucket of a tile with c pairs: 32 - bits(c), heavy tiles first
+#ifndef SEELE_LIGHT_FIRST
+__device__ __forceinline__ int tile_bucket(uint32_t c) { return __clz(c); }
+#else
+__device__ __forceinline__ int tile_bucket(uint32_t c) { return 32 - __clz(c); }
+#endif
+
 __global__ void __launch_bounds__(NT) k_pair_scan(Workspace ws, int tiles_x, int tiles_y, long long cap, int use_smem,
                                                   int64_t *stats) {
     extern __shared__ int32_t s_diff[];  // [(tiles_y + 1) * (tiles_x + 1)] if use_smem
@@ -545,7 +552,7 @@ __global__ void __launch_bounds__(NT) k_pair_scan(Workspace ws, int tiles_x, int
         const uint32_t c = (uint32_t)g[(i / tiles_x) * tx1 + i % tiles_x];
         ws.ranges[i] = over ? make_uint2(0u, 0u) : make_uint2(acc, acc + c);
         acc += c;
-        atomicAdd(&s_bucket[32 - (32 - __clz(c))], 1u);  // bucket 32 - bits(c): heavy tiles in low buckets
+        atomicAdd(&s_bucket[tile_bucket(c)], 1u);
     }
     __syncthreads();
     if (tid == 0) {  // exclusive scan over the 33 buckets
@@ -559,7 +566,7 @@ __global__ void __launch_bounds__(NT) k_pair_scan(Workspace ws, int tiles_x, int
     __syncthreads();
     for (int i = a0; i < a1; i++) {  // raster launch order (within a bucket arbitrary; results do not depend on it)
         const uint32_t c = (uint32_t)g[(i / tiles_x) * tx1 + i % tiles_x];
-        ws.tile_order[atomicAdd(&s_bucket[32 - (32 - __clz(c))], 1u)] = (uint32_t)i;
+        ws.tile_order[atomicAdd(&s_bucket[tile_bucket(c)], 1u)] = (uint32_t)i;
     }
     // entries per row -> row bases (row pass digit bases) and column-pass chunks
     for (int i = tid; i <= tiles_y; i += NT) s_row[i] = *(volatile int32_t *)&ws.row_diff[i];
