@@ -1,8 +1,9 @@
 """GPU edge cases of the sort / binning / raster path against the oracle:
 long runs of equal (and nearly equal) depths (the depth sort's exact fp64
 fix-up, including the CTA path for runs longer than 32), very wide splats
-(row entries split into 8-column segments), many tile rows and columns, and
-a frame with no binned splat."""
+(row entries split into 3-column segments), many tile rows and columns, runs
+of ties of every length 2..40 crossing the fix-up's 256-position blocks,
+near-opaque splats (the 0.99 alpha clamp), and a frame with no binned splat."""
 import numpy as np
 import pytest
 
@@ -48,6 +49,28 @@ def test_equal_and_nearly_equal_depths():
     d[1500:2500] = 4.0 + 1e-13 * rng.integers(0, 50, 1000)  # distinct depths inside one quantisation step
     d[2500:2600] = d[2600:2700]                           # scattered pairs of exact ties
     _check(_with_depths(scene, cam, d), cam, CFGS)
+
+
+def test_tie_runs_of_every_length():
+    # depths drawn from a small set so that equal-key runs of every length 2..40 occur at many offsets
+    # relative to the fix-up's 256-position blocks (runs > 32 take the CTA path)
+    cam = make_camera(192, 128)
+    rng = np.random.default_rng(8)
+    lengths = np.tile(np.arange(2, 41), 14)
+    rng.shuffle(lengths)
+    n = int(lengths.sum())
+    scene = random_scene(rng, n, sh_degree=1, camera=cam, opacity_range=(0.05, 0.6))
+    levels = np.sort(rng.uniform(2.0, 6.0, size=lengths.size))
+    d = np.repeat(levels, lengths)[rng.permutation(n)]
+    _check(_with_depths(scene, cam, d), cam, CFGS[:2])
+
+
+def test_near_opaque_splats():
+    # opacities above 0.99: alpha = min(o exp(-q/2), 0.99) clamps near the centres
+    cam = make_camera(128, 96)
+    rng = np.random.default_rng(13)
+    scene = random_scene(rng, 3000, sh_degree=2, camera=cam, opacity_range=(0.97, 0.9999))
+    _check(scene, cam, CFGS)
 
 
 def test_wide_splats_and_many_tiles():
