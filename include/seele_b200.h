@@ -155,6 +155,14 @@ int seele_render_split(const seele_scene *scene, const int64_t *ranges_dev, int3
                        size_t workspace_bytes, int64_t n_max, int64_t pair_capacity, float *image_dev,
                        int32_t *contrib_dev, int64_t *stats_dev, void *stream, void *raster_stream);
 
+/* frame_skip_bound (render.py:236-256, rasterize.py:325-377): per-pixel
+ * certified error bound of the group-gated engine (group width cfg->group_w)
+ * for the frame LAST RENDERED into this workspace with the same camera and
+ * config.  bound_dev: width * height doubles, row-major.  Stream-ordered after
+ * that render; does not synchronise. */
+int seele_skip_bound(void *workspace, int64_t n_max, int64_t pair_capacity, const seele_camera *cam,
+                     const seele_config *cfg, double *bound_dev, void *stream);
+
 /* select_clusters (residency.py:38-54) on device: nearest 1+m centroids
  * (fp64 squared distance in pose_feature space, compiler.py:113-121; ties
  * toward the smaller id) and the working-set range table for them:

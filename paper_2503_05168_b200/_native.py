@@ -48,6 +48,7 @@ EXPORTED_SYMBOLS = (
     "seele_render_split",
     "seele_select_clusters",
     "seele_plan_export",
+    "seele_skip_bound",
     "seele_profile_enable",
     "seele_profile_read",
     "seele_last_error",
@@ -127,6 +128,8 @@ def load(required: bool = True):
     lib.seele_select_clusters.restype = ctypes.c_int
     lib.seele_plan_export.argtypes = [P, I64, I64, I32, I32, I64, I64, P, P]
     lib.seele_plan_export.restype = ctypes.c_int
+    lib.seele_skip_bound.argtypes = [P, I64, I64, P, P, P, P]
+    lib.seele_skip_bound.restype = ctypes.c_int
     lib.seele_profile_enable.argtypes = [I32]
     lib.seele_profile_enable.restype = ctypes.c_int
     lib.seele_profile_read.argtypes = [P, I32]

@@ -75,6 +75,68 @@ __global__ void __launch_bounds__(256) k_raster_exact(Workspace ws, const uint32
     if (lane == 0) add_counters<W>(stats, k);
 }
 
+// ---------------------------------------------------------------------------
+// Certified per-pixel error bound of the group-gated engine
+// (skipped_contribution_bound, rasterize.py:325-377): the contribution-aware
+// schedule is replayed while tracking, per pixel, the transmittance the
+// reference engine would have had; every splat that blends under the
+// reference schedule but not under the group-gated one adds
+// T_ref * alpha * max(rgb) to the pixel's bound.  fp64, reference operation
+// order; one thread per pixel, the EXACT engine's pixel / group mapping.
+template <int W>
+__global__ void __launch_bounds__(256) k_skip_bound(Workspace ws, const uint32_t *__restrict__ pair_pos, CamK cam,
+                                                    CfgK cfg, double *bound) {
+    __shared__ double s_mx[256], s_my[256], s_a[256], s_b[256], s_c[256], s_o[256];
+    __shared__ float s_cmax[256];
+    const int tile = blockIdx.x;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    int lx, ly;
+    pixel_of<W>(warp, lane, lx, ly);
+    const int x = (tile % cam.tiles_x) * kTile + lx, y = (tile / cam.tiles_x) * kTile + ly;
+    const bool valid = x < cam.width && y < cam.height;
+    const double px = x + 0.5, py = y + 0.5;
+    int leader;
+    unsigned gmask;
+    group_of<W>(lane, leader, gmask);
+    double t_cr = 1.0, t_ref = 1.0, b = 0.0;
+    bool done_cr = !valid, done_ref = !valid;
+    const double th = cfg.alpha_theta, gm = cfg.gamma;
+    const uint2 rg = ws.ranges[tile];
+    for (uint32_t b0 = rg.x; b0 < rg.y; b0 += 256) {
+        if (__syncthreads_count(!(done_cr && done_ref)) == 0) break;  // rasterize.py:350-351
+        const uint32_t i = b0 + tid;
+        if (i < rg.y) {
+            const uint32_t p = pair_pos[i];
+            const double2 m = ws.mean[p];
+            const double4 co = ws.conic_op[p];
+            s_mx[tid] = m.x;
+            s_my[tid] = m.y;
+            s_a[tid] = co.x;
+            s_b[tid] = co.y;
+            s_c[tid] = co.z;
+            s_o[tid] = co.w;
+            const RasterRec &rr = ws.rec[p];
+            s_cmax[tid] = fmaxf(fmaxf(rr.r, rr.g), rr.b);
+        }
+        __syncthreads();
+        const int nb = min(256u, rg.y - b0);
+        for (int j = 0; j < nb; j++) {  // (a done pixel's updates are no-ops: no per-splat early exit needed)
+            const double a = alpha64(px, py, s_mx[j], s_my[j], s_a[j], s_b[j], s_c[j], s_o[j]);
+            const bool live_cr = !done_cr;
+            const bool live_g = (__ballot_sync(0xffffffffu, live_cr) & gmask) != 0u;
+            const double leader_a = __shfl_sync(0xffffffffu, a, leader);  // alpha taken even if the leader is done
+            const bool blend_cr = live_cr && live_g && leader_a >= th && a >= th;
+            const bool blend_ref = !done_ref && a >= th;
+            if (blend_ref && !blend_cr) b = __dadd_rn(b, __dmul_rn(__dmul_rn(t_ref, a), (double)s_cmax[j]));
+            if (blend_cr) t_cr = __dmul_rn(t_cr, __dsub_rn(1.0, a));
+            done_cr = done_cr || t_cr < gm;
+            if (blend_ref) t_ref = __dmul_rn(t_ref, __dsub_rn(1.0, a));
+            done_ref = done_ref || t_ref < gm;
+        }
+    }
+    if (valid) bound[(long long)y * cam.width + x] = b;
+}
+
 template <int W>
 void launch_engine(const Workspace &ws, const uint32_t *pair_pos, const CamK &cam, const CfgK &cfg, float *image,
                    int32_t *contrib, int64_t *stats, cudaStream_t st) {
@@ -89,6 +151,17 @@ void launch_engine(const Workspace &ws, const uint32_t *pair_pos, const CamK &ca
 }
 
 }  // namespace
+
+void launch_skip_bound(int group_w, const Workspace &ws, const uint32_t *pair_pos, const CamK &cam, const CfgK &cfg,
+                       double *bound, cudaStream_t st) {
+    const int n_tiles = cam.tiles_x * cam.tiles_y;
+    switch (group_w) {
+        case 1: k_skip_bound<1><<<n_tiles, 256, 0, st>>>(ws, pair_pos, cam, cfg, bound); break;
+        case 2: k_skip_bound<2><<<n_tiles, 256, 0, st>>>(ws, pair_pos, cam, cfg, bound); break;
+        default: k_skip_bound<4><<<n_tiles, 256, 0, st>>>(ws, pair_pos, cam, cfg, bound); break;
+    }
+    note_launches(1);
+}
 
 void launch_raster(const Workspace &ws, const uint32_t *pair_pos, const CamK &cam, const CfgK &cfg, float *image,
                    int32_t *contrib, int64_t *stats, cudaStream_t st) {

@@ -390,6 +390,26 @@ def plan_frame(scene, cam: CameraPose, cfg: EngineConfig) -> FramePlan:
     return renderer.export_plan(dscene, cam, host)
 
 
+def frame_skip_bound(scene, cam: CameraPose, cfg: EngineConfig, plan: FramePlan | None = None) -> np.ndarray:
+    """Drop-in for render.frame_skip_bound (render.py:236-256): per-pixel
+    certified error bound (H, W) float64 of the group-gated engine with group
+    width ``cfg.group_w`` (skipped_contribution_bound, rasterize.py:325-377),
+    computed on the GPU in fp64 over the GPU's own plan.  ``plan`` is
+    accepted for API compatibility (the GPU plan is bit-equal on the pairs)."""
+    dscene = _as_device_scene(scene)
+    renderer = get_renderer(dscene.device)
+    renderer.render_checked(dscene, cam, cfg)  # plan (pairs, ranges, fp64 splats) into the workspace
+    w, h = renderer.size
+    d = renderer.device
+    bound = torch.empty((h, w), dtype=torch.float64, device=d)
+    camc = _native.camera_struct(cam)
+    cfgc = _native.config_struct(cfg)
+    _native.check(renderer.lib.seele_skip_bound(renderer.workspace.data_ptr(), renderer.n_max, renderer.pair_capacity,
+                                                ctypes.byref(camc), ctypes.byref(cfgc), bound.data_ptr(),
+                                                torch.cuda.current_stream(d).cuda_stream))
+    return bound.cpu().numpy()
+
+
 def check_sorted_depths(depths: np.ndarray) -> None:
     """_check_sorted (rasterize.py:154-156) for caller-supplied tile lists."""
     if len(depths) > 1 and np.any(np.diff(depths) < 0):
