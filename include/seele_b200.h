@@ -155,6 +155,15 @@ int seele_render_split(const seele_scene *scene, const int64_t *ranges_dev, int3
                        size_t workspace_bytes, int64_t n_max, int64_t pair_capacity, float *image_dev,
                        int32_t *contrib_dev, int64_t *stats_dev, void *stream, void *raster_stream);
 
+/* Contribution harvest of one pose (compiler.py:196-231): for the frame LAST
+ * RENDERED into this workspace with the same camera and config, flags[p] = 1
+ * for every assembled position p whose splat is among some pixel's k
+ * strongest blend weights T * alpha (weight > 0; ties toward the smaller id,
+ * ids_dev[p] = gaussian id of position p).  1 <= k <= 32.  flags_dev is not
+ * cleared (poses of a cluster accumulate).  Stream-ordered; no sync. */
+int seele_harvest_topk(void *workspace, int64_t n_max, int64_t pair_capacity, const seele_camera *cam,
+                       const seele_config *cfg, const int64_t *ids_dev, int32_t k, uint8_t *flags_dev, void *stream);
+
 /* frame_skip_bound (render.py:236-256, rasterize.py:325-377): per-pixel
  * certified error bound of the group-gated engine (group width cfg->group_w)
  * for the frame LAST RENDERED into this workspace with the same camera and

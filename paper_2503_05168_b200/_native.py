@@ -49,6 +49,7 @@ EXPORTED_SYMBOLS = (
     "seele_select_clusters",
     "seele_plan_export",
     "seele_skip_bound",
+    "seele_harvest_topk",
     "seele_profile_enable",
     "seele_profile_read",
     "seele_last_error",
@@ -130,6 +131,8 @@ def load(required: bool = True):
     lib.seele_plan_export.restype = ctypes.c_int
     lib.seele_skip_bound.argtypes = [P, I64, I64, P, P, P, P]
     lib.seele_skip_bound.restype = ctypes.c_int
+    lib.seele_harvest_topk.argtypes = [P, I64, I64, P, P, P, I32, P, P]
+    lib.seele_harvest_topk.restype = ctypes.c_int
     lib.seele_profile_enable.argtypes = [I32]
     lib.seele_profile_enable.restype = ctypes.c_int
     lib.seele_profile_read.argtypes = [P, I32]

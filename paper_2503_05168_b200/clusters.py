@@ -8,12 +8,15 @@ shared / exclusive / discarded partition of the splats.
   ``partition`` restate pkg/src/seele/compiler.py:105-193, 234-261 with the
   same numpy call sequence, so a given seed yields the reference's centroids
   (pinned by tests/golden/clusters_orbit.npz).
-* The reference's per-pixel top-k contributor harvest (compiler.py:196-231)
-  needs a dense (P x H*W) matrix per pose and cannot run at benchmark scale;
-  for the synthetic configs the candidate set of a cluster is every splat
+* ``harvest_top_contributors`` / ``compile_table``: the reference's per-pixel
+  top-k contributor harvest (compiler.py:196-231, 264-311) on the GPU: the
+  EXACT engine's schedule keeps each pixel's k strongest blend weights in
+  shared memory (csrc/raster.cu k_harvest) instead of the reference's dense
+  (P x H*W) matrix per pose, so it runs at benchmark scale.
+* ``build_cluster_table``: the cheaper visibility harvest used for the
+  synthetic benchmark configs -- the candidate set of a cluster is every splat
   whose centre projects inside the image in front of the near plane for at
-  least one member pose.  That projection runs on the
-  GPU through torch (offline, not the render path).
+  least one member pose, projected through torch.
 """
 from __future__ import annotations
 
@@ -177,3 +180,60 @@ def build_cluster_table(scene: SceneArrays, poses, n_clusters: int = 24, neighbo
                         centroids=np.stack([s.centroid for s in specs]), beta=beta, neighbors=neighbors,
                         position_mean=np.asarray(norm[0]), position_scale=float(norm[1]), pose_assignments=assign,
                         share_threshold=share_threshold)
+
+
+def harvest_top_contributors(cluster, scene, k: int, cfg=None) -> np.ndarray:
+    """compiler.py:216-231 on the GPU: ids of every splat that makes some
+    pixel's top-k (blend weight T * alpha > 0, ties toward the smaller id) for
+    some member pose of ``cluster`` (anything with ``member_poses``)."""
+    import ctypes
+
+    import torch
+
+    from . import _native
+    from .render import EngineConfig, _as_device_scene, get_renderer
+
+    if k < 1:
+        raise InvalidArgumentError(f"k must be >= 1, got {k}")
+    if k > 32:
+        raise InvalidArgumentError(f"the GPU harvest keeps at most 32 contributors per pixel, got k={k}")
+    if not cluster.member_poses:
+        raise InvalidArgumentError("cannot harvest a cluster with no member poses")
+    cfg = cfg or EngineConfig()
+    dscene = _as_device_scene(scene)
+    renderer = get_renderer(dscene.device)
+    n = dscene.n
+    ids_host = np.asarray(dscene.host_ids[:n], dtype=np.int64)
+    ids = torch.as_tensor(ids_host, device=dscene.device)
+    flags = torch.zeros(max(n, 1), dtype=torch.uint8, device=dscene.device)
+    cfgc = _native.config_struct(cfg)
+    for pose in cluster.member_poses:
+        renderer.render_checked(dscene, pose, cfg)  # this pose's plan into the workspace
+        camc = _native.camera_struct(pose)
+        _native.check(renderer.lib.seele_harvest_topk(
+            renderer.workspace.data_ptr(), renderer.n_max, renderer.pair_capacity, ctypes.byref(camc),
+            ctypes.byref(cfgc), ids.data_ptr(), int(k), flags.data_ptr(),
+            torch.cuda.current_stream(dscene.device).cuda_stream))
+    picked = flags.cpu().numpy()[:n].astype(bool)
+    return np.unique(ids_host[picked])
+
+
+def compile_table(scene: SceneArrays, poses, n_clusters: int = 24, neighbors: int = 4, beta: float = 1.0,
+                  seed: int = 0, share_threshold: int = 2, top_k: int = 32, cfg=None) -> ClusterTable:
+    """compile_scene (compiler.py:264-311, without extra pose samples) with the
+    GPU contribution harvest: cluster the poses, harvest each cluster's top-k
+    contributors, partition."""
+    from .render import _as_device_scene
+
+    norm = compute_pose_normalization(poses)
+    specs = cluster_poses(poses, n_clusters, beta, seed, normalization=norm)
+    dscene = _as_device_scene(scene)  # uploaded once for every cluster's harvest
+    sets = [harvest_top_contributors(s, dscene, top_k, cfg) for s in specs]
+    shared, exclusive, discarded = partition(sets, dscene.host_ids[:dscene.n], share_threshold)
+    assign = np.zeros(len(poses), dtype=np.int64)
+    for c, s in enumerate(specs):
+        assign[s.member_indices] = c
+    return ClusterTable(shared_ids=shared, exclusive_ids=exclusive, discarded_ids=discarded,
+                        centroids=np.stack([s.centroid for s in specs]), beta=beta, neighbors=neighbors,
+                        position_mean=np.asarray(norm[0]), position_scale=float(norm[1]), pose_assignments=assign,
+                        share_threshold=share_threshold, top_k=top_k)

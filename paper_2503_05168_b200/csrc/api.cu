@@ -390,6 +390,28 @@ int seele_plan_export(void *workspace, int64_t n_max, int64_t pair_capacity, int
     return SEELE_OK;
 }
 
+int seele_harvest_topk(void *workspace, int64_t n_max, int64_t pair_capacity, const seele_camera *cam,
+                       const seele_config *cfg, const int64_t *ids_dev, int32_t k, uint8_t *flags_dev, void *stream) {
+    g_err[0] = 0;
+    int rc;
+    if ((rc = check_camera(cam)) != SEELE_OK) return rc;
+    if ((rc = check_config(cfg)) != SEELE_OK) return rc;
+    if (!workspace || !ids_dev || !flags_dev) return fail(SEELE_ERR_INVALID_ARGUMENT, "null argument");
+    if (k < 1 || k > 32) return fail(SEELE_ERR_INVALID_ARGUMENT, "k must lie in [1, 32], got %d", k);
+    const Workspace ws = carve_workspace(workspace, n_max, pair_capacity, cam->width, cam->height);
+    const CamK ck = make_cam(*cam);
+    CfgK cf{};
+    cf.engine = cfg->engine;
+    cf.group_w = cfg->group_w;
+    cf.alpha_theta = cfg->alpha_theta;
+    cf.gamma = cfg->gamma_threshold;
+    launch_harvest(cfg->engine == 0 ? 0 : cfg->group_w, ws, ws.pfinal, ck, cf, ids_dev, k, flags_dev,
+                   static_cast<cudaStream_t>(stream));
+    cudaError_t e;
+    if ((e = cudaGetLastError()) != cudaSuccess) return cuda_fail(e, "seele_harvest_topk");
+    return SEELE_OK;
+}
+
 int seele_skip_bound(void *workspace, int64_t n_max, int64_t pair_capacity, const seele_camera *cam,
                      const seele_config *cfg, double *bound_dev, void *stream) {
     g_err[0] = 0;

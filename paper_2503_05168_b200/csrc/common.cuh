@@ -148,6 +148,8 @@ void launch_raster(const Workspace &ws, const uint32_t *pair_pos, const CamK &ca
                    const CfgK &cfg, float *image, int32_t *contrib, int64_t *stats,
                    cudaStream_t st);
 // FAST engine tile kernel (raster_fast.cu); W = 0 (ref) or CR group width.
+void launch_harvest(int engine_w, const Workspace &ws, const uint32_t *pair_pos, const CamK &cam, const CfgK &cfg,
+                    const int64_t *ids, int k, uint8_t *flags, cudaStream_t st);
 void launch_skip_bound(int group_w, const Workspace &ws, const uint32_t *pair_pos, const CamK &cam, const CfgK &cfg,
                        double *bound, cudaStream_t st);
 void launch_raster_fast(int W, const Workspace &ws, const uint32_t *pair_pos, const CamK &cam,

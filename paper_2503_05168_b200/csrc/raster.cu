@@ -137,6 +137,122 @@ __global__ void __launch_bounds__(256) k_skip_bound(Workspace ws, const uint32_t
     if (valid) bound[(long long)y * cam.width + x] = b;
 }
 
+// ---------------------------------------------------------------------------
+// Contribution harvest (compiler.py:196-231, top_contributors_per_pixel): the
+// EXACT engine's schedule (reference or contribution-aware, step64 semantics),
+// keeping per pixel the k strongest blend weights T * alpha (ties toward the
+// smaller gaussian id, like the reference's stable id-ascending sort) in
+// shared memory; every splat in some pixel's top-k with weight > 0 is flagged
+// by its assembled position.
+constexpr int kHarvestMax = 32;
+
+template <int W>
+__global__ void __launch_bounds__(256) k_harvest(Workspace ws, const uint32_t *__restrict__ pair_pos, CamK cam, CfgK cfg,
+                                                 const int64_t *__restrict__ ids, int k, uint8_t *flags) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    double *s_w = reinterpret_cast<double *>(smem);                   // [kHarvestMax][256]
+    uint32_t *s_p = reinterpret_cast<uint32_t *>(s_w + kHarvestMax * 256);  // [kHarvestMax][256] positions
+    __shared__ double s_mx[256], s_my[256], s_a[256], s_b[256], s_c[256], s_o[256];
+    __shared__ uint32_t s_pp[256];
+    const int tile = blockIdx.x;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    int lx, ly;
+    pixel_of<W>(warp, lane, lx, ly);
+    const int x = (tile % cam.tiles_x) * kTile + lx, y = (tile / cam.tiles_x) * kTile + ly;
+    const bool valid = x < cam.width && y < cam.height;
+    const double px = x + 0.5, py = y + 0.5;
+    int leader;
+    unsigned gmask;
+    group_of<W>(lane, leader, gmask);
+    const bool is_leader = lane == leader;
+    double T = 1.0;
+    bool done = !valid;
+    int cnt = 0, mslot = 0;
+    double mw = 0.0;
+    int64_t mid = 0;
+    const double th = cfg.alpha_theta, gm = cfg.gamma;
+    const uint2 rg = ws.ranges[tile];
+    for (uint32_t b0 = rg.x; b0 < rg.y; b0 += 256) {
+        if (__syncthreads_count(!done) == 0) break;
+        const uint32_t i = b0 + tid;
+        if (i < rg.y) {
+            const uint32_t p = pair_pos[i];
+            const double2 m = ws.mean[p];
+            const double4 co = ws.conic_op[p];
+            s_mx[tid] = m.x;
+            s_my[tid] = m.y;
+            s_a[tid] = co.x;
+            s_b[tid] = co.y;
+            s_c[tid] = co.z;
+            s_o[tid] = co.w;
+            s_pp[tid] = p;
+        }
+        __syncthreads();
+        const int nb = min(256u, rg.y - b0);
+        for (int j = 0; j < nb; j++) {
+            const bool live = !done;
+            const unsigned lb = __ballot_sync(0xffffffffu, live);
+            if (lb == 0u) break;  // (warp-uniform: the model-warp stops, rasterize.py:203 per warp is equivalent here)
+            double al = 0.0;
+            bool blend = false;
+            if (W == 0) {
+                if (live) {
+                    al = alpha64(px, py, s_mx[j], s_my[j], s_a[j], s_b[j], s_c[j], s_o[j]);
+                    blend = al >= th;
+                }
+            } else {  // step64's contribution-aware gate (rasterize.py:249-322)
+                const bool glive = (lb & gmask) != 0u;
+                double la = 0.0;
+                bool lpass = false;
+                if (is_leader && glive) {
+                    la = alpha64(px, py, s_mx[j], s_my[j], s_a[j], s_b[j], s_c[j], s_o[j]);
+                    lpass = la >= th;
+                }
+                const unsigned pb = __ballot_sync(0xffffffffu, lpass);
+                if (live && ((pb >> leader) & 1u)) {
+                    al = is_leader ? la : alpha64(px, py, s_mx[j], s_my[j], s_a[j], s_b[j], s_c[j], s_o[j]);
+                    blend = al >= th;
+                }
+            }
+            if (blend) {
+                const double w = __dmul_rn(T, al);  // the contribution row (rasterize.py:176-177)
+                const uint32_t p = s_pp[j];
+                const int64_t id = ids[p];
+                if (cnt < k) {
+                    s_w[cnt * 256 + tid] = w;
+                    s_p[cnt * 256 + tid] = p;
+                    cnt++;
+                    if (cnt == k) {  // full: locate the weakest entry
+                        mslot = 0;
+                        mw = s_w[tid];
+                        mid = ids[s_p[tid]];
+                        for (int q = 1; q < k; q++) {
+                            const double wq = s_w[q * 256 + tid];
+                            const int64_t iq = ids[s_p[q * 256 + tid]];
+                            if (wq < mw || (wq == mw && iq > mid)) { mslot = q; mw = wq; mid = iq; }
+                        }
+                    }
+                } else if (w > mw || (w == mw && id < mid)) {
+                    s_w[mslot * 256 + tid] = w;
+                    s_p[mslot * 256 + tid] = p;
+                    mslot = 0;
+                    mw = s_w[tid];
+                    mid = ids[s_p[tid]];
+                    for (int q = 1; q < k; q++) {
+                        const double wq = s_w[q * 256 + tid];
+                        const int64_t iq = ids[s_p[q * 256 + tid]];
+                        if (wq < mw || (wq == mw && iq > mid)) { mslot = q; mw = wq; mid = iq; }
+                    }
+                }
+                T = __dmul_rn(T, __dsub_rn(1.0, al));
+                if (T < gm) done = true;
+            }
+        }
+    }
+    for (int q = 0; q < cnt; q++)
+        if (s_w[q * 256 + tid] > 0.0) flags[s_p[q * 256 + tid]] = 1u;
+}
+
 template <int W>
 void launch_engine(const Workspace &ws, const uint32_t *pair_pos, const CamK &cam, const CfgK &cfg, float *image,
                    int32_t *contrib, int64_t *stats, cudaStream_t st) {
@@ -159,6 +275,27 @@ void launch_skip_bound(int group_w, const Workspace &ws, const uint32_t *pair_po
         case 1: k_skip_bound<1><<<n_tiles, 256, 0, st>>>(ws, pair_pos, cam, cfg, bound); break;
         case 2: k_skip_bound<2><<<n_tiles, 256, 0, st>>>(ws, pair_pos, cam, cfg, bound); break;
         default: k_skip_bound<4><<<n_tiles, 256, 0, st>>>(ws, pair_pos, cam, cfg, bound); break;
+    }
+    note_launches(1);
+}
+
+void launch_harvest(int engine_w, const Workspace &ws, const uint32_t *pair_pos, const CamK &cam, const CfgK &cfg,
+                    const int64_t *ids, int k, uint8_t *flags, cudaStream_t st) {
+    const int n_tiles = cam.tiles_x * cam.tiles_y;
+    const size_t smem = (size_t)kHarvestMax * 256 * (sizeof(double) + sizeof(uint32_t));
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(k_harvest<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaFuncSetAttribute(k_harvest<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaFuncSetAttribute(k_harvest<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaFuncSetAttribute(k_harvest<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        attr = true;
+    }
+    switch (engine_w) {
+        case 0: k_harvest<0><<<n_tiles, 256, smem, st>>>(ws, pair_pos, cam, cfg, ids, k, flags); break;
+        case 1: k_harvest<1><<<n_tiles, 256, smem, st>>>(ws, pair_pos, cam, cfg, ids, k, flags); break;
+        case 2: k_harvest<2><<<n_tiles, 256, smem, st>>>(ws, pair_pos, cam, cfg, ids, k, flags); break;
+        default: k_harvest<4><<<n_tiles, 256, smem, st>>>(ws, pair_pos, cam, cfg, ids, k, flags); break;
     }
     note_launches(1);
 }
