@@ -860,17 +860,26 @@ __device__ __forceinline__ bool col_tile(const Workspace &ws, int tiles_x, int t
 #pragma unroll 1
         for (int r = 0; r < IPT; r++) {
             // columns of this entry inside the current group
-            const uint32_t a = max(x0[r], ca), b = min(x1[r] + 1u, cb);  // [a, b)
-            for (uint32_t v = a; v < b; v++) atomicOr(&S.mask[warp][v], 1u << lane);
+            const uint32_t a = max(x0[r], ca), b = min(x1[r] + 1u, cb);  // [a, b), at most kSegW columns
+            // (fixed-trip predicated loops: entries cover <= kSegW columns)
+#pragma unroll
+            for (uint32_t c = 0; c < kSegW; c++)
+                if (a + c < b) atomicOr(&S.mask[warp][a + c], 1u << lane);
             __syncwarp();
-            for (uint32_t v = a; v < b; v++) {
+#pragma unroll
+            for (uint32_t c = 0; c < kSegW; c++) {
+                if (a + c >= b) continue;
+                const uint32_t v = a + c;
                 const uint32_t m = S.mask[warp][v];
                 const uint32_t slot = (uint32_t)S.cnt[warp][v] + __popc(m & lt) - sbase;
                 S.stage[slot] = pv[r];
                 S.stx[slot] = (uint8_t)v;
             }
             __syncwarp();
-            for (uint32_t v = a; v < b; v++) {  // the highest covering lane advances the column
+#pragma unroll
+            for (uint32_t c = 0; c < kSegW; c++) {  // the highest covering lane advances the column
+                if (a + c >= b) continue;
+                const uint32_t v = a + c;
                 const uint32_t m = S.mask[warp][v];
                 if ((m >> lane) == 1u) {
                     S.cnt[warp][v] += __popc(m);
