@@ -163,6 +163,7 @@ __global__ void __launch_bounds__(NT, SEELE_DEPTH_MINB) k_depth_pass(Workspace w
     uint32_t *sval = skey + DTILE;
     uint32_t *srect = sval + DTILE;
     __shared__ uint32_t s_base[RADIX];
+    for (;;) {  // persistent when the grid is smaller than the tile count (tickets in order)
 #ifdef SEELE_SORT_TRACE
     const unsigned long long t_enter = gtime();
 #endif
@@ -252,6 +253,8 @@ __global__ void __launch_bounds__(NT, SEELE_DEPTH_MINB) k_depth_pass(Workspace w
     __syncthreads();
     TRACE(pass, t, 4)
 #endif
+    __syncthreads();  // the staging arrays are reused by the next ticket
+    }
 }
 
 __device__ __forceinline__ short4 unpack_rect(uint32_t v) {
@@ -953,7 +956,11 @@ void launch_depth_sort(const Workspace &ws, long long n_max, int64_t *stats, cud
     k_depth_hist<<<hist_grid > 0 ? hist_grid : 1, 256, 0, st>>>(ws);
     const size_t smem = 16 + sizeof(RankSmem) + 3 * sizeof(uint32_t) * DTILE;
     set_smem(k_depth_pass, smem);
-    const int grid = (int)ceil_div(n_max, DTILE);
+#ifndef SEELE_DEPTH_CTAS_PER_SM
+#define SEELE_DEPTH_CTAS_PER_SM 0  // 0: one CTA per tile (not persistent)
+#endif
+    int grid = (int)ceil_div(n_max, DTILE);
+    if (SEELE_DEPTH_CTAS_PER_SM > 0) grid = std::min(grid, SEELE_DEPTH_CTAS_PER_SM * 148);
     for (int p = 0; p < kDepthPasses; p++) k_depth_pass<<<grid, NT, smem, st>>>(ws, p);
     const int fix_grid = (int)ceil_div(n_max, kFixOwn);
     k_depth_fixup<<<fix_grid > 0 ? fix_grid : 1, kFixThreads, 0, st>>>(ws, stats);
@@ -975,16 +982,26 @@ void launch_binning(const Workspace &ws, long long n_max, long long cap, const C
     const size_t scan_smem = use_smem ? diff_bytes : 0;
     set_smem(k_pair_scan, 160 * 1024);
 #ifndef SEELE_SCAN_PER_SM2
-#define SEELE_SCAN_PER_SM2 4
+#define SEELE_SCAN_PER_SM2 2  // (half-SM units: one CTA per SM)
 #endif
     const int scan_grid = (int)std::min<long long>(ceil_div(n_max, TILE), SEELE_SCAN_PER_SM2 * sms / 2);
     k_pair_scan<<<scan_grid > 0 ? scan_grid : 1, NT, scan_smem, st>>>(ws, cam.tiles_x, cam.tiles_y, cap, use_smem,
                                                                       stats);
     set_smem(k_row_pass, sizeof(RowSmem));
-    const int persist = 2 * sms;  // two CTAs per SM (launch bounds)
+#ifndef SEELE_BIN_CTAS_PER_SM
+#define SEELE_BIN_CTAS_PER_SM 1  // one per SM: room for another frame's raster CTAs (pipelined 983 -> 994 FPS)
+#endif
+#ifndef SEELE_ROW_CTAS_PER_SM
+#define SEELE_ROW_CTAS_PER_SM SEELE_BIN_CTAS_PER_SM
+#endif
+#ifndef SEELE_COL_CTAS_PER_SM
+#define SEELE_COL_CTAS_PER_SM SEELE_BIN_CTAS_PER_SM
+#endif
+    const int persist = SEELE_ROW_CTAS_PER_SM * sms;  // resident CTAs (launch bounds allow two per SM)
     k_row_pass<<<(int)std::min<long long>(ceil_div(cap, TILE), persist), NT, sizeof(RowSmem), st>>>(ws, stats);
     set_smem(k_col_pass, sizeof(ColSmem));
-    k_col_pass<<<(int)std::min<long long>(ceil_div(cap, TILE) + cam.tiles_y, persist), NT, sizeof(ColSmem), st>>>(
+    const int persist_col = SEELE_COL_CTAS_PER_SM * sms;
+    k_col_pass<<<(int)std::min<long long>(ceil_div(cap, TILE) + cam.tiles_y, persist_col), NT, sizeof(ColSmem), st>>>(
         ws, cam.tiles_x, cam.tiles_y);
     note_launches(3);
 }
