@@ -997,10 +997,10 @@ void launch_binning(const Workspace &ws, long long n_max, long long cap, const C
 #ifndef SEELE_COL_CTAS_PER_SM
 #define SEELE_COL_CTAS_PER_SM SEELE_BIN_CTAS_PER_SM
 #endif
-    const int persist = SEELE_ROW_CTAS_PER_SM * sms;  // resident CTAs (launch bounds allow two per SM)
+    const int persist = (int)(SEELE_ROW_CTAS_PER_SM * sms);  // resident CTAs (launch bounds allow two per SM)
     k_row_pass<<<(int)std::min<long long>(ceil_div(cap, TILE), persist), NT, sizeof(RowSmem), st>>>(ws, stats);
     set_smem(k_col_pass, sizeof(ColSmem));
-    const int persist_col = SEELE_COL_CTAS_PER_SM * sms;
+    const int persist_col = (int)(SEELE_COL_CTAS_PER_SM * sms);
     k_col_pass<<<(int)std::min<long long>(ceil_div(cap, TILE) + cam.tiles_y, persist_col), NT, sizeof(ColSmem), st>>>(
         ws, cam.tiles_x, cam.tiles_y);
     note_launches(3);

@@ -466,10 +466,12 @@ __global__ void __launch_bounds__(64, SEELE_RASTER_MINB) k_raster_quad(Workspace
         image[3 * pix + 2] = fmaf(Ts, (float)cfg.bg[2], lane_of(C[r][2], c));
         if (contrib) contrib[pix] = (int32_t)slot(cnt, s);
     }
-    if (i == 0) {
-        Counters k{c_alpha, c_blend, c_leader};
-        add_counters<W>(stats, k);
-    }
+    // the four model-warps' counters summed in the warp: one set of atomics per warp (the stats words are
+    // shared by every CTA)
+    const uint32_t ca = i == 0 ? c_alpha : 0u, cb = i == 0 ? c_blend : 0u, cl = i == 0 ? c_leader : 0u;
+    Counters k{__reduce_add_sync(0xffffffffu, ca), __reduce_add_sync(0xffffffffu, cb),
+               __reduce_add_sync(0xffffffffu, cl)};
+    if (lane == 0) add_counters<W>(stats, k);
 }
 }  // namespace
 

@@ -40,7 +40,8 @@ class FramePipeline:
     """Renders frames of a resident (clustered) scene ``depth`` at a time."""
 
     def __init__(self, rr: ResidentRenderer, width: int, height: int, *, depth: int = 2,
-                 pair_capacity: int | None = None, contrib: bool = True, split: bool = False):
+                 pair_capacity: int | None = None, contrib: bool = True, split: bool = False,
+                 raster_priority: bool = False):
         if depth < 1:
             raise ValueError("depth must be >= 1")
         self.rr = rr
@@ -51,10 +52,11 @@ class FramePipeline:
             r = FrameRenderer(self.device)
             r.reserve(rr.n_max, width, height, pair_capacity=pair_capacity)
             least, greatest = torch.cuda.Stream.priority_range()  # lower number = higher priority
+            plan_pri, raster_pri = (least, greatest) if raster_priority else (greatest, least)
             self.slots.append(_Slot(
                 renderer=r,
-                stream=torch.cuda.Stream(self.device, priority=greatest if split else 0),
-                raster_stream=torch.cuda.Stream(self.device, priority=least if split else 0),
+                stream=torch.cuda.Stream(self.device, priority=plan_pri if split else 0),
+                raster_stream=torch.cuda.Stream(self.device, priority=raster_pri if split else 0),
                 free=torch.cuda.Event(),
                 sel_ids=torch.empty(rr.m + 1, dtype=torch.int32, device=self.device),
                 ranges=torch.empty((rr.m + 2, 2), dtype=torch.int64, device=self.device),

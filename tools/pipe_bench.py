@@ -25,8 +25,8 @@ for f in range(0, 120, 3):
 del probe
 cap = int(need * 1.05) + 4096
 main = torch.cuda.current_stream(dev)
-for depth, split in ((1, False), (3, False), (2, True), (3, True), (4, True)):
-    pipe = FramePipeline(rr, args.width, args.height, depth=depth, pair_capacity=cap, split=split)
+for depth, split, rp in ((3, False, False), (3, True, True), (2, True, True), (4, True, True), (3, True, False)):
+    pipe = FramePipeline(rr, args.width, args.height, depth=depth, pair_capacity=cap, split=split, raster_priority=rp)
     for k in range(6):
         pipe.submit(poses[k], cfg)
     pipe.join(main)
@@ -42,6 +42,6 @@ for depth, split in ((1, False), (3, False), (2, True), (3, True), (4, True)):
     torch.cuda.synchronize()
     ms = ev0.elapsed_time(ev1)
     ov = max(int(s.stats[_native.STAT_OVERFLOW].item()) for s in pipe.slots)
-    print(f"depth {depth} split {split}: {K / (ms / 1e3):.1f} frames/s  ({ms / K:.3f} ms/frame) overflow={ov}", flush=True)
+    print(f"depth {depth} split {split} raster-first {rp}: {K / (ms / 1e3):.1f} frames/s  ({ms / K:.3f} ms/frame) overflow={ov}", flush=True)
     del pipe
     torch.cuda.empty_cache()
