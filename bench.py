@@ -57,6 +57,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=60)
     ap.add_argument("--depth", type=int, default=3, help="frames in flight (streams)")
+    ap.add_argument("--raster-first", action="store_true",
+                    help="raster on a high-priority stream, the plan stages of the frames in flight below it")
     return ap.parse_args()
 
 
@@ -291,7 +293,8 @@ def run_ours(args):
         return ev0.elapsed_time(ev1)
 
     serial_ms = timed_serial()
-    pipe = FramePipeline(rr, args.width, args.height, depth=args.depth, pair_capacity=cap)
+    pipe = FramePipeline(rr, args.width, args.height, depth=args.depth, pair_capacity=cap,
+                         split=args.raster_first, raster_priority=args.raster_first)
     clocks = ClockSampler(device) if rank == 0 else None
     if clocks:
         clocks.start()
