@@ -948,6 +948,17 @@ void launch_frame_begin(const Workspace &ws, const CamK &cam, int64_t *stats, cu
     note_launches(1);
 }
 
+static int sm_count_cached() {
+    static int sms = 0;
+    if (!sms) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        if (sms <= 0) sms = 148;
+    }
+    return sms;
+}
+
 void launch_depth_sort(const Workspace &ws, long long n_max, int64_t *stats, cudaStream_t st) {
 #ifndef SEELE_HIST_PER_SM
 #define SEELE_HIST_PER_SM 2
@@ -957,10 +968,10 @@ void launch_depth_sort(const Workspace &ws, long long n_max, int64_t *stats, cud
     const size_t smem = 16 + sizeof(RankSmem) + 3 * sizeof(uint32_t) * DTILE;
     set_smem(k_depth_pass, smem);
 #ifndef SEELE_DEPTH_CTAS_PER_SM
-#define SEELE_DEPTH_CTAS_PER_SM 0  // 0: one CTA per tile (not persistent)
+#define SEELE_DEPTH_CTAS_PER_SM 2  // persistent at the resident CTAs (0: one CTA per tile)
 #endif
     int grid = (int)ceil_div(n_max, DTILE);
-    if (SEELE_DEPTH_CTAS_PER_SM > 0) grid = std::min(grid, SEELE_DEPTH_CTAS_PER_SM * 148);
+    if (SEELE_DEPTH_CTAS_PER_SM > 0) grid = std::min(grid, SEELE_DEPTH_CTAS_PER_SM * sm_count_cached());
     for (int p = 0; p < kDepthPasses; p++) k_depth_pass<<<grid, NT, smem, st>>>(ws, p);
     const int fix_grid = (int)ceil_div(n_max, kFixOwn);
     k_depth_fixup<<<fix_grid > 0 ? fix_grid : 1, kFixThreads, 0, st>>>(ws, stats);
@@ -970,13 +981,7 @@ void launch_depth_sort(const Workspace &ws, long long n_max, int64_t *stats, cud
 
 void launch_binning(const Workspace &ws, long long n_max, long long cap, const CamK &cam, int64_t *stats,
                     cudaStream_t st) {
-    static int sms = 0;
-    if (!sms) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        if (sms <= 0) sms = 148;
-    }
+    const int sms = sm_count_cached();
     const size_t diff_bytes = sizeof(int32_t) * (cam.tiles_x + 1) * (cam.tiles_y + 1);
     const int use_smem = diff_bytes <= 160 * 1024;
     const size_t scan_smem = use_smem ? diff_bytes : 0;
