@@ -23,12 +23,6 @@ __device__ __forceinline__ float ex2_approx(float x) {
     return y;
 }
 
-__device__ __forceinline__ float rcp_approx(float x) {
-    float y;
-    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
-    return y;
-}
-
 // Pixel owned by (warp, lane) for engine width W (0 = ref).
 template <int W>
 __device__ __forceinline__ void pixel_of(int warp, int lane, int &lx, int &ly) {

@@ -24,18 +24,25 @@
 //
 // Exactness (same discrete result as the fp64 reference), everything in fp32:
 //  * alpha test: q' = log2(e) q / 2 evaluated in fp32 (Cholesky form, hi/lo
-//    tile-relative mean) has |q'32 - q'| <= e0q + e1q q' (derivation at
-//    write_raster_record); q'32 < q_lo' passes,
-//    q'32 > q_hi' fails, in between the pixel is re-decided with the
-//    reference's fp64 formula (alpha64).
-//  * transmittance: alpha32 = min(o 2^-q'32, 0.99) with relative error
-//    <= e0 + e1 q'; 1 - alpha for alpha > 0.5 is rebuilt as (1 - o) +
-//    o (1 - 2^-q') so it keeps ~5e-7 relative accuracy.  Each pixel carries T
-//    in fp32 and an absolute bound D >= |T32 - T|, D' = D (1 - alpha) +
-//    T (ef + 2^-24).  T < gamma is decided in fp32 unless T lies within D of
-//    gamma; then the pixel's transmittance is recomputed exactly in fp64 over
-//    the tile list so far (exact_transmittance) and the decision is the
+//    mean) has |q'32 - q'| <= e0q + e1q q' (derivation at
+//    write_raster_record), giving the bracket [q_lo, q_up): q'32 < q_lo
+//    passes, q'32 >= q_up fails, in between the pixel is re-decided with the
+//    reference's fp64 formula (alpha64).  The decisions are sign bits of
+//    q'32 - q_lo and q'32 - q_up (exact for float subtraction).
+//  * transmittance: alpha32 = min(o 2^-q'32, 0.99) has relative error
+//    <= e0 + e1 q'; 1 - alpha32 is exact for alpha >= 0.5 and within 2^-25
+//    otherwise.  Each pixel carries T in fp32 and a bound D >= |T32 - T|,
+//    D' = D (1 - alpha) + T (alpha (e0 + e1 q') + 1e-7), products rounded
+//    upward.  A clear sign of T32 - (D + gamma) (rounded up) proves T >=
+//    gamma; otherwise T + D < gamma proves the pixel done, and in between
+//    its transmittance is recomputed exactly in fp64 over the tile list so
+//    far (exact_transmittance, warp-cooperative) and the decision is the
 //    reference's.
+//
+// Data flow per warp: batches of 32 records (64 B each) are staged in shared
+// memory by cp.async one batch ahead; a batch's relevance to the warp's
+// region is one ballot; the blend of a step is branch-free packed math with
+// 0 / 1 factors (sign-bit masks & liveness & the group leader's verdict).
 #include "raster_common.cuh"
 
 namespace seele {
@@ -78,8 +85,6 @@ __device__ __forceinline__ float sqrt_approx(float x) {
     asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
     return y;
 }
-// all-ones if the sign bit of x is set, else 0
-__device__ __forceinline__ uint32_t sign_mask(float x) { return (uint32_t)((int)__float_as_uint(x) >> 31); }
 
 // The two pixels of a quad row are one float2 (.x = left, .y = right) so the
 // per-pixel math runs as packed fp32x2 instructions (FFMA2 / FMUL2 / FADD2,
