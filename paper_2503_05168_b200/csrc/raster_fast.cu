@@ -298,7 +298,6 @@ __global__ void __launch_bounds__(64, SEELE_RASTER_MINB) k_raster_quad(Workspace
         while (mlo) {
             const int j = __ffs(mlo) - 1;  // next relevant splat
             mlo &= mlo - 1u;
-            const uint32_t step = b0 + (uint32_t)j - rg.x + 1u;  // tile splats processed including this one
             const Staged &sg = s_g[j];
             float2 q[2], al[2], d[2], E[2];
             quad_q(sg, lxp, lyp, q);
@@ -387,7 +386,7 @@ __global__ void __launch_bounds__(64, SEELE_RASTER_MINB) k_raster_quad(Workspace
                         slot(Lf, s) = 0.0f;
                         s_T[tid][s] = slot(T, s);
                         slot(T, s) = 1e30f;
-                        di[s] = step;
+                        di[s] = b0 + (uint32_t)j - rg.x + 1u;  // its death step: tile splats processed
                         nlive--;
                         n_skip -= (uint32_t)__popc(skipped >> j >> 1);
                     } else {
@@ -418,7 +417,7 @@ __global__ void __launch_bounds__(64, SEELE_RASTER_MINB) k_raster_quad(Workspace
                                 slot(Lf, ss) = 0.0f;
                                 s_T[tid][ss] = slot(T, ss);
                                 slot(T, ss) = 1e30f;
-                                di[ss] = step;
+                                di[ss] = b0 + (uint32_t)j - rg.x + 1u;
                                 nlive--;
                                 n_skip -= (uint32_t)__popc(skipped >> j >> 1);
                             }
