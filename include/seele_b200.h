@@ -155,6 +155,17 @@ int seele_render_split(const seele_scene *scene, const int64_t *ranges_dev, int3
                        size_t workspace_bytes, int64_t n_max, int64_t pair_capacity, float *image_dev,
                        int32_t *contrib_dev, int64_t *stats_dev, void *stream, void *raster_stream);
 
+/* Image metrics on the device (metrics.py:44-112) of two (H, W, 3) fp64
+ * images a_dev, b_dev: PSNR in dB (+inf when equal) and mean SSIM over the
+ * BT.601 luminance (11x11 Gaussian window, sigma 1.5, valid positions).  The
+ * result is one double at out_dev; scratch_dev holds
+ * seele_metrics_scratch_doubles(width, height) doubles.  Stream-ordered. */
+int seele_psnr(const double *a_dev, const double *b_dev, int64_t n, double *scratch_dev, double *out_dev,
+               void *stream);
+int seele_ssim(const double *a_dev, const double *b_dev, int32_t width, int32_t height, double *scratch_dev,
+               double *out_dev, void *stream);
+int64_t seele_metrics_scratch_doubles(int32_t width, int32_t height);
+
 /* Contribution harvest of one pose (compiler.py:196-231): for the frame LAST
  * RENDERED into this workspace with the same camera and config, flags[p] = 1
  * for every assembled position p whose splat is among some pixel's k

@@ -50,6 +50,9 @@ EXPORTED_SYMBOLS = (
     "seele_plan_export",
     "seele_skip_bound",
     "seele_harvest_topk",
+    "seele_psnr",
+    "seele_ssim",
+    "seele_metrics_scratch_doubles",
     "seele_profile_enable",
     "seele_profile_read",
     "seele_last_error",
@@ -133,6 +136,12 @@ def load(required: bool = True):
     lib.seele_skip_bound.restype = ctypes.c_int
     lib.seele_harvest_topk.argtypes = [P, I64, I64, P, P, P, I32, P, P]
     lib.seele_harvest_topk.restype = ctypes.c_int
+    lib.seele_psnr.argtypes = [P, P, I64, P, P, P]
+    lib.seele_psnr.restype = ctypes.c_int
+    lib.seele_ssim.argtypes = [P, P, I32, I32, P, P, P]
+    lib.seele_ssim.restype = ctypes.c_int
+    lib.seele_metrics_scratch_doubles.argtypes = [I32, I32]
+    lib.seele_metrics_scratch_doubles.restype = I64
     lib.seele_profile_enable.argtypes = [I32]
     lib.seele_profile_enable.restype = ctypes.c_int
     lib.seele_profile_read.argtypes = [P, I32]
