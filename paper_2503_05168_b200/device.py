@@ -128,6 +128,14 @@ class DeviceScene:
                    host_ids)
 
     # -- C-ABI view --------------------------------------------------------------
+    @classmethod
+    def from_ply(cls, path, device=None) -> "DeviceScene":
+        """A trained-scene PLY straight into the planes layout (plyio.ply_to_planes)."""
+        from .plyio import ply_to_planes
+
+        planes, ids, _ = ply_to_planes(path)
+        return cls.from_planes(planes, ids, device)
+
     def struct(self) -> _native.Scene:
         s = _native.Scene()
         s.n = self.n
