@@ -289,10 +289,10 @@ __global__ void __launch_bounds__(kFixThreads) k_depth_fixup(Workspace ws, const
     const uint32_t *key = ws.dkey[kDepthFinal];
     uint32_t *val = ws.dval[kDepthFinal];
     uint32_t *rs = ws.drect[kDepthFinal];
-    const long long b0 = (long long)blockIdx.x * kFixOwn;
-    if (b0 >= n) return;
     const int tid = threadIdx.x;
     constexpr int kWin = kFixHalo + kFixOwn + 2 * kFixHalo;
+    // (a grid-stride loop: the grid may be smaller than the block count)
+    for (long long b0 = (long long)blockIdx.x * kFixOwn; b0 < n; b0 += (long long)gridDim.x * kFixOwn) {
     for (int k = tid; k < kWin; k += kFixThreads) {
         const long long g = b0 - kFixHalo + k;
         sk[k] = (g >= 0 && g < (long long)n) ? key[g] : 0xffffffffu;  // keys are 24-bit: never equal
@@ -336,6 +336,8 @@ __global__ void __launch_bounds__(kFixThreads) k_depth_fixup(Workspace ws, const
     if (out >= 0) {
         val[out] = p;
         rs[out] = rr;
+    }
+    __syncthreads();  // the key window is reloaded
     }
 }
 
@@ -973,7 +975,11 @@ void launch_depth_sort(const Workspace &ws, long long n_max, int64_t *stats, cud
     int grid = (int)ceil_div(n_max, DTILE);
     if (SEELE_DEPTH_CTAS_PER_SM > 0) grid = std::min(grid, SEELE_DEPTH_CTAS_PER_SM * sm_count_cached());
     for (int p = 0; p < kDepthPasses; p++) k_depth_pass<<<grid, NT, smem, st>>>(ws, p);
-    const int fix_grid = (int)ceil_div(n_max, kFixOwn);
+#ifndef SEELE_FIX_PER_SM
+#define SEELE_FIX_PER_SM 0  // 0: one CTA per 256 positions
+#endif
+    int fix_grid = (int)ceil_div(n_max, kFixOwn);
+    if (SEELE_FIX_PER_SM > 0) fix_grid = std::min(fix_grid, SEELE_FIX_PER_SM * sm_count_cached());
     k_depth_fixup<<<fix_grid > 0 ? fix_grid : 1, kFixThreads, 0, st>>>(ws, stats);
     k_depth_fix_long<<<64, 512, 0, st>>>(ws);
     note_launches(3 + kDepthPasses);
