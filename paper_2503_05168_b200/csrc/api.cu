@@ -290,7 +290,7 @@ int seele_render_split(const seele_scene *scene, const int64_t *ranges_dev, int3
 #ifndef SEELE_PRE_GRID_PER_SM
 #define SEELE_PRE_GRID_PER_SM 3  // persistent: the resident CTAs of k_preprocess (launch bounds 256, 3)
 #endif
-    const long long pre_cap = (long long)SEELE_PRE_GRID_PER_SM * sms;
+    const long long pre_cap = (long long)(SEELE_PRE_GRID_PER_SM * sms);
     const int pre_grid = (int)(pre_blocks < pre_cap ? (pre_blocks > 0 ? pre_blocks : 1) : pre_cap);
     launch_frame_begin(ws, ck, stats_dev, st);
     prof_mark(0, st);
