@@ -973,7 +973,7 @@ void launch_depth_sort(const Workspace &ws, long long n_max, int64_t *stats, cud
 #define SEELE_DEPTH_CTAS_PER_SM 2  // persistent at the resident CTAs (0: one CTA per tile)
 #endif
     int grid = (int)ceil_div(n_max, DTILE);
-    if (SEELE_DEPTH_CTAS_PER_SM > 0) grid = std::min(grid, SEELE_DEPTH_CTAS_PER_SM * sm_count_cached());
+    if (SEELE_DEPTH_CTAS_PER_SM > 0) grid = std::min(grid, (int)(SEELE_DEPTH_CTAS_PER_SM * sm_count_cached()));
     for (int p = 0; p < kDepthPasses; p++) k_depth_pass<<<grid, NT, smem, st>>>(ws, p);
 #ifndef SEELE_FIX_PER_SM
 #define SEELE_FIX_PER_SM 0  // 0: one CTA per 256 positions
