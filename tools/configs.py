@@ -9,7 +9,8 @@ RUNS = {
     "C1 100K SH3 256x256 (single view)": ["--c1"],
     "C2 1M 1080p orbit (flat)": ["--n", "1000000", "--flat"],
     "C3 3M 1080p clustered (HP + CR w=2)": [],
-    "C4 6M 3840x2160 (flat)": ["--n", "6000000", "--width", "3840", "--height", "2160", "--flat", "--steps", "30"],
+    "C4 6M 3840x2160 (flat)": ["--n", "6000000", "--width", "3840", "--height", "2160", "--flat", "--steps", "30",
+                               "--depth", "2"],
     "C5 HP off + ref (baseline 3DGS raster)": ["--flat", "--no-opacity-aware", "--engine", "ref"],
     "C5 HP off + CR w=2": ["--flat", "--no-opacity-aware", "--engine", "cr2"],
     "C5 HP on + ref": ["--engine", "ref"],
