@@ -55,7 +55,7 @@ def parse():
     ap.add_argument("--c1", action="store_true", help="BASELINE config 1 (100K random scene, one 256x256 view)")
     ap.add_argument("--no-opacity-aware", action="store_true", help="plain 3-sigma binning (C5 'HP off')")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--e2e-steps", type=int, default=60)
+    ap.add_argument("--e2e-steps", type=int, default=120, help="frames of the e2e run (120 = the whole orbit)")
     ap.add_argument("--depth", type=int, default=3, help="frames in flight (streams)")
     ap.add_argument("--raster-first", action="store_true",
                     help="raster on a high-priority stream, the plan stages of the frames in flight below it")
