@@ -34,6 +34,8 @@ class _Slot:
     contrib: torch.Tensor
     stats: torch.Tensor
     done: torch.cuda.Event
+    outs: list = None          # extra output buffer sets (image, contrib, stats, free event), alternated
+    out_next: int = 0
 
 
 class FramePipeline:
@@ -41,7 +43,7 @@ class FramePipeline:
 
     def __init__(self, rr: ResidentRenderer, width: int, height: int, *, depth: int = 2,
                  pair_capacity: int | None = None, contrib: bool = True, split: bool = False,
-                 raster_priority: bool = False):
+                 raster_priority: bool = False, out_buffers: int = 1):
         if depth < 1:
             raise ValueError("depth must be >= 1")
         self.rr = rr
@@ -64,6 +66,11 @@ class FramePipeline:
                 contrib=torch.empty((height, width), dtype=torch.int32, device=self.device) if contrib else None,
                 stats=torch.zeros(_native.STAT_COUNT, dtype=torch.int64, device=self.device),
                 done=torch.cuda.Event()))
+            s = self.slots[-1]
+            s.outs = [(s.image, s.contrib, s.stats, torch.cuda.Event())]
+            for _ in range(out_buffers - 1):  # more output sets: a consumer may still be reading the last one
+                s.outs.append((torch.empty_like(s.image), torch.empty_like(s.contrib) if contrib else None,
+                               torch.zeros_like(s.stats), torch.cuda.Event()))
         self._next = 0
         self.split = split
 
@@ -99,54 +106,67 @@ class FramePipeline:
         s = self.slots[self._next]
         self._next = (self._next + 1) % len(self.slots)
         rr = self.rr
+        image, contrib, stats, free = s.outs[s.out_next]
+        s.out_next = (s.out_next + 1) % len(s.outs)
+        if len(s.outs) > 1:  # this output set is rewritten only after its consumer released it
+            s.stream.wait_event(free)
         if self.split:  # the slot's workspace and outputs are reused: wait for its previous raster
             s.stream.wait_event(s.free)
         _select_on_device(cam, rr.centroids, rr.m, rr.beta, rr.normalization, rr.chunks, s.sel_ids, s.ranges,
                           s.stream)
         out = s.renderer.render(rr.scene, cam, cfg, ranges=s.ranges, n_ranges=rr.m + 2, n_max=rr.n_max,
-                                image=s.image, contrib=s.contrib if s.contrib is not None else False,
-                                stats=s.stats, stream=s.stream,
+                                image=image, contrib=contrib if contrib is not None else False,
+                                stats=stats, stream=s.stream,
                                 raster_stream=s.raster_stream if self.split else None)
         if self.split:
             s.free.record(s.raster_stream)
+        out.release = free  # record on the consumer's stream once done with the outputs
         return out
 
 
 class TrajectoryRenderer:
     """Host-facing trajectory rendering: frames are pipelined on the device
-    (FramePipeline) and each frame's image, contributor counts and stats are
-    copied into pinned host buffers on its slot's stream, so the device->host
-    transfer of frame k overlaps the rendering of frames k+1 .. k+depth-1.
-    ``run`` yields ``(index, image, contrib, stats)`` numpy views into pinned
+    (FramePipeline, two output sets per slot) and each frame's image,
+    contributor counts and stats are copied into pinned host buffers on a
+    dedicated copy stream, so a frame's device->host transfer overlaps the
+    rendering of the following frames without holding its slot.  ``run``
+    yields ``(index, image, contrib, stats)`` numpy views into pinned
     buffers; they stay valid until the next item is requested."""
 
     def __init__(self, rr: ResidentRenderer, width: int, height: int, *, depth: int = 2,
                  pair_capacity: int | None = None):
-        self.pipe = FramePipeline(rr, width, height, depth=depth, pair_capacity=pair_capacity)
+        self.pipe = FramePipeline(rr, width, height, depth=depth, pair_capacity=pair_capacity, out_buffers=2)
+        self.copy_stream = torch.cuda.Stream(rr.device)
+        self.n_host = 2 * depth
         self.host = [(torch.empty((height, width, 3), dtype=torch.float32, pin_memory=True),
                       torch.empty((height, width), dtype=torch.int32, pin_memory=True),
                       torch.empty(_native.STAT_COUNT, dtype=torch.int64, pin_memory=True),
-                      torch.cuda.Event()) for _ in range(depth)]
+                      torch.cuda.Event()) for _ in range(self.n_host)]
 
     def run(self, cams, cfg: EngineConfig):
-        pending = []  # (index, slot)
+        pending = []  # (index, host buffer)
+        nxt = 0
         for i, cam in enumerate(cams):
-            k = self.pipe.slot_of_next()
-            if len(pending) == self.pipe.depth:  # oldest frame must be consumed before its slot is reused
-                j, ks = pending.pop(0)
-                img, cnt, st, ev = self.host[ks]
+            if len(pending) == self.n_host:  # the oldest host buffer must be consumed before it is reused
+                j, hb = pending.pop(0)
+                img, cnt, st, ev = self.host[hb]
                 ev.synchronize()
                 yield j, img.numpy(), cnt.numpy(), st.numpy()
+            k = self.pipe.slot_of_next()
             out = self.pipe.submit(cam, cfg)
-            img, cnt, st, ev = self.host[k]
-            ostream = self.pipe.output_stream(k)
-            with torch.cuda.stream(ostream):
+            rendered = torch.cuda.Event()
+            rendered.record(self.pipe.output_stream(k))
+            img, cnt, st, ev = self.host[nxt]
+            with torch.cuda.stream(self.copy_stream):
+                self.copy_stream.wait_event(rendered)
                 st.copy_(out.stats, non_blocking=True)
                 img.copy_(out.image, non_blocking=True)
                 cnt.copy_(out.contrib, non_blocking=True)
-                ev.record(ostream)
-            pending.append((i, k))
-        for j, ks in pending:
-            img, cnt, st, ev = self.host[ks]
+                ev.record(self.copy_stream)
+                out.release.record(self.copy_stream)
+            pending.append((i, nxt))
+            nxt = (nxt + 1) % self.n_host
+        for j, hb in pending:
+            img, cnt, st, ev = self.host[hb]
             ev.synchronize()
             yield j, img.numpy(), cnt.numpy(), st.numpy()
