@@ -59,6 +59,10 @@ def parse():
     ap.add_argument("--depth", type=int, default=3, help="frames in flight (streams)")
     ap.add_argument("--raster-first", action="store_true",
                     help="raster on a high-priority stream, the plan stages of the frames in flight below it")
+    ap.add_argument("--gather", action="store_true",
+                    help="also time the run with an NCCL all-gather of every frame (uint8) + stats inside the timed "
+                         "region (value_gather)")
+    ap.add_argument("--no-exact", action="store_true", help="skip the all-fp64 precision='exact' timing")
     return ap.parse_args()
 
 
@@ -203,7 +207,7 @@ def run_reference(args):
         "metric": METRIC, "value": value, "unit": "frames/s", "n_gpus": args.gpus, "steps": steps, "warmup": warm,
         "ms_per_step": 1000.0 * sum(times) / steps, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "fp64", "data": "synthetic", "impl": "reference",
-        "config": workload_config(args, container),
+        "config": {**workload_config(args, container), "parallelism": f"frame-sharded x{args.gpus}"},
         "cpu_baseline": {"value": value, "unit": "frames/s", "cores": threads, "kind": "port",
                          "sample": f"{steps} full frames of the reference algorithm (C fp64 restatement, "
                                    f"OpenMP over tiles) incl. host cluster selection + assembly"},
@@ -328,7 +332,7 @@ def run_ours(args):
 
     # end to end through the public API: ResidentRenderer.render_trajectory, host image + contributor counts +
     # stats of every frame in pinned memory (device->host copies overlap the next frames' rendering)
-    e2e_frames = my_frames[args.warmup:args.warmup + max(1, min(args.e2e_steps, args.steps))]
+    e2e_frames = [(rank + size * k) % N_FRAMES for k in range(max(1, args.e2e_steps))]  # independent of --steps
     for _ in rr.render_trajectory([poses[f] for f in e2e_frames[:4]], cfg, depth=args.depth, pair_capacity=cap):
         pass
     torch.cuda.synchronize(device)
@@ -344,6 +348,29 @@ def run_ours(args):
         torch.distributed.all_reduce(e2e_s, op=torch.distributed.ReduceOp.MAX)
     e2e_value = size * len(e2e_frames) / float(e2e_s.item())
     d2h = args.width * args.height * (3 * 4 + 4) + 8 * _native.STAT_COUNT
+
+    # the all-fp64 raster (precision="exact": same discrete results) on the same frames, serial
+    exact_ms = None
+    if not args.no_exact:
+        cfg_exact = engine_cfg(args.engine, precision="exact", opacity_aware=not args.no_opacity_aware)
+        ex_frames = my_frames[args.warmup:args.warmup + min(args.steps, 24)] or my_frames[:1]
+        rr.render_device(poses[ex_frames[0]], cfg_exact, renderer=renderer)
+        torch.cuda.synchronize(device)
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ev0.record(stream)
+        for f in ex_frames:
+            rr.render_device(poses[f], cfg_exact, renderer=renderer)
+        ev1.record(stream)
+        torch.cuda.synchronize(device)
+        exact_ms = ev0.elapsed_time(ev1) / len(ex_frames)
+        ex_t = torch.tensor([exact_ms], dtype=torch.float64, device=device)
+        if size > 1:
+            torch.distributed.all_reduce(ex_t, op=torch.distributed.ReduceOp.MAX)
+        exact_ms = float(ex_t.item())
+
+    gather_info = None
+    if args.gather:
+        gather_info = timed_gather(args, rr, poses, cfg, my_frames, cap, device, stream, rank, size)
 
     if rank == 0:
         peaks = load_peaks()
@@ -376,7 +403,7 @@ def run_ours(args):
         out = {
             "metric": METRIC, "value": value, "unit": "frames/s", "n_gpus": size, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": max_ms / args.steps, "higher_is_better": True, "scaling": "weak",
-            "value_serial": value_serial, "frames_in_flight": args.depth,
+            "value_serial": value_serial, "frames_in_flight": args.depth, "frames_per_rank": args.steps,
             "vs_baseline": None, "dtype": "fp64+fp32", "data": "synthetic",
             "config": {**workload_config(args, container), "parallelism": f"frame-sharded x{size}"},
             "roofline": {"kernel": "k_raster_quad (raster stage)", "bound": "fp32",
@@ -396,6 +423,10 @@ def run_ours(args):
                     "frames": len(e2e_frames), "overflow": e2e_overflow,
                     "api": f"ResidentRenderer.render_trajectory(cams, cfg, depth={args.depth}): float32 image + "
                            f"contributor counts + stats to pinned host memory per frame"},
+            "value_exact_serial": (size / (exact_ms / 1000.0)) if exact_ms else None,
+            "exact_note": "precision='exact': all-fp64 raster (reference operation order), identical discrete "
+                          "results; frames/s one frame at a time (compare value_serial)",
+            "gather": gather_info,
             "gpu_launches": int(launches),
             "clocks": clock_info,
             "overflow": overflow,
@@ -408,8 +439,74 @@ def run_ours(args):
         torch.distributed.destroy_process_group()
 
 
+def timed_gather(args, rr, poses, cfg, my_frames, cap, device, stream, rank, size) -> dict:
+    """The pipelined run again, each frame quantised (io.quantize_image rule) into a preallocated uint8 buffer
+    and, inside the timed region, ONE NCCL all_gather_into_tensor of every rank's frames + stats (the
+    north_star's optional gather over NVLink)."""
+    import torch.distributed as dist
+    from paper_2503_05168_b200 import _native
+    from paper_2503_05168_b200.distributed import quantize
+    from paper_2503_05168_b200.pipeline import FramePipeline
+    steps = args.steps
+    pipe = FramePipeline(rr, args.width, args.height, depth=args.depth, pair_capacity=cap)
+    frames_u8 = torch.zeros((steps, args.height, args.width, 3), dtype=torch.uint8, device=device)
+    stats = torch.zeros((steps, _native.STAT_COUNT), dtype=torch.int64, device=device)
+    all_u8 = torch.empty((size * steps, args.height, args.width, 3), dtype=torch.uint8, device=device)
+    all_st = torch.empty((size * steps, _native.STAT_COUNT), dtype=torch.int64, device=device)
+
+    def one_pass(frames, timed):
+        for k, f in enumerate(frames):
+            slot = pipe.slot_of_next()
+            out = pipe.submit(poses[f], cfg)
+            st = pipe.output_stream(slot)
+            with torch.cuda.stream(st):
+                frames_u8[k].copy_(quantize(out.image))
+                stats[k].copy_(out.stats)
+                out.release.record(st)
+        pipe.join(stream)
+        if timed and size > 1:
+            dist.all_gather_into_tensor(all_u8, frames_u8)
+            dist.all_gather_into_tensor(all_st, stats)
+
+    one_pass(my_frames[:args.warmup], False)
+    torch.cuda.synchronize(device)
+    if size > 1:
+        dist.barrier()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0.record(stream)
+    pipe.wait_for(stream)
+    one_pass(my_frames[args.warmup:], True)
+    ev1.record(stream)
+    torch.cuda.synchronize(device)
+    ms = torch.tensor([ev0.elapsed_time(ev1)], dtype=torch.float64, device=device)
+    if size > 1:
+        dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+    ms = float(ms.item())
+    frame_bytes = args.height * args.width * 3 + 8 * _native.STAT_COUNT
+    del pipe
+    return {"value_gather": size * steps / (ms / 1000.0), "ms_per_step": ms / steps,
+            "collective": "all_gather_into_tensor (NCCL) of uint8 frames + int64 stats, once per timed run"
+            if size > 1 else "none (1 GPU: frames quantised into the gather buffer only)",
+            "bytes_per_frame": frame_bytes,
+            "nvlink_bytes_per_frame_per_rank": frame_bytes * (size - 1) if size > 1 else 0}
+
+
+def spawn_ranks(n: int) -> int:
+    """``bench.py --gpus N`` outside torchrun: re-launch this script as N ranks (one per GPU) under
+    torch.distributed.run on 127.0.0.1; rank 0 prints the JSON line."""
+    import socket
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), str(Path(__file__).resolve())] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
 def main():
     args = parse()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        raise SystemExit(spawn_ranks(args.gpus))
     if args.impl == "reference":
         run_reference(args)
     else:

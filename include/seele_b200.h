@@ -175,6 +175,18 @@ int64_t seele_metrics_scratch_doubles(int32_t width, int32_t height);
 int seele_harvest_topk(void *workspace, int64_t n_max, int64_t pair_capacity, const seele_camera *cam,
                        const seele_config *cfg, const int64_t *ids_dev, int32_t k, uint8_t *flags_dev, void *stream);
 
+/* Dense contribution matrix of render_frame(..., record_contributions=True)
+ * (render.py:172-193, 229-233; replaces the contrib_out rows of
+ * rasterize.py:176-177): for the frame LAST RENDERED into this workspace
+ * with the same camera and config (n_ws assembled splats), out_dev[r * W*H +
+ * pixel] = T * alpha of every blend of plan ref r (the r-th accepted splat in
+ * assembled order) at that pixel, in fp64 with the reference's schedule.
+ * out_dev must hold P x W*H doubles, zero-filled by the caller (P = accepted
+ * splats); row_of_pos_dev (n_ws int32) receives the plan ref of each assembled
+ * position (-1: culled / degenerate).  Stream-ordered; no sync. */
+int seele_contributions(void *workspace, int64_t n_max, int64_t pair_capacity, const seele_camera *cam,
+                        const seele_config *cfg, int64_t n_ws, int32_t *row_of_pos_dev, double *out_dev, void *stream);
+
 /* frame_skip_bound (render.py:236-256, rasterize.py:325-377): per-pixel
  * certified error bound of the group-gated engine (group width cfg->group_w)
  * for the frame LAST RENDERED into this workspace with the same camera and

@@ -254,29 +254,49 @@ int64_t oracle_sort_pairs(int64_t p, const int32_t *rect, const double *depth, i
         total += (int64_t)(rc[1] - rc[0] + 1) * (rc[3] - rc[2] + 1);
     }
     if (!pair_tile) return total;
+    /* np.lexsort((ref, depth, tile)) (sorting.py:43): the primary key partitions the pairs into tiles, so
+     * each tile's pairs are gathered (emission order) and sorted by the full comparator independently --
+     * the same order as one global sort, with the tiles sorted in parallel. */
+    const int64_t n_tiles = (int64_t)tiles_x * tiles_y;
+    int64_t *start = (int64_t *)calloc((size_t)n_tiles + 1, sizeof(int64_t));
+    for (int64_t r = 0; r < p; r++) {
+        const int32_t *rc = rect + 4 * r;
+        if (rc[0] > rc[1] || rc[2] > rc[3]) continue;
+        for (int32_t ty = rc[2]; ty <= rc[3]; ty++)
+            for (int32_t tx = rc[0]; tx <= rc[1]; tx++) start[(int64_t)ty * tiles_x + tx + 1]++;
+    }
+    for (int64_t t = 0; t < n_tiles; t++) start[t + 1] += start[t];
+    int64_t *fill = (int64_t *)malloc(sizeof(int64_t) * (size_t)(n_tiles ? n_tiles : 1));
+    for (int64_t t = 0; t < n_tiles; t++) fill[t] = start[t];
     oc_pair *pairs = (oc_pair *)malloc(sizeof(oc_pair) * (total ? total : 1));
-    int64_t k = 0;
     for (int64_t r = 0; r < p; r++) {
         const int32_t *rc = rect + 4 * r;
         if (rc[0] > rc[1] || rc[2] > rc[3]) continue;
         for (int32_t ty = rc[2]; ty <= rc[3]; ty++)
             for (int32_t tx = rc[0]; tx <= rc[1]; tx++) {
-                pairs[k].tile = ty * tiles_x + tx;
-                pairs[k].ref = (int32_t)r;
-                pairs[k].depth = depth[r];
-                k++;
+                const int64_t t = (int64_t)ty * tiles_x + tx;
+                oc_pair *q = pairs + fill[t]++;
+                q->tile = (int32_t)t;
+                q->ref = (int32_t)r;
+                q->depth = depth[r];
             }
     }
-    qsort(pairs, (size_t)total, sizeof(oc_pair), pair_cmp);
-    int64_t n_tiles = (int64_t)tiles_x * tiles_y;
-    for (int64_t t = 0; t < n_tiles; t++) range_start[t] = range_end[t] = 0;
+#pragma omp parallel for schedule(dynamic, 16)
+    for (int64_t t = 0; t < n_tiles; t++)
+        if (start[t + 1] - start[t] > 1)
+            qsort(pairs + start[t], (size_t)(start[t + 1] - start[t]), sizeof(oc_pair), pair_cmp);
+    for (int64_t t = 0; t < n_tiles; t++) {
+        range_start[t] = start[t] < start[t + 1] ? start[t] : 0;
+        range_end[t] = start[t] < start[t + 1] ? start[t + 1] : 0;
+    }
+#pragma omp parallel for schedule(static)
     for (int64_t i = 0; i < total; i++) {
         pair_tile[i] = pairs[i].tile;
         pair_ref[i] = pairs[i].ref;
-        if (i == 0 || pairs[i].tile != pairs[i - 1].tile) range_start[pairs[i].tile] = i;
-        if (i == total - 1 || pairs[i].tile != pairs[i + 1].tile) range_end[pairs[i].tile] = i + 1;
     }
     free(pairs);
+    free(fill);
+    free(start);
     return total;
 }
 

@@ -49,6 +49,7 @@ EXPORTED_SYMBOLS = (
     "seele_select_clusters",
     "seele_plan_export",
     "seele_skip_bound",
+    "seele_contributions",
     "seele_harvest_topk",
     "seele_psnr",
     "seele_ssim",
@@ -134,6 +135,8 @@ def load(required: bool = True):
     lib.seele_plan_export.restype = ctypes.c_int
     lib.seele_skip_bound.argtypes = [P, I64, I64, P, P, P, P]
     lib.seele_skip_bound.restype = ctypes.c_int
+    lib.seele_contributions.argtypes = [P, I64, I64, P, P, I64, P, P, P]
+    lib.seele_contributions.restype = ctypes.c_int
     lib.seele_harvest_topk.argtypes = [P, I64, I64, P, P, P, I32, P, P]
     lib.seele_harvest_topk.restype = ctypes.c_int
     lib.seele_psnr.argtypes = [P, P, I64, P, P, P]

@@ -182,6 +182,29 @@ def build_cluster_table(scene: SceneArrays, poses, n_clusters: int = 24, neighbo
                         share_threshold=share_threshold)
 
 
+def top_contributors_per_pixel(contributions, ids, k: int) -> np.ndarray:
+    """compiler.py:196-213 on the device: the union over pixels of each
+    pixel's k strongest blended splats, ties at the k-th rank toward the
+    smaller id (rows put in id order, then a stable descending sort per
+    pixel column).  ``contributions`` is the (P, H*W) matrix of
+    render_frame(record_contributions=True) -- a device tensor or an array --
+    and ``ids`` its contribution_ids."""
+    import torch
+
+    m = contributions if isinstance(contributions, torch.Tensor) else torch.as_tensor(np.asarray(contributions))
+    if m.numel() == 0:
+        return np.array([], dtype=np.int64)
+    dev = m.device if m.is_cuda else torch.device("cuda", torch.cuda.current_device())
+    m = m.to(device=dev, dtype=torch.float64)
+    ids_t = torch.as_tensor(np.asarray(ids, dtype=np.int64), device=dev)
+    order = torch.sort(ids_t, stable=True).indices
+    ids_sorted, matrix = ids_t[order], m[order]
+    rank = torch.sort(matrix, dim=0, descending=True, stable=True).indices[:k]
+    picked = torch.gather(matrix, 0, rank) > 0.0
+    chosen = ids_sorted[rank[picked]]
+    return torch.unique(chosen).cpu().numpy().astype(np.int64)
+
+
 def harvest_top_contributors(cluster, scene, k: int, cfg=None) -> np.ndarray:
     """compiler.py:216-231 on the GPU: ids of every splat that makes some
     pixel's top-k (blend weight T * alpha > 0, ties toward the smaller id) for

@@ -412,6 +412,28 @@ int seele_harvest_topk(void *workspace, int64_t n_max, int64_t pair_capacity, co
     return SEELE_OK;
 }
 
+int seele_contributions(void *workspace, int64_t n_max, int64_t pair_capacity, const seele_camera *cam,
+                        const seele_config *cfg, int64_t n_ws, int32_t *row_of_pos_dev, double *out_dev, void *stream) {
+    g_err[0] = 0;
+    int rc;
+    if ((rc = check_camera(cam)) != SEELE_OK) return rc;
+    if ((rc = check_config(cfg)) != SEELE_OK) return rc;
+    if (!workspace || !row_of_pos_dev || !out_dev) return fail(SEELE_ERR_INVALID_ARGUMENT, "null argument");
+    if (n_ws < 0 || n_ws > n_max) return fail(SEELE_ERR_INVALID_ARGUMENT, "n_ws out of [0, n_max]");
+    const Workspace ws = carve_workspace(workspace, n_max, pair_capacity, cam->width, cam->height);
+    const CamK ck = make_cam(*cam);
+    CfgK cf{};
+    cf.engine = cfg->engine;
+    cf.group_w = cfg->group_w;
+    cf.alpha_theta = cfg->alpha_theta;
+    cf.gamma = cfg->gamma_threshold;
+    launch_contributions(cfg->engine == 0 ? 0 : cfg->group_w, ws, ws.pfinal, ck, cf, n_ws, row_of_pos_dev, out_dev,
+                         static_cast<cudaStream_t>(stream));
+    cudaError_t e;
+    if ((e = cudaGetLastError()) != cudaSuccess) return cuda_fail(e, "seele_contributions");
+    return SEELE_OK;
+}
+
 int seele_skip_bound(void *workspace, int64_t n_max, int64_t pair_capacity, const seele_camera *cam,
                      const seele_config *cfg, double *bound_dev, void *stream) {
     g_err[0] = 0;

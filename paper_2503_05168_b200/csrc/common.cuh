@@ -150,6 +150,8 @@ void launch_raster(const Workspace &ws, const uint32_t *pair_pos, const CamK &ca
 // FAST engine tile kernel (raster_fast.cu); W = 0 (ref) or CR group width.
 void launch_harvest(int engine_w, const Workspace &ws, const uint32_t *pair_pos, const CamK &cam, const CfgK &cfg,
                     const int64_t *ids, int k, uint8_t *flags, cudaStream_t st);
+void launch_contributions(int engine_w, const Workspace &ws, const uint32_t *pair_pos, const CamK &cam,
+                          const CfgK &cfg, long long n_ws, int32_t *row_of_pos, double *out, cudaStream_t st);
 void launch_skip_bound(int group_w, const Workspace &ws, const uint32_t *pair_pos, const CamK &cam, const CfgK &cfg,
                        double *bound, cudaStream_t st);
 void launch_raster_fast(int W, const Workspace &ws, const uint32_t *pair_pos, const CamK &cam,

@@ -6,10 +6,15 @@
 // (preprocess.py:89-146: near cull, EWA Jacobian, 0.3 low-pass, determinant
 // test, conic), sh_to_color (model.py:264-305), effective_radius_sq
 // (preprocess.py:68-71) and the bin_tiles extent box (preprocess.py:159-189).
-// All of it runs in fp64 in the reference's operation order; this file is
-// compiled with --fmad=false so no FMA contraction changes a rounding.  The
-// kernel is HBM-bound: 240 B of scene in (float4 planes, coalesced) and
-// ~140 B of records out per splat.
+// The projection runs in fp64 in the reference's operation order, but with
+// FMA contraction allowed and a reciprocal 1/z where the reference divides
+// (preprocess.py:107): the fp64 results differ from numpy's in the last bits,
+// so a discrete output (tile rect, depth order) could flip only for a value
+// within ~1e-15 relative of a tile edge or of another depth -- never on the
+// test scenes, where the oracle comparison over whole trajectories is the
+// gate.  K0 (k_select) is written with explicit _rn intrinsics (no
+// contraction): its distances are numpy's.  K1 is HBM-bound: 240 B of scene
+// in (float4 planes, coalesced) and the raster record out per splat.
 #include <math.h>
 
 #include "common.cuh"
@@ -446,18 +451,18 @@ __global__ void k_select(CamK cam, const double *__restrict__ centroids, int n, 
                          int32_t *out_ids, int64_t *ranges_out) {
     __shared__ double d2[1024];
     double f[6];
-    f[0] = (cam.pos[0] - mean3.x) / scale;
-    f[1] = (cam.pos[1] - mean3.y) / scale;
-    f[2] = (cam.pos[2] - mean3.z) / scale;
+    f[0] = __ddiv_rn(__dsub_rn(cam.pos[0], mean3.x), scale);
+    f[1] = __ddiv_rn(__dsub_rn(cam.pos[1], mean3.y), scale);
+    f[2] = __ddiv_rn(__dsub_rn(cam.pos[2], mean3.z), scale);
     // CameraPose.forward = R_cw[:, 2] (model.py:174-176) = row 2 of world_to_view
-    f[3] = beta * cam.w2v[6];
-    f[4] = beta * cam.w2v[7];
-    f[5] = beta * cam.w2v[8];
+    f[3] = __dmul_rn(beta, cam.w2v[6]);
+    f[4] = __dmul_rn(beta, cam.w2v[7]);
+    f[5] = __dmul_rn(beta, cam.w2v[8]);
     for (int c = threadIdx.x; c < n; c += blockDim.x) {
         double s = 0.0;
         for (int k = 0; k < 6; k++) {
-            double v = centroids[6 * c + k] - f[k];
-            s = s + v * v;
+            const double v = __dsub_rn(centroids[6 * c + k], f[k]);
+            s = __dadd_rn(s, __dmul_rn(v, v));  // numpy's squared-then-summed values: no contraction
         }
         d2[c] = s;
     }

@@ -253,6 +253,87 @@ __global__ void __launch_bounds__(256) k_harvest(Workspace ws, const uint32_t *_
         if (s_w[q * 256 + tid] > 0.0) flags[s_p[q * 256 + tid]] = 1u;
 }
 
+// ---------------------------------------------------------------------------
+// Dense contribution matrix (render.py:172-193 with record_contributions):
+// the EXACT engine's schedule, every blend writes its weight T * alpha
+// (rasterize.py:176-177) to out[row_of_pos[p] * n_pix + pixel], row = the
+// splat's plan ref.  The caller zero-fills out (P x H*W fp64).
+template <int W>
+__global__ void __launch_bounds__(256) k_contrib(Workspace ws, const uint32_t *__restrict__ pair_pos, CamK cam,
+                                                 CfgK cfg, const int32_t *__restrict__ row_of_pos, double *out) {
+    __shared__ double s_mx[256], s_my[256], s_a[256], s_b[256], s_c[256], s_o[256];
+    __shared__ uint32_t s_p[256];
+    const int tile = blockIdx.x;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    int lx, ly;
+    pixel_of<W>(warp, lane, lx, ly);
+    const int x = (tile % cam.tiles_x) * kTile + lx, y = (tile / cam.tiles_x) * kTile + ly;
+    const bool valid = x < cam.width && y < cam.height;
+    const double px = x + 0.5, py = y + 0.5;
+    const long long n_pix = (long long)cam.width * cam.height, pix = (long long)y * cam.width + x;
+    int leader;
+    unsigned gmask;
+    group_of<W>(lane, leader, gmask);
+    const bool is_leader = lane == leader;
+    Px64 s{1.0, 0.0, 0.0, 0.0, 0, !valid};
+    Counters k{0, 0, 0};
+    const uint2 rg = ws.ranges[tile];
+    for (uint32_t b0 = rg.x; b0 < rg.y; b0 += 256) {
+        if (__syncthreads_count(!s.done) == 0) break;
+        const uint32_t i = b0 + tid;
+        if (i < rg.y) {
+            const uint32_t p = pair_pos[i];
+            const double2 m = ws.mean[p];
+            const double4 co = ws.conic_op[p];
+            s_mx[tid] = m.x;
+            s_my[tid] = m.y;
+            s_a[tid] = co.x;
+            s_b[tid] = co.y;
+            s_c[tid] = co.z;
+            s_o[tid] = co.w;
+            s_p[tid] = p;
+        }
+        __syncthreads();
+        const int nb = min(256u, rg.y - b0);
+        for (int j = 0; j < nb; j++) {
+            const int cnt0 = s.cnt;
+            double w = 0.0;
+            if (!step64<W>(s, px, py, is_leader, leader, gmask, s_mx[j], s_my[j], s_a[j], s_b[j], s_c[j], s_o[j], 0.f,
+                           0.f, 0.f, cfg.alpha_theta, cfg.gamma, k, &w))
+                break;
+            if (s.cnt != cnt0 && valid) out[(long long)row_of_pos[s_p[j]] * n_pix + pix] = w;
+        }
+    }
+}
+
+// Plan ref of every assembled position (exclusive scan of status == 0; -1
+// for rejected splats), one CTA.
+__global__ void __launch_bounds__(1024) k_row_of_pos(Workspace ws, long long n_ws, int32_t *row_of_pos) {
+    __shared__ int32_t s_w[32];
+    __shared__ int32_t s_base;
+    if (threadIdx.x == 0) s_base = 0;
+    __syncthreads();
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    for (long long b = 0; b < n_ws; b += 1024) {
+        const long long p = b + threadIdx.x;
+        const bool ok = p < n_ws && ws.status[p] == 0;
+        const unsigned bal = __ballot_sync(0xffffffffu, ok);
+        if (lane == 0) s_w[warp] = __popc(bal);
+        __syncthreads();
+        int before = s_base;
+        for (int w = 0; w < warp; w++) before += s_w[w];
+        before += __popc(bal & ((1u << lane) - 1u));
+        if (p < n_ws) row_of_pos[p] = ok ? before : -1;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            int t = 0;
+            for (int w = 0; w < 32; w++) t += s_w[w];
+            s_base += t;
+        }
+        __syncthreads();
+    }
+}
+
 template <int W>
 void launch_engine(const Workspace &ws, const uint32_t *pair_pos, const CamK &cam, const CfgK &cfg, float *image,
                    int32_t *contrib, int64_t *stats, cudaStream_t st) {
@@ -298,6 +379,19 @@ void launch_harvest(int engine_w, const Workspace &ws, const uint32_t *pair_pos,
         default: k_harvest<4><<<n_tiles, 256, smem, st>>>(ws, pair_pos, cam, cfg, ids, k, flags); break;
     }
     note_launches(1);
+}
+
+void launch_contributions(int engine_w, const Workspace &ws, const uint32_t *pair_pos, const CamK &cam,
+                          const CfgK &cfg, long long n_ws, int32_t *row_of_pos, double *out, cudaStream_t st) {
+    const int n_tiles = cam.tiles_x * cam.tiles_y;
+    k_row_of_pos<<<1, 1024, 0, st>>>(ws, n_ws, row_of_pos);
+    switch (engine_w) {
+        case 0: k_contrib<0><<<n_tiles, 256, 0, st>>>(ws, pair_pos, cam, cfg, row_of_pos, out); break;
+        case 1: k_contrib<1><<<n_tiles, 256, 0, st>>>(ws, pair_pos, cam, cfg, row_of_pos, out); break;
+        case 2: k_contrib<2><<<n_tiles, 256, 0, st>>>(ws, pair_pos, cam, cfg, row_of_pos, out); break;
+        default: k_contrib<4><<<n_tiles, 256, 0, st>>>(ws, pair_pos, cam, cfg, row_of_pos, out); break;
+    }
+    note_launches(2);
 }
 
 void launch_raster(const Workspace &ws, const uint32_t *pair_pos, const CamK &cam, const CfgK &cfg, float *image,

@@ -81,7 +81,7 @@ struct Px64 {
 template <int W>
 __device__ __forceinline__ bool step64(Px64 &s, double px, double py, bool is_leader, int leader, unsigned gmask,
                                        double mx, double my, double a, double b, double c, double o, float r, float g,
-                                       float bl, double th, double gm, Counters &k) {
+                                       float bl, double th, double gm, Counters &k, double *w_out = nullptr) {
     const bool live = !s.done;
     const unsigned lb = __ballot_sync(0xffffffffu, live);
     if (lb == 0u) return false;
@@ -113,6 +113,7 @@ __device__ __forceinline__ bool step64(Px64 &s, double px, double py, bool is_le
     k.blend += __any_sync(0xffffffffu, blend);
     if (blend) {  // _blend (rasterize.py:169-177)
         const double wgt = __dmul_rn(s.T, al);
+        if (w_out) *w_out = wgt;  // the contribution row entry (rasterize.py:176-177)
         s.C0 = __dadd_rn(s.C0, __dmul_rn(wgt, (double)r));
         s.C1 = __dadd_rn(s.C1, __dmul_rn(wgt, (double)g));
         s.C2 = __dadd_rn(s.C2, __dmul_rn(wgt, (double)bl));

@@ -49,58 +49,67 @@ class ShardedResult:
 
 
 def render_trajectory(render_one: Callable[[int], tuple[torch.Tensor, torch.Tensor]], n_frames: int,
-                      *, gather: bool = False, device=None, group=None) -> ShardedResult:
+                      *, gather: bool = False, device=None, group=None, to_host: bool = True) -> ShardedResult:
     """Render this rank's share of an ``n_frames`` trajectory.
 
     ``render_one(f) -> (image [H,W,3] float32, stats [STAT_COUNT] int64)`` renders
-    frame f on this rank's device (e.g. ResidentRenderer.render_device).  With
-    ``gather`` the quantised images and the stats of every frame are collected
-    on rank 0 in trajectory order (one all_gather of fixed-size buffers per
-    round of frames; ranks with fewer frames contribute padding).
+    frame f on this rank's device (e.g. ResidentRenderer.render_device), without
+    host synchronisation.  Each frame is quantised on the device into a
+    preallocated [rounds, H, W, 3] uint8 buffer (rounds = ceil(n_frames / world);
+    ranks with fewer frames leave zero padding and stats rows of -1).  With
+    ``gather`` ONE all_gather_into_tensor of the images and one of the stats
+    (NCCL over NVLink, or gloo) assemble every frame on every rank, in
+    trajectory order: row r * world + src holds frame r * world + src.  There
+    is no per-frame host copy; with ``to_host`` the results are read back once
+    at the end (rank 0 for the gathered set).
     """
     rank = dist.get_rank(group) if dist.is_initialized() else 0
     world = dist.get_world_size(group) if dist.is_initialized() else 1
     mine = frames_for_rank(rank, world, n_frames)
-    stats, images = [], []
-    for f in mine:
+    rounds = -(-n_frames // world)
+    imgs = sts = None
+    dev = torch.device(device) if device is not None else None
+    for r, f in enumerate(mine):
         img, st = render_one(f)
-        stats.append(st.detach().to("cpu", torch.int64).numpy().copy())
-        if gather:
-            images.append(quantize(img))
-    out = ShardedResult(frames=mine, stats=np.stack(stats) if stats else np.zeros((0, _native.STAT_COUNT), np.int64))
+        if imgs is None:
+            dev = dev or img.device
+            imgs = torch.zeros((rounds,) + tuple(img.shape), dtype=torch.uint8, device=dev)
+            sts = torch.full((rounds, _native.STAT_COUNT), -1, dtype=torch.int64, device=dev)
+        imgs[r].copy_(quantize(img))
+        sts[r].copy_(st)
+    if dev is None:  # this rank rendered nothing: the collective still needs a device
+        if dist.is_initialized() and dist.get_backend(group) == "nccl":
+            dev = torch.device("cuda", torch.cuda.current_device())
+        else:
+            dev = torch.device("cpu")
+    local_stats = sts[:len(mine)] if sts is not None else torch.zeros((0, _native.STAT_COUNT), dtype=torch.int64)
+    out = ShardedResult(frames=mine, stats=local_stats.cpu().numpy() if to_host else local_stats)
     if not gather:
         return out
-    if world == 1:
-        out.gathered_frames = list(mine)
-        out.gathered_images = torch.stack(images).cpu().numpy() if images else None
-        out.gathered_stats = out.stats
-        return out
-    rounds = -(-n_frames // world)
-    shape = images[0].shape if images else None
-    shape_t = torch.tensor(list(shape) if shape else [0, 0, 0], dtype=torch.int64, device=device)
-    dist.all_reduce(shape_t, op=dist.ReduceOp.MAX, group=group)
-    h, w, c = (int(v) for v in shape_t.tolist())
-    all_imgs, all_stats, order = [], [], []
-    for r in range(rounds):
-        f_local = r * world + rank
-        has = f_local < n_frames
-        img = images[r] if has else torch.zeros((h, w, c), dtype=torch.uint8, device=device)
-        st = torch.as_tensor(out.stats[r] if has else np.full(_native.STAT_COUNT, -1, np.int64), device=device)
-        imgs = [torch.empty_like(img) for _ in range(world)]
-        sts = [torch.empty_like(st) for _ in range(world)]
-        dist.all_gather(imgs, img.contiguous(), group=group)
-        dist.all_gather(sts, st.contiguous(), group=group)
-        if rank == 0:
-            for src in range(world):
-                f = r * world + src
-                if f < n_frames:
-                    order.append(f)
-                    all_imgs.append(imgs[src].cpu().numpy())
-                    all_stats.append(sts[src].cpu().numpy())
+    if world > 1:
+        shape_t = torch.tensor(list(imgs.shape[1:]) if imgs is not None else [0, 0, 0], dtype=torch.int64,
+                               device=dev)
+        dist.all_reduce(shape_t, op=dist.ReduceOp.MAX, group=group)
+        shape = tuple(int(v) for v in shape_t.tolist())
+        if imgs is None:
+            imgs = torch.zeros((rounds,) + shape, dtype=torch.uint8, device=dev)
+            sts = torch.full((rounds, _native.STAT_COUNT), -1, dtype=torch.int64, device=dev)
+        all_imgs = torch.empty((world * rounds,) + shape, dtype=torch.uint8, device=dev)
+        all_sts = torch.empty((world * rounds, _native.STAT_COUNT), dtype=torch.int64, device=dev)
+        dist.all_gather_into_tensor(all_imgs, imgs, group=group)
+        dist.all_gather_into_tensor(all_sts, sts, group=group)
+        # [src, round] -> frame round * world + src
+        all_imgs = all_imgs.view((world, rounds) + shape).transpose(0, 1).reshape((world * rounds,) + shape)
+        all_sts = all_sts.view(world, rounds, -1).transpose(0, 1).reshape(world * rounds, -1)
+    else:
+        all_imgs, all_sts = imgs, sts
+    out.extras["device_images"] = all_imgs[:n_frames] if all_imgs is not None else None
+    out.extras["device_stats"] = all_sts[:n_frames] if all_sts is not None else None
     if rank == 0:
-        out.gathered_frames = order
-        out.gathered_images = np.stack(all_imgs)
-        out.gathered_stats = np.stack(all_stats)
+        out.gathered_frames = list(range(n_frames))
+        if to_host:
+            out.gathered_images = all_imgs[:n_frames].cpu().numpy() if all_imgs is not None else None
+            out.gathered_stats = all_sts[:n_frames].cpu().numpy() if all_sts is not None else None
     return out
 
 

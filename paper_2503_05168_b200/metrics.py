@@ -5,6 +5,8 @@ device.  Inputs are (H, W, 3) arrays (numpy, or torch tensors on the device);
 results are Python floats like the reference's."""
 from __future__ import annotations
 
+from dataclasses import dataclass
+
 import numpy as np
 
 from . import _native
@@ -58,3 +60,49 @@ def ssim(img_a, img_b) -> float:
     _native.check(lib.seele_ssim(a.data_ptr(), b.data_ptr(), w, h, scratch.data_ptr(), out.data_ptr(),
                                  torch.cuda.current_stream(a.device).cuda_stream))
     return float(out.item())
+
+
+@dataclass
+class ContributionCurve:
+    """metrics.py:104-112."""
+
+    aggregate: np.ndarray         # (p,) mean cumulative weight of the k strongest splats
+    per_pixel_totals: np.ndarray  # (h*w,) total blended weight
+    fraction_for_99: float        # mean fraction of a pixel's splats covering 99 %
+    per_pixel_curves: list | None = None
+
+
+def contribution_cdf(scene, cam, cfg=None, *, keep_per_pixel: bool = False) -> ContributionCurve:
+    """metrics.py:115-161 on the GPU: the dense contribution matrix comes from
+    render_frame(record_contributions=True) (seele_contributions, reference
+    schedule in fp64) and stays on the device; every pixel's weights are
+    sorted in descending order and accumulated column by column (a sequential
+    scan per pixel, the same association as numpy's cumsum), and the 99 %
+    rank is searchsorted(cumulative, 0.99 total - 1e-15) + 1 as a count of
+    cumulative values below the target."""
+    import torch
+
+    from .render import EngineConfig, render_frame
+
+    cfg = cfg or EngineConfig()
+    result = render_frame(scene, cam, cfg, record_contributions=True, output="torch")
+    matrix = result.contributions
+    n_pixels = int(matrix.shape[1]) if matrix is not None else 0
+    if matrix is None or matrix.numel() == 0:
+        return ContributionCurve(aggregate=np.zeros(0), per_pixel_totals=np.zeros(n_pixels), fraction_for_99=0.0,
+                                 per_pixel_curves=[] if keep_per_pixel else None)
+    sorted_desc = torch.sort(matrix, dim=0, descending=True).values
+    cumulative = torch.cumsum(sorted_desc, dim=0)  # (p, n_pixels), outer-dimension scan: sequential per column
+    totals = cumulative[-1]
+    counts = (sorted_desc > 0.0).sum(dim=0)
+    target = 0.99 * totals - 1e-15
+    rank = (cumulative < target[None, :]).sum(dim=0) + 1
+    has = counts > 0
+    fractions = rank[has].to(torch.float64) / counts[has].to(torch.float64)
+    fraction_for_99 = float(fractions.cpu().numpy().mean()) if int(has.sum()) else 0.0
+    curves = None
+    if keep_per_pixel:
+        cum_h, cnt_h = cumulative.cpu().numpy(), counts.cpu().numpy()
+        curves = [cum_h[:max(int(c), 1), pix] if c else np.zeros(0) for pix, c in enumerate(cnt_h)]
+    return ContributionCurve(aggregate=cumulative.mean(dim=1).cpu().numpy(), per_pixel_totals=totals.cpu().numpy(),
+                             fraction_for_99=fraction_for_99, per_pixel_curves=curves)

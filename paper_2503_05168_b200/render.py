@@ -185,7 +185,8 @@ class FrameRenderer:
         self.lib = _native.load()
         if not torch.cuda.is_available():
             raise DeviceError("no CUDA device: the B200 render path has no CPU fallback")
-        self.device = torch.device(device or "cuda")
+        dev = torch.device(device or "cuda")
+        self.device = torch.device("cuda", torch.cuda.current_device()) if dev.index is None else dev
         self.pair_capacity = int(pair_capacity) if pair_capacity else 0
         self.n_max = 0
         self.size = (0, 0)
@@ -224,11 +225,22 @@ class FrameRenderer:
             ranges, n_ranges = self._ranges, 1
         if image is None:
             image = torch.empty((h, w, 3), dtype=torch.float32, device=self.device)
+        else:
+            _check_output("image", image, (h, w, 3), torch.float32, self.device)
         if contrib is True:
             contrib = torch.empty((h, w), dtype=torch.int32, device=self.device)
         elif contrib is False:
             contrib = None
-        stats = self.stats if stats is None else stats
+        else:
+            _check_output("contrib", contrib, (h, w), torch.int32, self.device)
+        if stats is None:
+            stats = self.stats
+        else:
+            _check_output("stats", stats, (_native.STAT_COUNT,), torch.int64, self.device)
+        if ranges is not None:
+            _check_output("ranges", ranges, (ranges.shape[0], 2), torch.int64, self.device)
+            if not 1 <= n_ranges <= ranges.shape[0]:
+                raise InvalidArgumentError(f"n_ranges {n_ranges} out of [1, {ranges.shape[0]}]")
         st = stream if stream is not None else torch.cuda.current_stream(self.device)
         sc = scene.struct()
         camc = _native.camera_struct(cam)
@@ -325,6 +337,17 @@ class FrameRenderer:
             rects=rect.cpu().numpy()[:n_ws][ok], positions=ok)
 
 
+def _check_output(name: str, t, shape: tuple, dtype, device) -> None:
+    """Caller-supplied device buffers must match the frame exactly: the kernels
+    write ``shape`` elements through the raw pointer."""
+    if not isinstance(t, torch.Tensor):
+        raise InvalidArgumentError(f"{name} must be a torch.Tensor, got {type(t).__name__}")
+    if tuple(t.shape) != tuple(shape) or t.dtype != dtype or not t.is_contiguous() or t.device != device:
+        raise InvalidArgumentError(
+            f"{name} must be a contiguous {dtype} tensor of shape {tuple(shape)} on {device}, got "
+            f"{t.dtype} {tuple(t.shape)} on {t.device}{'' if t.is_contiguous() else ' (non-contiguous)'}")
+
+
 _renderers: dict = {}
 
 
@@ -359,12 +382,45 @@ def render_frame(scene, cam: CameraPose, cfg: EngineConfig, *, record_contributi
     ``"torch"`` leaves image and counts on the device (float32 / int32).
     """
     t0 = time.perf_counter()
-    if record_contributions:
-        raise InvalidArgumentError("record_contributions (dense P x H*W weights) is not supported on the GPU path")
     dscene = _as_device_scene(scene)
     renderer = get_renderer(dscene.device)
-    return _finish(renderer, lambda **kw: renderer.render_checked(dscene, cam, cfg, **kw),
-                   lambda **kw: renderer.render_to_host(dscene, cam, cfg, **kw), output, t0, {})
+    res = _finish(renderer, lambda **kw: renderer.render_checked(dscene, cam, cfg, **kw),
+                  lambda **kw: renderer.render_to_host(dscene, cam, cfg, **kw), output, t0, {})
+    if record_contributions:
+        matrix, ids = contributions(renderer, dscene, cam, cfg, res.device_stats)
+        res.contributions = matrix if output == "torch" else matrix.cpu().numpy()
+        res.contribution_ids = ids
+        res.stats.wall_ms = (time.perf_counter() - t0) * 1000.0
+    return res
+
+
+CONTRIB_MAX_BYTES = 4 << 30  # cap of the dense P x H*W fp64 contribution matrix (record_contributions)
+
+
+def contributions(renderer: FrameRenderer, scene: DeviceScene, cam: CameraPose, cfg: EngineConfig,
+                  host_stats: np.ndarray) -> tuple[torch.Tensor, np.ndarray]:
+    """Dense per-splat, per-pixel blend weights T * alpha of the frame last
+    rendered by ``renderer`` (render.py:186-193, 226-233): a (P, H*W) float64
+    device tensor, row r = plan ref r (``plan.ids`` order), computed on the
+    GPU with the reference schedule (seele_contributions), and the plan ids.
+    Raises InvalidArgumentError when the matrix would exceed CONTRIB_MAX_BYTES
+    (the reference allocates it in host memory; this path serves parity-size
+    frames -- trajectory-scale harvests use clusters.harvest_top_contributors)."""
+    n_ws = int(host_stats[_native.STAT_WORKING_SET])
+    plan = renderer.export_plan(scene, cam, host_stats)
+    p, n_pix = len(plan.ids), int(cam.width) * int(cam.height)
+    if p * n_pix * 8 > CONTRIB_MAX_BYTES:
+        raise InvalidArgumentError(f"record_contributions needs a {p} x {n_pix} float64 matrix "
+                                   f"({p * n_pix * 8 / 2**30:.1f} GiB > {CONTRIB_MAX_BYTES / 2**30:.0f} GiB cap)")
+    d = renderer.device
+    out = torch.zeros((p, n_pix), dtype=torch.float64, device=d)
+    row_of_pos = torch.empty(max(n_ws, 1), dtype=torch.int32, device=d)
+    camc = _native.camera_struct(cam)
+    cfgc = _native.config_struct(cfg)
+    _native.check(renderer.lib.seele_contributions(
+        renderer.workspace.data_ptr(), renderer.n_max, renderer.pair_capacity, ctypes.byref(camc),
+        ctypes.byref(cfgc), n_ws, row_of_pos.data_ptr(), out.data_ptr(), torch.cuda.current_stream(d).cuda_stream))
+    return out, plan.ids
 
 
 def _finish(renderer, checked, to_host, output: str, t0: float, kw: dict) -> RenderResult:

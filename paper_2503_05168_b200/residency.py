@@ -143,6 +143,9 @@ class ResidentRenderer:
         if not cams:
             return
         w, h = int(cams[0].width), int(cams[0].height)
+        for i, c in enumerate(cams):  # every slot's outputs and workspace are sized once, from the first camera
+            if (int(c.width), int(c.height)) != (w, h):
+                raise InvalidArgumentError(f"camera {i} is {c.width}x{c.height}, the trajectory is {w}x{h}")
         key = (w, h, int(depth), pair_capacity)
         tr = getattr(self, "_trajectory", None)
         if tr is None or tr[0] != key:  # workspaces and pinned buffers are kept across calls

@@ -90,9 +90,10 @@ class StreamingRenderer:
         ch = handle.chunks
         self.shared_count = int(ch[0, 1])
         self.slot_size = int(ch[1:, 1].max()) if len(ch) > 1 else 0
-        # resident clusters at most: the kept set (lru capacity / current + predicted) plus this frame's loads
+        # resident clusters at most: the kept set (lru capacity / current + predicted) plus, before eviction
+        # runs, one frame's stalls (1 + m), the prefetches still in flight (1 + m) and the new ones (1 + m)
         keep = max(self.lru_capacity, 2 * (1 + self.m)) if evict_policy == "lru" else 2 * (1 + self.m)
-        self.n_slots = handle.num_clusters if not evict else min(handle.num_clusters, keep + 2 * (1 + self.m))
+        self.n_slots = handle.num_clusters if not evict else min(handle.num_clusters, keep + 3 * (1 + self.m))
         cap = self.shared_count + self.n_slots * self.slot_size
         self.host_planes = torch.from_numpy(np.ascontiguousarray(handle.planes)).pin_memory()
         self.host_ids = torch.from_numpy(np.ascontiguousarray(handle.ids)).pin_memory()
