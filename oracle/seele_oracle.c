@@ -139,7 +139,12 @@ void oracle_preprocess(int64_t n, const double *pos, const double *log_scale, co
         const double *p = pos + 3 * i;
         double d[3] = {p[0] - cam->position[0], p[1] - cam->position[1], p[2] - cam->position[2]};
         double t[3];
-        for (int r = 0; r < 3; r++) t[r] = w2v[r][0] * d[0] + w2v[r][1] * d[1] + w2v[r][2] * d[2];
+        /* world_to_view @ (position - cam.position) (preprocess.py:100): numpy hands this 3x3 @ 3 product
+         * to OpenBLAS dgemv, whose kernel on this container accumulates with fused multiply-adds left to
+         * right -- t[r] = fma(w[r][2], d[2], fma(w[r][1], d[1], w[r][0] d[0])) matches numpy bit for bit
+         * on every tested splat (tools/blas_order.py), the plain sum does not for ~25 % of them.  The depth
+         * feeds the sort, where one ulp decides near-ties (fp32 container positions make them common). */
+        for (int r = 0; r < 3; r++) t[r] = fma(w2v[r][2], d[2], fma(w2v[r][1], d[1], w2v[r][0] * d[0]));
         double z = t[2];
         rect[4 * i + 0] = 1;
         rect[4 * i + 1] = 0;

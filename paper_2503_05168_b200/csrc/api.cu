@@ -138,8 +138,7 @@ Workspace carve_workspace(void *base, long long n_max, long long cap, int width,
     w.look_tiles_d = (n + kSortTile - 1) / kSortTile;
     // the column pass has at most one partial chunk per row beyond cap / tile
     w.look_tiles_p = (cap + kSortTile - 1) / kSortTile + kMaxTileAxis + 1;
-    w.look = c.take<unsigned long long>(kDepthPasses * w.look_tiles_d * 256 + w.look_tiles_d +
-                                        2 * w.look_tiles_p * 256);
+    w.look = c.take<unsigned long long>(w.look_tiles_d + 2 * w.look_tiles_p * 256 + kDepthBuckets / kDepthScanItems);
     w.status = c.take<uint8_t>(n);
     w.depth = c.take<double>(n);
     w.rect = c.take<short4>(n);
@@ -147,9 +146,11 @@ Workspace carve_workspace(void *base, long long n_max, long long cap, int width,
     w.conic_op = c.take<double4>(n);
     w.rec = c.take<RasterRec>(n);
     w.bbox = c.take<float4>(n);
-    w.dkey[0] = c.take<uint32_t>(n);
-    w.dkey[1] = c.take<uint32_t>(n);
-    w.long_runs = c.take<uint2>(kLongRunsMax);
+    w.bhist = c.take<uint32_t>(kDepthBuckets + 1);
+    w.bidx = c.take<uint32_t>(n);
+    w.brec[0] = c.take<uint4>(n);
+    w.brec[1] = c.take<uint4>(n);
+    w.gfirst = c.take<uint32_t>(n / kDepthGroup + 2);
     w.dval[0] = c.take<uint32_t>(n);
     w.dval[1] = c.take<uint32_t>(n);
     w.drect[0] = c.take<uint32_t>(n);
@@ -161,12 +162,10 @@ Workspace carve_workspace(void *base, long long n_max, long long cap, int width,
     w.pfinal = c.take<uint32_t>(cap);
     w.ranges = c.take<uint2>(tiles);
     w.tile_order = c.take<uint32_t>(tiles);
-    w.dhist = c.take<uint32_t>(kDepthPasses * 256);
     w.row_start = c.take<uint32_t>(kMaxTileAxis + 2);
     w.chunk_first = c.take<uint32_t>(kMaxTileAxis + 2);
     w.tile_diff = c.take<int32_t>((long long)(tiles_x + 1) * (tiles_y + 1));
     w.row_diff = c.take<int32_t>(tiles_y + 1);
-    w.minmax = c.take<unsigned long long>(2);
     w.counters = c.take<uint32_t>(CNT_COUNT);
     w.pairs64 = c.take<unsigned long long>(1);
     w.bytes = c.off;
@@ -296,7 +295,7 @@ int seele_render_split(const seele_scene *scene, const int64_t *ranges_dev, int3
     prof_mark(0, st);
     launch_preprocess(sk, ranges_dev, n_ranges, ck, cf, ws, stats_dev, pre_grid, st);
     prof_mark(1, st);
-    launch_depth_sort(ws, n_max, stats_dev, st);
+    launch_depth_sort(ws, ck, n_max, stats_dev, st);
     prof_mark(2, st);
     launch_binning(ws, n_max, pair_capacity, ck, stats_dev, st);
     prof_mark(3, st);

@@ -1,25 +1,22 @@
-// Depth ordering, tile binning and the tile sort on sm_100a.  Every size is
-// read from device memory, so a frame needs no host round trip:
+// Tile binning and the tile sort on sm_100a, over the binned splats in exact
+// (depth, position) order (depth.cu).  Every size is read from device
+// memory, so a frame needs no host round trip:
 //
-//   depth sort   stable LSD radix sort of all assembled splats on
-//                key = fp64 depth bits - min binned bits (binned splats;
-//                the others get key = range + 1 and sort last), value =
-//                assembled position.  Input in assembled order, so ties
-//                break by position = the reference's (depth, gaussian_ref)
-//                order (sorting.py:43, render.py:108).  One up-front
-//                histogram kernel + one onesweep kernel per 8-bit digit;
-//                passes beyond the key's significant bits exit at once.
-//   pair scan    exclusive scan of tile counts in depth-rank order
-//                (decoupled look-back), first rank of every 4096-pair
-//                emission tile, per-axis tile histograms (difference arrays)
-//                from which the last CTA derives every tile-sort digit base.
-//   emission     bin_tiles (preprocess.py:159-189) in depth-rank order, key
-//                = ty << xb | tx (sorted key = linear tile id), fused with
-//                the first stable radix pass of the tile sort.
-//   tile sort    remaining passes; the last one writes only the splat
-//                position of each pair (final order = sort_intersections,
-//                sorting.py:32-54) and the per-tile [start, end) ranges
-//                (sorting.py:46-53) by atomicMin / atomicMax of its runs.
+//   pair scan    k_pair_scan: exclusive scan of each splat's row-entry count
+//                in depth order (decoupled look-back), first rank of every
+//                4096-entry row-pass tile, and the 2D / 1D difference arrays
+//                of per-tile pair counts and per-row entry counts; the last
+//                CTA turns them into the tile ranges (sorting.py:46-53), the
+//                raster launch order, the row bases and the column-pass chunks.
+//   row pass     k_row_pass: bin_tiles (preprocess.py:159-189) of each splat
+//                as row entries (one per covered tile row, split into <= 3
+//                columns), stably grouped by tile row: one onesweep pass whose
+//                digit is the row.
+//   column pass  k_col_pass: every row chunk expands its entries into pairs,
+//                each written straight to its final slot (sorting.py:32-54
+//                order) = tile range start + pairs of that column in earlier
+//                chunks (look-back along the row) + earlier entries of the
+//                chunk covering the column.
 #include "onesweep.cuh"
 
 namespace seele {
@@ -41,356 +38,23 @@ __device__ __forceinline__ unsigned long long gtime() {
 
 namespace {
 
-// Depth-sort key: the fp64 depth quantised to 24 bits over [min, max] of the
-// binned depths.  Every IEEE operation is monotone, so key(d) is monotone
-// non-decreasing in d: sorting by key orders by depth except inside runs of
-// equal keys, which the fix-up re-sorts by (fp64 depth, position).
-struct DepthKey {
-    double lo, scale;
-};
-
-__device__ __forceinline__ DepthKey depth_key(const Workspace &ws) {
-    DepthKey k;
-    const unsigned long long lo = ws.minmax[0], hi = ws.minmax[1];
-    k.lo = 0.0;
-    k.scale = 0.0;
-    if (lo <= hi) {
-        k.lo = __longlong_as_double((long long)lo);
-        const double span = __longlong_as_double((long long)hi) - k.lo;
-        k.scale = span > 0.0 ? 16777214.0 / span : 0.0;
-    }
-    return k;
-}
-
-__device__ __forceinline__ uint32_t depth_quant(const DepthKey &k, short4 rect, double d) {
-    if (rect.x > rect.y) return 0xffffffu;  // not binned (empty tile rect): after every binned splat
-    const double q = floor((d - k.lo) * k.scale);
-    return q < 16777214.0 ? (uint32_t)q : 0xfffffeu;
-}
-
 // ---- frame start ---------------------------------------------------------------
 
 __global__ void k_frame_begin(Workspace ws, int64_t *stats, int n_diff, int tiles_y) {
     const int tid = blockIdx.x * blockDim.x + threadIdx.x, stride = gridDim.x * blockDim.x;
     if (tid == 0) {
         *ws.epoch += 1u;
-        ws.minmax[0] = ~0ull;
-        ws.minmax[1] = 0ull;
         *ws.pairs64 = 0ull;
     }
     if (tid < SEELE_STAT_COUNT) stats[tid] = 0;
     if (tid < CNT_COUNT) ws.counters[tid] = 0u;
-    for (int i = tid; i < kDepthPasses * 256; i += stride) ws.dhist[i] = 0u;
+    for (int i = tid; i < kDepthBuckets / 4; i += stride) reinterpret_cast<uint4 *>(ws.bhist)[i] = make_uint4(0, 0, 0, 0);
     for (int i = tid; i < n_diff; i += stride) ws.tile_diff[i] = 0;
     for (int i = tid; i <= tiles_y; i += stride) ws.row_diff[i] = 0;
 }
 
-// ---- depth sort ------------------------------------------------------------------
-
-__global__ void __launch_bounds__(256) k_depth_hist(Workspace ws) {
-    __shared__ uint32_t h[kDepthPasses][256];
-    __shared__ bool s_last;
-    const int tid = threadIdx.x;
-    for (int i = tid; i < kDepthPasses * 256; i += 256) (&h[0][0])[i] = 0u;
-    __syncthreads();
-    const DepthKey k = depth_key(ws);
-    const uint32_t n = ws.counters[CNT_WS];
-    constexpr int U = 8;
-    for (uint32_t i0 = blockIdx.x * 256 * U + tid; i0 < n; i0 += gridDim.x * 256 * U) {
-        short4 tl[U];
-        double d[U];
-#pragma unroll
-        for (int u = 0; u < U; u++) {
-            const uint32_t i = min(i0 + u * 256, n - 1);
-            tl[u] = ws.rect[i];
-            d[u] = ws.depth[i];
-        }
-#pragma unroll
-        for (int u = 0; u < U; u++) {
-            if (i0 + u * 256 >= n) break;
-            if (tl[u].x > tl[u].y) continue;  // not binned: dropped by the sort
-            const uint32_t key = depth_quant(k, tl[u], d[u]);
-#pragma unroll
-            for (int p = 0; p < kDepthPasses; p++) atomicAdd(&h[p][(key >> (8 * p)) & 0xffu], 1u);
-        }
-    }
-    __syncthreads();
-#pragma unroll
-    for (int p = 0; p < kDepthPasses; p++)
-        if (h[p][tid]) atomicAdd(&ws.dhist[p * 256 + tid], h[p][tid]);
-    __threadfence();
-    __syncthreads();
-    if (tid == 0) s_last = atomicAdd(&ws.counters[CNT_DONE_HIST], 1u) == gridDim.x - 1;
-    __syncthreads();
-    if (!s_last) return;
-    __threadfence();
-    // last CTA: digit totals -> exclusive digit bases (256 threads, one digit each)
-    for (int p = 0; p < kDepthPasses; p++) {
-        const uint32_t v = *(volatile uint32_t *)&ws.dhist[p * 256 + tid];
-        __shared__ uint32_t s_v[256];
-        s_v[tid] = v;
-        __syncthreads();
-        if (tid == 0) {
-            uint32_t run = 0;
-            for (int d = 0; d < 256; d++) {
-                const uint32_t c = s_v[d];
-                s_v[d] = run;
-                run += c;
-            }
-        }
-        __syncthreads();
-        ws.dhist[p * 256 + tid] = s_v[tid];
-        __syncthreads();
-    }
-}
-
-// One 8-bit pass of the depth sort.  Pass 0 builds its keys from the
-// preprocess outputs (value = assembled position).
-#ifndef SEELE_DEPTH_MINB
-#define SEELE_DEPTH_MINB 2
-#endif
-#ifndef SEELE_DEPTH_IPT
-#define SEELE_DEPTH_IPT 8
-#endif
-constexpr int DIPT = SEELE_DEPTH_IPT;  // items per thread of the depth passes
-constexpr int DTILE = NT * DIPT;
-__global__ void __launch_bounds__(NT, SEELE_DEPTH_MINB) k_depth_pass(Workspace ws, int pass) {
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    // every extern __shared__ array of this file aliases one symbol whose alignment may be 4: align here
-    unsigned char *smem = reinterpret_cast<unsigned char *>((reinterpret_cast<uintptr_t>(smem_raw) + 15) & ~uintptr_t(15));
-    RankSmem &rs = *reinterpret_cast<RankSmem *>(smem);
-    uint32_t *skey = reinterpret_cast<uint32_t *>(smem + sizeof(RankSmem));
-    uint32_t *sval = skey + DTILE;
-    uint32_t *srect = sval + DTILE;
-    __shared__ uint32_t s_base[RADIX];
-    for (;;) {  // persistent when the grid is smaller than the tile count (tickets in order)
-#ifdef SEELE_SORT_TRACE
-    const unsigned long long t_enter = gtime();
-#endif
-    const uint32_t t = take_ticket(&ws.counters[CNT_TICKET + kLookDepth + pass]);
-    // pass 0 reads every assembled splat and keeps the binned ones; later passes sort only those
-    const uint32_t n = pass == 0 ? ws.counters[CNT_WS] : (uint32_t)ws.counters_binned();
-    const uint32_t t0 = t * DTILE;
-    if (t0 >= n) return;
-#ifdef SEELE_SORT_TRACE
-    if (threadIdx.x == 0 && t < 4096) g_trace[pass][t][0] = t_enter;
-#endif
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int shift = 8 * pass;
-    uint32_t key[DIPT], val[DIPT], rcv[DIPT], dig[DIPT], pos[DIPT];
-    const uint32_t ib = t0 + warp * 32 * DIPT + lane;
-    if (pass == 0) {
-        const DepthKey dk = depth_key(ws);
-        short4 tl[DIPT];
-        double d[DIPT];
-#pragma unroll
-        for (int r = 0; r < DIPT; r++) {
-            const uint32_t i = min(ib + r * 32, n - 1);
-            tl[r] = ws.rect[i];
-            d[r] = ws.depth[i];
-        }
-#pragma unroll
-        for (int r = 0; r < DIPT; r++) {
-            key[r] = depth_quant(dk, tl[r], d[r]);
-            val[r] = ib + r * 32;
-            rcv[r] = (uint32_t)(tl[r].x & 0xff) | ((uint32_t)(tl[r].y & 0xff) << 8) | ((uint32_t)(tl[r].z & 0xff) << 16) |
-                     ((uint32_t)(tl[r].w & 0xff) << 24);
-        }
-    } else {
-        const uint32_t *kin = ws.dkey[(pass + 1) & 1];
-        const uint32_t *vin = ws.dval[(pass + 1) & 1];
-        const uint32_t *rin = ws.drect[(pass + 1) & 1];
-#pragma unroll
-        for (int r = 0; r < DIPT; r++) {
-            const uint32_t i = min(ib + r * 32, n - 1);
-            key[r] = kin[i];
-            val[r] = vin[i];
-            rcv[r] = rin[i];
-        }
-    }
-#pragma unroll
-    for (int r = 0; r < DIPT; r++)
-        dig[r] = ib + r * 32 < n && key[r] != 0xffffffu ? (key[r] >> shift) & 0xffu : NO_DIGIT;
-#ifdef SEELE_SORT_TRACE
-    __syncthreads();
-    TRACE(pass, t, 1)
-#endif
-    uint32_t count;
-#ifndef SEELE_DEPTH_BALLOT
-#define SEELE_DEPTH_BALLOT 1
-#endif
-    block_rank<SEELE_DEPTH_BALLOT, DIPT>(dig, pos, rs, count);
-    TRACE(pass, t, 2)
-    if (tid < RADIX) {
-        const uint32_t ex = lookback(ws.look_region(kLookDepth + pass) + tid, RADIX, t,
-                                     *ws.epoch * 16u + (uint32_t)(kLookDepth + pass), count, t == 0);
-        s_base[tid] = ws.dhist[pass * 256 + tid] + ex - rs.start[tid];
-    }
-#ifdef SEELE_SORT_TRACE
-    __syncthreads();
-    TRACE(pass, t, 3)
-#endif
-#pragma unroll
-    for (int r = 0; r < DIPT; r++) {
-        if (dig[r] == NO_DIGIT) continue;
-        skey[pos[r]] = key[r];
-        sval[pos[r]] = val[r];
-        srect[pos[r]] = rcv[r];
-    }
-    __syncthreads();
-    const int nv = (int)rs.total;  // ranked (binned) items of this tile
-    uint32_t *kout = ws.dkey[pass & 1];
-    uint32_t *vout = ws.dval[pass & 1];
-    uint32_t *rout = ws.drect[pass & 1];
-    for (int i = tid; i < nv; i += NT) {
-        const uint32_t k = skey[i];
-        const uint32_t dst = s_base[(k >> shift) & 0xffu] + (uint32_t)i;
-        kout[dst] = k;
-        vout[dst] = sval[i];
-        rout[dst] = srect[i];
-    }
-#ifdef SEELE_SORT_TRACE
-    __syncthreads();
-    TRACE(pass, t, 4)
-#endif
-    __syncthreads();  // the staging arrays are reused by the next ticket
-    }
-}
-
 __device__ __forceinline__ short4 unpack_rect(uint32_t v) {
     return make_short4((short)(v & 0xff), (short)((v >> 8) & 0xff), (short)((v >> 16) & 0xff), (short)(v >> 24));
-}
-__device__ __forceinline__ uint32_t pack_rect(short4 r) {
-    return (uint32_t)(r.x & 0xff) | ((uint32_t)(r.y & 0xff) << 8) | ((uint32_t)(r.z & 0xff) << 16) |
-           ((uint32_t)(r.w & 0xff) << 24);
-}
-
-// (fp64 depth, position) order inside one run of equal quantised keys.
-__device__ __forceinline__ bool depth_less(double da, uint32_t pa, double db, uint32_t pb) {
-    return da < db || (da == db && pa < pb);
-}
-
-// Exact order inside runs of equal 32-bit keys among the binned splats:
-// short runs by the thread at the run start (insertion sort, already sorted
-// by position), runs longer than 32 are queued for k_depth_fix_long.
-// Exact order inside runs of equal quantised keys, in place: a run's members
-// are ranked among themselves in (fp64 depth, position) order -- independent
-// loads, no serial chain -- and written to s + rank after a CTA barrier.  A
-// CTA owns the runs that START in its 256 positions; its 32 extra threads
-// cover the tail of a run that crosses into the next CTA's range (which skips
-// runs started before it), so every run is read and written by one CTA only.
-// Positions outside runs are untouched.  Runs longer than 32 are queued by
-// their first position for k_depth_fix_long.
-constexpr int kFixOwn = 256, kFixHalo = 32, kFixThreads = kFixOwn + kFixHalo;
-
-__global__ void __launch_bounds__(kFixThreads) k_depth_fixup(Workspace ws, const int64_t *stats) {
-    __shared__ uint32_t sk[kFixHalo + kFixOwn + 2 * kFixHalo];  // keys [b0 - 32, b0 + 256 + 64)
-    const uint32_t n = (uint32_t)stats[SEELE_STAT_BINNED];
-    const uint32_t *key = ws.dkey[kDepthFinal];
-    uint32_t *val = ws.dval[kDepthFinal];
-    uint32_t *rs = ws.drect[kDepthFinal];
-    const int tid = threadIdx.x;
-    constexpr int kWin = kFixHalo + kFixOwn + 2 * kFixHalo;
-    // (a grid-stride loop: the grid may be smaller than the block count)
-    for (long long b0 = (long long)blockIdx.x * kFixOwn; b0 < n; b0 += (long long)gridDim.x * kFixOwn) {
-    for (int k = tid; k < kWin; k += kFixThreads) {
-        const long long g = b0 - kFixHalo + k;
-        sk[k] = (g >= 0 && g < (long long)n) ? key[g] : 0xffffffffu;  // keys are 24-bit: never equal
-    }
-    __syncthreads();
-    const long long i = b0 + tid;
-    const int c = tid + kFixHalo;
-    long long out = -1;
-    uint32_t p = 0, rr = 0;
-    if (i < n) {
-        const uint32_t k = sk[c];
-        if (sk[c - 1] == k || sk[c + 1] == k) {  // in a run
-            int s = c, e = c + 1;
-            while (s > 0 && sk[s - 1] == k) s--;
-            while (e < kWin && sk[e] == k) e++;
-            // owned: the run starts in [b0, b0 + 256) (s == 0 means it starts before the window: not ours)
-            if (s >= kFixHalo && s < kFixHalo + kFixOwn) {
-                if (e == kWin || e - s > 32) {  // long run
-                    if (c == s) {
-                        uint32_t end = (uint32_t)i + 1;
-                        while (end < n && key[end] == k) end++;
-                        const uint32_t slot = atomicAdd(&ws.counters[CNT_LONG_RUNS], 1u);
-                        if (slot < kLongRunsMax) ws.long_runs[slot] = make_uint2((uint32_t)i, end - (uint32_t)i);
-                    }
-                } else {
-                    p = val[i];
-                    rr = rs[i];
-                    const double d = ws.depth[p];
-                    uint32_t rank = 0;
-                    for (int q = s; q < e; q++) {
-                        if (q == c) continue;
-                        const uint32_t pq = val[b0 - kFixHalo + q];
-                        rank += depth_less(ws.depth[pq], pq, d, p);
-                    }
-                    out = b0 - kFixHalo + s + rank;
-                }
-            }
-        }
-    }
-    __syncthreads();  // every member of every owned run has been read
-    if (out >= 0) {
-        val[out] = p;
-        rs[out] = rr;
-    }
-    __syncthreads();  // the key window is reloaded
-    }
-}
-
-// Long equal-key runs (rare: > 32 splats within one quantisation step): one
-// CTA per run, each item's rank = number of run items before it in
-// (depth, position) order, read from the last pass's buffer and written to
-// its slot, in place.  Runs up to kFixSmem items are staged in shared
-// memory; longer ones are ranked from global memory through the spare buffer.
-constexpr int kFixSmem = 4096;
-
-__global__ void __launch_bounds__(512) k_depth_fix_long(Workspace ws) {
-    __shared__ double s_d[kFixSmem];
-    __shared__ uint32_t s_p[kFixSmem];
-    const uint32_t nq = min(ws.counters[CNT_LONG_RUNS], (uint32_t)kLongRunsMax);
-    uint32_t *val = ws.dval[kDepthFinal];
-    uint32_t *spare = ws.dval[kDepthFinal ^ 1];
-    for (uint32_t q = blockIdx.x; q < nq; q += gridDim.x) {
-        const uint2 run = ws.long_runs[q];
-        const uint32_t s = run.x, m = run.y;
-        if (m <= (uint32_t)kFixSmem) {
-            for (uint32_t j = threadIdx.x; j < m; j += blockDim.x) {
-                s_p[j] = val[s + j];
-                s_d[j] = ws.depth[s_p[j]];
-            }
-            __syncthreads();
-            for (uint32_t j = threadIdx.x; j < m; j += blockDim.x) {
-                const double dj = s_d[j];
-                const uint32_t pj = s_p[j];
-                uint32_t r = 0;
-                for (uint32_t k = 0; k < m; k++) r += depth_less(s_d[k], s_p[k], dj, pj);
-                val[s + r] = pj;
-                ws.drect[kDepthFinal][s + r] = pack_rect(ws.rect[pj]);
-            }
-            __syncthreads();
-        } else {  // ranked from global memory into the other ping-pong buffer, then copied back
-            for (uint32_t j = threadIdx.x; j < m; j += blockDim.x) {
-                const uint32_t pj = val[s + j];
-                const double dj = ws.depth[pj];
-                uint32_t r = 0;
-                for (uint32_t k = 0; k < m; k++) {
-                    const uint32_t pk = val[s + k];
-                    r += depth_less(ws.depth[pk], pk, dj, pj);
-                }
-                spare[s + r] = pj;
-            }
-            __syncthreads();
-            for (uint32_t j = threadIdx.x; j < m; j += blockDim.x) {
-                val[s + j] = spare[s + j];
-                ws.drect[kDepthFinal][s + j] = pack_rect(ws.rect[spare[s + j]]);
-            }
-            __syncthreads();
-        }
-    }
 }
 
 // ---- row entries: offsets, tile counts, ranges -------------------------------------
@@ -923,12 +587,6 @@ __global__ void k_fill_pair_tiles(const uint2 *ranges, int n_tiles, int32_t *pai
     }
 }
 
-int key_bits(int n) {
-    int b = 0;
-    while ((1 << b) < n) b++;
-    return b;
-}
-
 template <typename K>
 void set_smem(K kernel, size_t bytes) {
     static bool done = false;  // per instantiation
@@ -944,8 +602,7 @@ long long ceil_div(long long a, long long b) { return (a + b - 1) / b; }
 
 void launch_frame_begin(const Workspace &ws, const CamK &cam, int64_t *stats, cudaStream_t st) {
     const int n_diff = (cam.tiles_x + 1) * (cam.tiles_y + 1);
-    int grid = (n_diff + 255) / 256;
-    grid = grid < 8 ? 8 : (grid > 256 ? 256 : grid);
+    const int grid = 256;  // (the depth histogram alone is 4 MB)
     k_frame_begin<<<grid, 256, 0, st>>>(ws, stats, n_diff, cam.tiles_y);
     note_launches(1);
 }
@@ -959,30 +616,6 @@ static int sm_count_cached() {
         if (sms <= 0) sms = 148;
     }
     return sms;
-}
-
-void launch_depth_sort(const Workspace &ws, long long n_max, int64_t *stats, cudaStream_t st) {
-#ifndef SEELE_HIST_PER_SM
-#define SEELE_HIST_PER_SM 2
-#endif
-    const int hist_grid = (int)std::min<long long>(ceil_div(n_max, 256 * 8), SEELE_HIST_PER_SM * 148);
-    k_depth_hist<<<hist_grid > 0 ? hist_grid : 1, 256, 0, st>>>(ws);
-    const size_t smem = 16 + sizeof(RankSmem) + 3 * sizeof(uint32_t) * DTILE;
-    set_smem(k_depth_pass, smem);
-#ifndef SEELE_DEPTH_CTAS_PER_SM
-#define SEELE_DEPTH_CTAS_PER_SM 2  // persistent at the resident CTAs (0: one CTA per tile)
-#endif
-    int grid = (int)ceil_div(n_max, DTILE);
-    if (SEELE_DEPTH_CTAS_PER_SM > 0) grid = std::min(grid, (int)(SEELE_DEPTH_CTAS_PER_SM * sm_count_cached()));
-    for (int p = 0; p < kDepthPasses; p++) k_depth_pass<<<grid, NT, smem, st>>>(ws, p);
-#ifndef SEELE_FIX_PER_SM
-#define SEELE_FIX_PER_SM 0  // 0: one CTA per 256 positions
-#endif
-    int fix_grid = (int)ceil_div(n_max, kFixOwn);
-    if (SEELE_FIX_PER_SM > 0) fix_grid = std::min(fix_grid, SEELE_FIX_PER_SM * sm_count_cached());
-    k_depth_fixup<<<fix_grid > 0 ? fix_grid : 1, kFixThreads, 0, st>>>(ws, stats);
-    k_depth_fix_long<<<64, 512, 0, st>>>(ws);
-    note_launches(3 + kDepthPasses);
 }
 
 void launch_binning(const Workspace &ws, long long n_max, long long cap, const CamK &cam, int64_t *stats,

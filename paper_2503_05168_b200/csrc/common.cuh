@@ -41,9 +41,7 @@ enum {
     CNT_ENTRIES = 1,      // row entries (one per binned splat and tile row it covers)
     CNT_PAIRS = 2,        // tile pairs (0 on overflow; the u64 count is in stats)
     CNT_OVERFLOW = 3,
-    CNT_LONG_RUNS = 4,    // equal depth-key runs queued for the CTA fix-up
-    CNT_DONE_HIST = 5,    // last-block tickets
-    CNT_DONE_SCAN = 6,
+    CNT_DONE_SCAN = 6,    // last-block ticket of the pair scan
     CNT_CHUNKS = 7,       // row chunks of the column pass
     CNT_TICKET = 8,       // 16 per-pass tile tickets
     CNT_COUNT = 32
@@ -56,14 +54,31 @@ enum {
 #define SEELE_SORT_IPT 8
 #endif
 constexpr int kSortTile = SEELE_SORT_NT * SEELE_SORT_IPT;  // items per onesweep CTA tile (onesweep.cuh TILE)
-constexpr int kDepthPasses = 3;   // 8-bit passes of the 24-bit depth key
-constexpr int kDepthFinal = (kDepthPasses - 1) & 1;  // ping-pong buffer holding the sorted order (ties fixed in place)
-constexpr int kLongRunsMax = 4096; // equal-key runs longer than this many go to the CTA fix-up
 constexpr int kMaxTileAxis = 256;  // tiles per image axis (row / column digits fit one pass)
-constexpr int kLookDepth = 0;     // look-back regions (pass ids)
-constexpr int kLookScan = 3;
-constexpr int kLookRows = 4;
-constexpr int kLookCols = 5;
+constexpr int kLookScan = 0;       // look-back regions (pass ids)
+constexpr int kLookRows = 1;
+constexpr int kLookCols = 2;
+constexpr int kLookBuckets = 3;
+
+// Depth order (depth.cu): buckets of the order-preserving fp64 bit pattern of
+// z above the near plane, 2^(52 - kDepthShift) = 65,536 per binade over 16
+// binades (deeper splats share the last bucket); groups of ~kDepthGroup
+// items are sorted exactly by (depth, position) by one CTA each.
+constexpr int kDepthBuckets = 1 << 20;
+constexpr int kDepthShift = 36;
+constexpr int kDepthScanItems = 16384;  // buckets per CTA of the offset scan
+constexpr int kDepthGroup = 1024;
+constexpr int kDepthSmem = 2048;  // items a sort CTA holds in shared memory
+constexpr int kDepthFinal = 0;    // dval / drect buffer holding the sorted order
+
+__device__ __forceinline__ unsigned long long depth_order_key(double z) {
+    const unsigned long long b = (unsigned long long)__double_as_longlong(z);
+    return (b >> 63) ? ~b : (b | 0x8000000000000000ull);  // monotone in z over all finite doubles
+}
+__device__ __forceinline__ uint32_t depth_bucket_of_key(unsigned long long key, unsigned long long base) {
+    const unsigned long long q = key > base ? (key - base) >> kDepthShift : 0ull;
+    return q < (unsigned long long)(kDepthBuckets - 1) ? (uint32_t)q : (uint32_t)(kDepthBuckets - 1);
+}
 
 // FAST raster record of one splat (raster_fast.cu), written by preprocess.
 // q' = q log2(e) / 2, so alpha = o 2^-q'; one 64-byte line, staged into
@@ -86,12 +101,16 @@ struct Workspace {
     double4 *conic_op;   // (a, b, c, opacity)
     RasterRec *rec;      // FAST raster records (also the colour of the exact engine)
     float4 *bbox;        // (x_min, x_max, y_min, y_max) of {q' < q_up} in pixel coordinates
-    // depth sort (ping-pong): key = depth quantised monotonically to 24 bits,
-    // value = assembled position; the sorted order ends in dkey/dval[kDepthFinal]
-    uint32_t *dkey[2];
+    // depth order (depth.cu): bucket counts (K1) -> exclusive offsets, bhist[kDepthBuckets] = binned; each
+    // binned splat's index inside its bucket (K1's atomic); bucket-order records (order key lo / hi, position,
+    // packed tile rect x0 | x1 << 8 | y0 << 16 | y1 << 24) in brec[0] (brec[1]: merge buffer of large groups);
+    // first bucket of each sort group; the sorted order in dval[0] / drect[0] (dval[1] / drect[1]: unused)
+    uint32_t *bhist;     // [kDepthBuckets + 1]
+    uint32_t *bidx;      // [n_max]
+    uint4 *brec[2];      // [n_max]
+    uint32_t *gfirst;    // [n_max / kDepthGroup + 2]
     uint32_t *dval[2];
-    uint32_t *drect[2];  // tile rect carried with each item: x0 | x1 << 8 | y0 << 16 | y1 << 24
-    uint2 *long_runs;    // [kLongRunsMax] (start, length) of long equal-key runs
+    uint32_t *drect[2];
     // first row entry of each depth-ranked binned splat (+ sentinel) and first
     // rank of each 4096-entry tile of the row pass
     uint32_t *poff;
@@ -106,12 +125,10 @@ struct Workspace {
     // scratch
     unsigned long long *look;  // epoch-tagged look-back status words
     long long look_tiles_d, look_tiles_p;  // tiles per depth / pair pass region
-    uint32_t *dhist;     // [kDepthPasses][256] digit totals -> exclusive offsets
     uint32_t *row_start; // [kMaxTileAxis + 1] first entry of each tile row
     uint32_t *chunk_first;  // [kMaxTileAxis + 1] first column-pass chunk of each row
     int32_t *tile_diff;  // [(tiles_y + 1) x (tiles_x + 1)] 2D difference array of tile counts
     int32_t *row_diff;   // [tiles_y + 1] entries per row (difference array)
-    unsigned long long *minmax;  // min / max fp64 bits of binned depths
     uint32_t *counters;  // CNT_COUNT
     uint32_t *epoch;     // frame epoch (never cleared)
     unsigned long long *pairs64;  // total tile pairs (u64)
@@ -121,10 +138,9 @@ struct Workspace {
     __device__ __forceinline__ long long counters_binned() const { return stats_ptr[SEELE_STAT_BINNED]; }
 
     __device__ __forceinline__ unsigned long long *look_region(int pass) const {
-        if (pass < kLookScan) return look + (size_t)pass * look_tiles_d * 256;
-        if (pass == kLookScan) return look + (size_t)kDepthPasses * look_tiles_d * 256;
-        return look + (size_t)kDepthPasses * look_tiles_d * 256 + look_tiles_d +
-               (size_t)(pass - kLookRows) * look_tiles_p * 256;
+        if (pass == kLookScan) return look;
+        if (pass == kLookBuckets) return look + look_tiles_d + 2 * (size_t)look_tiles_p * 256;
+        return look + look_tiles_d + (size_t)(pass - kLookRows) * look_tiles_p * 256;
     }
 };
 
@@ -139,8 +155,8 @@ void launch_select(const CamK &cam, const double *centroids, int n, int m, doubl
                    int64_t *ranges_out, cudaStream_t st);
 // frame start: counters, stats, epoch, range / histogram init (binning.cu)
 void launch_frame_begin(const Workspace &ws, const CamK &cam, int64_t *stats, cudaStream_t st);
-// stable depth sort of the assembled splats (binned first, by (depth, position)).
-void launch_depth_sort(const Workspace &ws, long long n_max, int64_t *stats, cudaStream_t st);
+// exact (depth, position) order of the binned splats (depth.cu).
+void launch_depth_sort(const Workspace &ws, const CamK &cam, long long n_max, int64_t *stats, cudaStream_t st);
 // pair offsets, emission + tile sort, ranges; final pair -> position in ws.pfinal.
 void launch_binning(const Workspace &ws, long long n_max, long long cap, const CamK &cam, int64_t *stats,
                     cudaStream_t st);

@@ -209,32 +209,16 @@ __device__ __forceinline__ void write_raster_record(const Workspace &ws, long lo
     ws.bbox[p] = bb;
 }
 
-// Block-level reduction of the per-thread frame counters and of the min / max
-// fp64 bit pattern of binned depths (the depth sort's key range): one atomic
-// per counter per CTA instead of one per warp and iteration.
-__device__ __forceinline__ void flush_block(const Workspace &ws, int64_t *stats, uint32_t (&c)[4],
-                                            unsigned long long kmin, unsigned long long kmax) {
+// Block-level reduction of the per-thread frame counters: one atomic per
+// counter per CTA instead of one per warp and iteration.
+__device__ __forceinline__ void flush_block(int64_t *stats, uint32_t (&c)[4]) {
     __shared__ uint32_t s_c[4];
-    __shared__ unsigned long long s_min, s_max;
     if (threadIdx.x < 4) s_c[threadIdx.x] = 0u;
-    if (threadIdx.x == 0) {
-        s_min = ~0ull;
-        s_max = 0ull;
-    }
     __syncthreads();
 #pragma unroll
     for (int k = 0; k < 4; k++) {
         const uint32_t v = __reduce_add_sync(0xffffffffu, c[k]);
         if ((threadIdx.x & 31) == 0 && v) atomicAdd(&s_c[k], v);
-    }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-        kmin = min(kmin, __shfl_xor_sync(0xffffffffu, kmin, o));
-        kmax = max(kmax, __shfl_xor_sync(0xffffffffu, kmax, o));
-    }
-    if ((threadIdx.x & 31) == 0) {
-        atomicMin(&s_min, kmin);
-        atomicMax(&s_max, kmax);
     }
     __syncthreads();
     if (threadIdx.x == 0) {
@@ -243,10 +227,6 @@ __device__ __forceinline__ void flush_block(const Workspace &ws, int64_t *stats,
         if (s_c[1]) atomicAdd(st + SEELE_STAT_DROPPED_DEGENERATE, (unsigned long long)s_c[1]);
         if (s_c[2]) atomicAdd(st + SEELE_STAT_PROJECTED, (unsigned long long)s_c[2]);
         if (s_c[3]) atomicAdd(st + SEELE_STAT_BINNED, (unsigned long long)s_c[3]);
-        if (s_min <= s_max) {
-            atomicMin(&ws.minmax[0], s_min);
-            atomicMax(&ws.minmax[1], s_max);
-        }
     }
 }
 
@@ -290,11 +270,10 @@ __global__ void __launch_bounds__(kPre, SEELE_PRE_MINB) k_preprocess(SceneK sc, 
     const int sh_planes = cfg.sh_degree >= 3 ? 4 : (cfg.sh_degree == 2 ? 3 : 1);
     const long long stride = (long long)gridDim.x * blockDim.x;
     uint32_t cnt[4] = {0u, 0u, 0u, 0u};
-    unsigned long long kmin = ~0ull, kmax = 0ull;
+    const unsigned long long zbase = depth_order_key(cam.near_clip);
     for (long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x; p < n_ws; p += stride) {
         int status = 3;
         uint32_t n_tiles = 0;
-        unsigned long long zbits = 0ull;
         {
             int r = 0;
             while (r + 1 < n_ranges && s_prefix[r + 1] <= p) r++;
@@ -315,9 +294,12 @@ __global__ void __launch_bounds__(kPre, SEELE_PRE_MINB) k_preprocess(SceneK sc, 
             }
             Splat g;
             load_splat<LAYOUT>(sc, i, sh_planes, g);
-            double d[3] = {g.p[0] - cam.pos[0], g.p[1] - cam.pos[1], g.p[2] - cam.pos[2]};
+            const double d[3] = {__dsub_rn(g.p[0], cam.pos[0]), __dsub_rn(g.p[1], cam.pos[1]), __dsub_rn(g.p[2], cam.pos[2])};
             double t[3];
-            for (int k = 0; k < 3; k++) t[k] = cam.w2v[3 * k] * d[0] + cam.w2v[3 * k + 1] * d[1] + cam.w2v[3 * k + 2] * d[2];
+            // world_to_view @ (p - c) rounded like the reference's BLAS dgemv (fused, left to right:
+            // tools/blas_order.py); the depth decides near-ties of the sort, so it is bit-exact by construction
+            for (int k = 0; k < 3; k++)
+                t[k] = __fma_rn(cam.w2v[3 * k + 2], d[2], __fma_rn(cam.w2v[3 * k + 1], d[1], __dmul_rn(cam.w2v[3 * k], d[0])));
             const double z = t[2];
             short4 rect = make_short4(1, 0, 1, 0);
             if (z <= cam.near_clip) {
@@ -423,7 +405,8 @@ __global__ void __launch_bounds__(kPre, SEELE_PRE_MINB) k_preprocess(SceneK sc, 
                         }
                     }
                     ws.depth[p] = z;
-                    zbits = (unsigned long long)__double_as_longlong(z);
+                    // depth-order bucket (depth.cu) of a binned splat: count it and keep its index in the bucket
+                    if (n_tiles > 0) ws.bidx[p] = atomicAdd(&ws.bhist[depth_bucket_of_key(depth_order_key(z), zbase)], 1u);
                     ws.mean[p] = make_double2(m0, m1);
                     ws.conic_op[p] = make_double4(ca, cb, cc, g.o);
                     write_raster_record(ws, p, m0, m1, ca, cb, cc, g.o, qth, qth_err, col);
@@ -436,13 +419,9 @@ __global__ void __launch_bounds__(kPre, SEELE_PRE_MINB) k_preprocess(SceneK sc, 
         cnt[0] += status == 1;
         cnt[1] += status == 2;
         cnt[2] += status == 0;
-        if (n_tiles > 0) {
-            cnt[3] += 1u;
-            kmin = zbits < kmin ? zbits : kmin;
-            kmax = zbits > kmax ? zbits : kmax;
-        }
+        cnt[3] += n_tiles > 0;
     }
-    flush_block(ws, stats, cnt, kmin, kmax);
+    flush_block(stats, cnt);
 }
 
 // K0: select_clusters (residency.py:38-54) with pose_feature (compiler.py:113-121).
