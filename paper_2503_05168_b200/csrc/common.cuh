@@ -86,7 +86,8 @@ __device__ __forceinline__ uint32_t depth_bucket_of_key(unsigned long long key, 
 struct __align__(16) RasterRec {
     float mxh, mxl, myh, myl;  // mean in pixel coordinates as hi + lo floats
     float l11, l21, l22, o;    // Cholesky factor of the conic in q' units; opacity
-    float q_lo, q_up, e0, e1;  // pass: q' < q_lo; fail: q' >= q_up; alpha relative error <= e0 + e1 q'
+    float q_lo, w_up, e0, e1;  // pass: q' < q_lo; in the bracket (re-decided): 0 <= q' - q_lo <= w_up, else
+                               // fail; alpha relative error <= e0 + e1 q'
     float r, g, b;             // colour
     uint32_t p;                // assembled position (fp64 re-decisions)
 };

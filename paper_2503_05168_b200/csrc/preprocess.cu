@@ -203,8 +203,11 @@ __device__ __forceinline__ void write_raster_record(const Workspace &ws, long lo
     float4 *rec = reinterpret_cast<float4 *>(ws.rec + p);
     rec[0] = make_float4(mxh, (float)(m0 - (double)mxh), myh, (float)(m1 - (double)myh));
     rec[1] = make_float4((float)l11, (float)l21, (float)l22, (float)o);
-    rec[2] = make_float4(rq.x, nextafterf(rq.y, INFINITY), rq.z * (1.0f + 1.0f / 1024.0f),
-                         rq.w * (1.0f + 1.0f / 1024.0f));
+    // (q_lo, w_up): the bracket [q_lo, q_up) as its width rounded upward, so the raster tests it on
+    // d = q' - q_lo alone (0 <= d <= w_up, compared as bit patterns); an empty bracket (o < theta) has w_up = 0
+    const float q_up = nextafterf(rq.y, INFINITY);
+    const float w_up = rq.x == -INFINITY ? 0.0f : __double2float_ru(__dsub_ru((double)q_up, (double)rq.x));
+    rec[2] = make_float4(rq.x, w_up, rq.z * (1.0f + 1.0f / 1024.0f), rq.w * (1.0f + 1.0f / 1024.0f));
     rec[3] = make_float4(col.x, col.y, col.z, __uint_as_float((uint32_t)p));
     ws.bbox[p] = bb;
 }

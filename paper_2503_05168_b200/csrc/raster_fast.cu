@@ -142,11 +142,11 @@ __device__ __forceinline__ bool rect_reaches(float mx, float my, float l11, floa
 // decided from fp64 q against the fp32 bracket (valid a fortiori), with the
 // reference formula inside it.
 __device__ __forceinline__ bool exact_test(double px, double py, const double2 &m, const double4 &co, float q_lo,
-                                           float q_up, double th, double &a) {
+                                           float w_up, double th, double &a) {
     const double dx = px - m.x, dy = py - m.y;
     const double q = fma(co.x * dx, dx, fma(2.0 * co.y * dx, dy, (co.z * dy) * dy));
     const double qp = kQ * q;
-    if (qp >= (double)q_up) return false;
+    if (qp > (double)q_lo + (double)w_up) return false;  // (an empty bracket: q_lo = -inf, w_up = 0)
     if (qp < (double)q_lo) {
         a = fmin(co.w * exp(-0.5 * q), kAlphaClamp);
         return true;
@@ -169,7 +169,7 @@ __device__ __noinline__ double exact_transmittance(const Workspace &ws, const ui
         const uint32_t p = pair_pos[k];
         const double2 m = ws.mean[p];
         const double4 co = ws.conic_op[p];
-        const float4 f = reinterpret_cast<const float4 *>(ws.rec + p)[2];  // (q_lo, q_up, e0, e1)
+        const float4 f = reinterpret_cast<const float4 *>(ws.rec + p)[2];  // (q_lo, w_up, e0, e1)
         double a;
         if (W >= 2 && !exact_test(lx + 0.5, ly + 0.5, m, co, f.x, f.y, th, a)) continue;
         if (!exact_test(px + 0.5, py + 0.5, m, co, f.x, f.y, th, a)) continue;
@@ -243,6 +243,9 @@ __global__ void __launch_bounds__(64, SEELE_RASTER_MINB) k_raster_quad(Workspace
     // CR group leader pixel (rasterize.py:235-246): top-left pixel of the w x w group
     const int lead_x = W == 4 ? ox + 4 * (bx >> 1) : x0, lead_y = W == 4 ? oy + 4 * (by >> 1) : y0;
     uint32_t c_alpha = 0, c_blend = 0, n_redecide = 0, n_tamb = 0, n_skip = 0;
+#ifdef SEELE_RASTER_PROFILE
+    uint32_t pr_rel = 0, pr_nolead = 0, pr_noblend = 0, pr_amb = 0, pr_death = 0;
+#endif
     const uint2 rg = ws.ranges[tile];
 
     const float ry0 = warp ? 8.5f : 0.5f, ry1 = ry0 + 7.0f;  // this warp's pixel-centre rows (tile-relative)
@@ -282,7 +285,7 @@ __global__ void __launch_bounds__(64, SEELE_RASTER_MINB) k_raster_quad(Workspace
                 // (margin terms only need upper bounds: approximate square roots, widened by 1e-4)
                 const float P = 1.0001f * sqrt_approx(fmaf(sv.l11, sv.l11, fmaf(sv.l21, sv.l21, sv.l22 * sv.l22)));
                 const float ep = 1.2e-7f * (fabsf(mx) + fabsf(my) + 32.0f);
-                const float qh = sv.q_up, pe = P * ep;
+                const float qh = __fadd_ru(sv.q_lo, sv.w_up), pe = P * ep;  // top of the alpha bracket
                 const float qm = qh + 2.0f * (qh - sv.q_lo) + 1e-6f * qh + 2.2f * pe * (1.0001f * sqrt_approx(fmaxf(qh, 0.f))) +
                                  1.1f * pe * pe + 1e-6f;
                 rel = rect_reaches(mx, my, sv.l11, sv.l21, sv.l22, qm, 0.5f, 15.5f, ry0, ry1);
@@ -299,16 +302,21 @@ __global__ void __launch_bounds__(64, SEELE_RASTER_MINB) k_raster_quad(Workspace
             const int j = __ffs(mlo) - 1;  // next relevant splat
             mlo &= mlo - 1u;
             const Staged &sg = s_g[j];
+#ifdef SEELE_RASTER_PROFILE
+            pr_rel++;
+#endif
+            const float4 rc3 = make_float4(sg.r, sg.g, sg.b, 0.0f);
             float2 q[2], al[2], d[2], E[2];
             quad_q(sg, lxp, lyp, q);
-            uint32_t amb = 0;
+            const uint32_t wb = fbits(sg.w_up);
+            bool amb = false;  // some pixel with 0 <= q' - q_lo <= w_up (bit patterns: a negative d is huge)
 #pragma unroll
             for (int r = 0; r < 2; r++) {
                 al[r] = __fmul2_rn(f2(sg.o), make_float2(ex2_approx(-q[r].x), ex2_approx(-q[r].y)));
                 d[r] = __fadd2_rn(q[r], f2(-sg.q_lo));  // sign set <=> q' < q_lo: surely passes
-                const float2 u = __fadd2_rn(q[r], f2(-sg.q_up));  // sign set <=> q' <= top of the bracket
                 E[r] = __ffma2_rn(f2(sg.e1), q[r], f2(sg.e0));
-                amb |= (fbits(u.x) & ~fbits(d[r].x)) | (fbits(u.y) & ~fbits(d[r].y));
+                amb |= fbits(d[r].x) <= wb;
+                amb |= fbits(d[r].y) <= wb;
             }
             // alpha = min(o 2^-q', 0.99): the clamp can only bind for o > 0.99 (the error model covers
             // 0.99f vs 0.99 and a clamp of the exact value)
@@ -316,16 +324,18 @@ __global__ void __launch_bounds__(64, SEELE_RASTER_MINB) k_raster_quad(Workspace
 #pragma unroll
                 for (int r = 0; r < 2; r++) al[r] = make_float2(fminf(al[r].x, 0.99f), fminf(al[r].y, 0.99f));
             }
-            if (__any_sync(0xffffffffu, (int)amb < 0)) {
+#ifdef SEELE_RASTER_PROFILE
+            pr_amb += __any_sync(0xffffffffu, amb);
+#endif
+            if (__any_sync(0xffffffffu, amb)) {
                 // inside the bracket: decide with the reference formula in fp64 (rare); needed for live pixels
                 // and for the group leader pixel while its group is live
                 const bool glive = W == 4 ? (lb & gmask) != 0u : qlive;
 #pragma unroll
                 for (int s = 0; s < 4; s++) {
                     const int r = s >> 1;
-                    const float qs = slot(q, s);
                     const bool need = slot(Lf, s) != 0.0f || (W >= 2 && s == 0 && leader_thread && glive);
-                    if (!need || qs < sg.q_lo || qs >= sg.q_up) continue;
+                    if (!need || fbits(slot(d, s)) > wb) continue;
                     const double2 m = ws.mean[sg.p];
                     const double4 co = ws.conic_op[sg.p];
                     const double a64 = alpha64((double)(x0 + (s & 1)) + 0.5, (double)(y0 + r) + 0.5, m.x, m.y, co.x,
@@ -342,6 +352,9 @@ __global__ void __launch_bounds__(64, SEELE_RASTER_MINB) k_raster_quad(Workspace
                 const bool glive = W == 4 ? (lb & gmask) != 0u : qlive;
                 const bool lp = leader_thread && glive && (int)fbits(d[0].x) < 0;
                 const unsigned pb = __ballot_sync(0xffffffffu, lp);
+#ifdef SEELE_RASTER_PROFILE
+                pr_nolead += pb == 0u;
+#endif
                 count_any(c_alpha, pb, bm);
                 // w = 2: the group is the thread's own quad, its leader verdict is lp itself
                 my = W == 2 ? (lp ? ~0u : 0u) : 0u - ((pb >> leader_lane) & 1u);
@@ -353,6 +366,9 @@ __global__ void __launch_bounds__(64, SEELE_RASTER_MINB) k_raster_quad(Workspace
                                    __uint_as_float(sign_and(d[r].y, fbits(Lf[r].y), my)));
             const unsigned bb =
                 __ballot_sync(0xffffffffu, (fbits(m[0].x) | fbits(m[0].y) | fbits(m[1].x) | fbits(m[1].y)) != 0u);
+#ifdef SEELE_RASTER_PROFILE
+            pr_noblend += bb == 0u;
+#endif
             if (bb == 0u) continue;
             count_any(c_blend, bb, bm);
             if (W == 1) count_any(c_alpha, bb, bm);  // each pixel is its own leader
@@ -362,9 +378,9 @@ __global__ void __launch_bounds__(64, SEELE_RASTER_MINB) k_raster_quad(Workspace
                 const float2 am = __fmul2_rn(al[r], m[r]);
                 const float2 t0 = T[r];
                 const float2 wgt = __fmul2_rn(t0, am);  // T alpha, or 0
-                C[r][0] = __ffma2_rn(wgt, f2(sg.r), C[r][0]);
-                C[r][1] = __ffma2_rn(wgt, f2(sg.g), C[r][1]);
-                C[r][2] = __ffma2_rn(wgt, f2(sg.b), C[r][2]);
+                C[r][0] = __ffma2_rn(wgt, f2(rc3.x), C[r][0]);
+                C[r][1] = __ffma2_rn(wgt, f2(rc3.y), C[r][1]);
+                C[r][2] = __ffma2_rn(wgt, f2(rc3.z), C[r][2]);
                 const float2 omm = __ffma2_rn(am, f2(-1.0f), f2(1.0f));  // 1 - alpha, or 1 (exact)
                 // |omm - (1 - alpha_ref)| <= alpha (e0 + e1 q') + 1e-7 (rounding of 1 - alpha and of T omm)
                 const float2 efm = __fmul2_rn(__ffma2_rn(al[r], E[r], f2(1.0e-7f)), m[r]);
@@ -378,6 +394,9 @@ __global__ void __launch_bounds__(64, SEELE_RASTER_MINB) k_raster_quad(Workspace
                 cnt[r] = __fadd2_rn(cnt[r], m[r]);
             }
             if (__any_sync(0xffffffffu, (int)(fbits(y[0].x) | fbits(y[0].y) | fbits(y[1].x) | fbits(y[1].y)) < 0)) {
+#ifdef SEELE_RASTER_PROFILE
+                pr_death++;
+#endif
                 uint32_t ambT = 0;
 #pragma unroll
                 for (int s = 0; s < 4; s++) {
@@ -451,7 +470,19 @@ __global__ void __launch_bounds__(64, SEELE_RASTER_MINB) k_raster_quad(Workspace
     const uint32_t w_live = __reduce_add_sync(0xffffffffu, n_live);
     const uint32_t w_blend = __reduce_add_sync(0xffffffffu, n_blend);
     const uint32_t w_skip = __reduce_add_sync(0xffffffffu, n_skip);
+#ifdef SEELE_RASTER_PROFILE
+    if (lane == 0) {  // (profile build: warp-step phase counts replace the fast-path counters 11..15)
+        unsigned long long *sp = (unsigned long long *)stats;
+        atomicAdd(sp + 11, (unsigned long long)pr_rel);
+        atomicAdd(sp + 12, (unsigned long long)pr_nolead);
+        atomicAdd(sp + 13, (unsigned long long)pr_noblend);
+        atomicAdd(sp + 14, (unsigned long long)pr_amb);
+        atomicAdd(sp + 15, (unsigned long long)pr_death);
+    }
+    if (false) {
+#else
     if (lane == 0) {
+#endif
         unsigned long long *sp = (unsigned long long *)stats;
         if (w_red) atomicAdd(sp + SEELE_STAT_ALPHA_REDECIDE, (unsigned long long)w_red);
         if (w_tamb) atomicAdd(sp + SEELE_STAT_T_AMBIGUOUS, (unsigned long long)w_tamb);

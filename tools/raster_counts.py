@@ -17,4 +17,5 @@ cfg = bench.engine_cfg(args.engine)
 for f in (0, 40, 80):
     rr.select_async(poses[f])
     _, h = r.render_checked(rr.scene, poses[f], cfg, ranges=rr.ranges, n_ranges=rr.m + 2, n_max=rr.n_max)
-    print(f"frame {f}: steps={h[11]} member={h[12]} blend={h[13]} near={h[14]} hi={h[15]} pairs={h[4]}")
+    print(f"frame {f} {args.engine}: relevant warp-steps={h[11]} no-leader/no-pass={h[12]} no-blend={h[13]} "
+          f"ambiguous={h[14]} death-branch={h[15]} pairs={h[4]} alpha_eval={h[0]} blend={h[1]} leader={h[2]}")
