@@ -535,25 +535,28 @@ __device__ __forceinline__ bool col_tile(const Workspace &ws, int tiles_x, int t
             for (uint32_t c = 0; c < kSegW; c++)
                 if (a + c < b) atomicOr(&S.mask[warp][a + c], 1u << lane);
             __syncwarp();
+            uint32_t adv = 0u;  // per covered column: this lane is the highest covering lane (advances it)
+            uint32_t n_cov[kSegW];
 #pragma unroll
             for (uint32_t c = 0; c < kSegW; c++) {
+                n_cov[c] = 0u;
                 if (a + c >= b) continue;
                 const uint32_t v = a + c;
                 const uint32_t m = S.mask[warp][v];
                 const uint32_t slot = (uint32_t)S.cnt[warp][v] + __popc(m & lt) - sbase;
                 S.stage[slot] = pv[r];
                 S.stx[slot] = (uint8_t)v;
-            }
-            __syncwarp();
-#pragma unroll
-            for (uint32_t c = 0; c < kSegW; c++) {  // the highest covering lane advances the column
-                if (a + c >= b) continue;
-                const uint32_t v = a + c;
-                const uint32_t m = S.mask[warp][v];
                 if ((m >> lane) == 1u) {
-                    S.cnt[warp][v] += __popc(m);
-                    S.mask[warp][v] = 0u;
+                    adv |= 1u << c;
+                    n_cov[c] = __popc(m);
                 }
+            }
+            __syncwarp();  // every lane has read the masks and counters of its columns
+#pragma unroll
+            for (uint32_t c = 0; c < kSegW; c++) {
+                if (!((adv >> c) & 1u)) continue;
+                S.cnt[warp][a + c] += n_cov[c];
+                S.mask[warp][a + c] = 0u;
             }
             __syncwarp();
         }
