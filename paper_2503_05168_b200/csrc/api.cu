@@ -135,10 +135,7 @@ Workspace carve_workspace(void *base, long long n_max, long long cap, int width,
     const long long tiles = (long long)tiles_x * tiles_y;
     // never-cleared state first (epoch + look-back words; zero-filled once by the owner)
     w.epoch = c.take<uint32_t>(1);
-    w.look_tiles_d = (n + kSortTile - 1) / kSortTile;
-    // the column pass has at most one partial chunk per row beyond cap / tile
-    w.look_tiles_p = (cap + kSortTile - 1) / kSortTile + kMaxTileAxis + 1;
-    w.look = c.take<unsigned long long>(w.look_tiles_d + 2 * w.look_tiles_p * 256 + kDepthBuckets / kDepthScanItems);
+    w.look = c.take<unsigned long long>(kDepthBuckets / kDepthScanItems);
     w.status = c.take<uint8_t>(n);
     w.depth = c.take<double>(n);
     w.rect = c.take<short4>(n);
@@ -155,17 +152,19 @@ Workspace carve_workspace(void *base, long long n_max, long long cap, int width,
     w.dval[1] = c.take<uint32_t>(n);
     w.drect[0] = c.take<uint32_t>(n);
     w.drect[1] = c.take<uint32_t>(n);
-    w.poff = c.take<uint32_t>(n + 1);
-    w.tile_r0 = c.take<uint32_t>(cap / kSortTile + 2);
-    w.ent_x = c.take<uint32_t>(cap);
-    w.ent_p = c.take<uint32_t>(cap);
+    const BinGeom g = bin_geometry(n, width, height);
+    w.cmat = c.take<uint32_t>((long long)g.n_chunks * g.n_st);
+    w.st_cnt = c.take<uint32_t>(g.n_st);
+    w.st_start = c.take<uint32_t>(g.n_st + 1);
+    w.seg_first = c.take<uint32_t>(g.n_st + 1);
+    w.seg_st = c.take<uint32_t>(cap / kSeg + g.n_st + 1);
+    w.segcnt = c.take<uint32_t>((cap / kSeg + g.n_st + 1) * 16);
+    w.ent = c.take<uint2>(cap);
+    w.head_cnt = c.take<uint32_t>(tiles);
     w.pfinal = c.take<uint32_t>(cap);
     w.ranges = c.take<uint2>(tiles);
     w.tile_order = c.take<uint32_t>(tiles);
-    w.row_start = c.take<uint32_t>(kMaxTileAxis + 2);
-    w.chunk_first = c.take<uint32_t>(kMaxTileAxis + 2);
     w.tile_diff = c.take<int32_t>((long long)(tiles_x + 1) * (tiles_y + 1));
-    w.row_diff = c.take<int32_t>(tiles_y + 1);
     w.counters = c.take<uint32_t>(CNT_COUNT);
     w.pairs64 = c.take<unsigned long long>(1);
     w.bytes = c.off;

@@ -1,46 +1,55 @@
 // Tile binning and the tile sort on sm_100a, over the binned splats in exact
-// (depth, position) order (depth.cu).  Every size is read from device
-// memory, so a frame needs no host round trip:
+// (depth, position) order (depth.cu).  The output is sort_intersections'
+// order (sorting.py:32-54): pairs grouped by tile id, inside a tile by depth
+// rank.  Depth order -> tile order is a transpose; it is done in two stable
+// partitions, each counted up front so no pass has a look-back chain:
 //
-//   pair scan    k_pair_scan: exclusive scan of each splat's row-entry count
-//                in depth order (decoupled look-back), first rank of every
-//                4096-entry row-pass tile, and the 2D / 1D difference arrays
-//                of per-tile pair counts and per-row entry counts; the last
-//                CTA turns them into the tile ranges (sorting.py:46-53), the
-//                raster launch order, the row bases and the column-pass chunks.
-//   row pass     k_row_pass: bin_tiles (preprocess.py:159-189) of each splat
-//                as row entries (one per covered tile row, split into <= 3
-//                columns), stably grouped by tile row: one onesweep pass whose
-//                digit is the row.
-//   column pass  k_col_pass: every row chunk expands its entries into pairs,
-//                each written straight to its final slot (sorting.py:32-54
-//                order) = tile range start + pairs of that column in earlier
-//                chunks (look-back along the row) + earlier entries of the
-//                chunk covering the column.
+//   count   k_bin_count: the depth ranks are cut into C equal chunks; every
+//           chunk counts its entries per super-tile (4 x 4 tiles, 64 x 64
+//           pixels) -- a splat makes one entry per super-tile its tile rect
+//           (bin_tiles, preprocess.py:159-189) touches -- into row c of a
+//           C x S count matrix, and adds its rect to the 2D difference array
+//           of per-tile pair counts (both by 2D difference arrays: four
+//           shared-memory atomics per splat, whatever its size).
+//   scan    k_bin_scan: exclusive scan of every super-tile column of the
+//           count matrix over the chunks (in place: chunk c's first entry
+//           slot inside super-tile s's list); the last CTA scans the
+//           super-tile totals into list offsets and cuts every list into
+//           segments of kSeg entries, turns the difference array into
+//           per-tile counts and the tile ranges (sorting.py:46-53), and
+//           orders the tiles heavy-first for the raster.
+//   split   k_bin_split: each chunk re-reads its ranks and writes every entry
+//           (position, the rect's 2-bit sub-rectangle inside the super-tile)
+//           to its slot: chunk base + earlier warps of the chunk (per-warp
+//           counts, scanned across warps) + earlier ranks of the warp round
+//           (lane masks per super-tile, popc below the lane).
+//   head    k_bin_head: chunk 0 -- the nearest, largest splats -- is not put
+//           in the lists; one warp per tile pulls its pairs (they precede
+//           every later rank in the tile).
+//   expand  k_bin_segcount counts every segment's pairs per tile (ballots);
+//           k_bin_expand walks a segment in batches: every entry covers a
+//           subset of the super-tile's 16 tiles, one ballot per tile ranks it
+//           among the batch's warps, and the pairs are written with one
+//           coalesced store per tile into ranges[tile].x + head pairs + pairs
+//           of that tile in earlier segments + running count.
+//
+// Every size is read from device memory: a frame needs no host round trip.
+#include <algorithm>
+
 #include "onesweep.cuh"
 
 namespace seele {
 
-using namespace sweep;
-
-#ifdef SEELE_SORT_TRACE
-__device__ unsigned long long g_trace[8][4096][6];
-__device__ __forceinline__ unsigned long long gtime() {
-    unsigned long long t;
-    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
-    return t;
-}
-#define TRACE(pass, t, k) \
-    if (threadIdx.x == 0 && (t) < 4096) g_trace[pass][t][k] = gtime();
-#else
-#define TRACE(pass, t, k)
-#endif
-
 namespace {
+
+constexpr int kSt = 4;  // super-tile edge in tiles
+constexpr int kCountThreads = 256;
+constexpr int kScanThreads = sweep::NT;  // 512 (block_scan)
+constexpr int kExpandThreads = 256;
 
 // ---- frame start ---------------------------------------------------------------
 
-__global__ void k_frame_begin(Workspace ws, int64_t *stats, int n_diff, int tiles_y) {
+__global__ void k_frame_begin(Workspace ws, int64_t *stats, int n_diff) {
     const int tid = blockIdx.x * blockDim.x + threadIdx.x, stride = gridDim.x * blockDim.x;
     if (tid == 0) {
         *ws.epoch += 1u;
@@ -50,136 +59,242 @@ __global__ void k_frame_begin(Workspace ws, int64_t *stats, int n_diff, int tile
     if (tid < CNT_COUNT) ws.counters[tid] = 0u;
     for (int i = tid; i < kDepthBuckets / 4; i += stride) reinterpret_cast<uint4 *>(ws.bhist)[i] = make_uint4(0, 0, 0, 0);
     for (int i = tid; i < n_diff; i += stride) ws.tile_diff[i] = 0;
-    for (int i = tid; i <= tiles_y; i += stride) ws.row_diff[i] = 0;
 }
 
-__device__ __forceinline__ short4 unpack_rect(uint32_t v) {
-    return make_short4((short)(v & 0xff), (short)((v >> 8) & 0xff), (short)((v >> 16) & 0xff), (short)(v >> 24));
+struct Rect {
+    uint32_t x0, x1, y0, y1;
+};
+__device__ __forceinline__ Rect unpack_rect(uint32_t v) {
+    return Rect{v & 0xffu, (v >> 8) & 0xffu, (v >> 16) & 0xffu, v >> 24};
 }
 
-// ---- row entries: offsets, tile counts, ranges -------------------------------------
+// chunk c of the depth ranks: [c * K, min(n, (c + 1) * K)), K = ceil(n / C)
+__device__ __forceinline__ void chunk_range(uint32_t n, uint32_t C, uint32_t c, uint32_t &r0, uint32_t &r1) {
+    const uint32_t K = (n + C - 1) / C;
+    r0 = min(n, c * K);
+    r1 = min(n, r0 + K);
+}
 
-// Row entries cover at most kSegW columns (wider ones are split; pieces of one
-// splat cover disjoint columns, so the per-column order is unaffected): the
-// column pass's per-entry loops stay short.
-#ifndef SEELE_SEGW
-#define SEELE_SEGW 3
-#endif
-constexpr uint32_t kSegW = SEELE_SEGW;
+// ---- count -----------------------------------------------------------------------
 
-// bin_tiles (preprocess.py:159-189) of splat rank r covers rect [x0,x1] x [y0,y1]
-// -> ceil(w / kSegW) row entries per covered tile row y and w * h pairs.
-// This persistent kernel scans the entry counts h in depth-rank order
-// (decoupled look-back over 4096-rank tiles) into poff, marks the first rank
-// of every 4096-entry tile of the row pass, counts pairs, and accumulates the
-// 2D difference array of per-tile pair counts and the 1D one of per-row entry
-// counts.  The last CTA turns those into the tile ranges (sorting.py:46-53),
-// the row bases of the row pass and the chunk table of the column pass.
-// raster launch order bucket of a tile with c pairs: 32 - bits(c), heavy tiles first
-#ifndef SEELE_LIGHT_FIRST
-__device__ __forceinline__ int tile_bucket(uint32_t c) { return __clz(c); }
-#else
-__device__ __forceinline__ int tile_bucket(uint32_t c) { return 32 - __clz(c); }
-#endif
+// super-tile rect of a tile rect
+struct StRect {
+    uint32_t x0, x1, y0, y1;
+};
+__device__ __forceinline__ StRect st_rect(const Rect &rc) {
+    return StRect{rc.x0 / kSt, rc.x1 / kSt, rc.y0 / kSt, rc.y1 / kSt};
+}
 
-__global__ void __launch_bounds__(NT) k_pair_scan(Workspace ws, int tiles_x, int tiles_y, long long cap, int use_smem,
-                                                  int64_t *stats) {
-    extern __shared__ int32_t s_diff[];  // [(tiles_y + 1) * (tiles_x + 1)] if use_smem
-    __shared__ int32_t s_row[kMaxTileAxis + 1];
-    __shared__ bool s_last;
-    __shared__ uint32_t s_prev;
-    __shared__ unsigned long long s_pairs;
-    const int tid = threadIdx.x;
-    const int tx1 = tiles_x + 1;
-    const int ndiff = tx1 * (tiles_y + 1);
-    if (use_smem)
-        for (int i = tid; i < ndiff; i += NT) s_diff[i] = 0;
-    for (int i = tid; i <= tiles_y; i += NT) s_row[i] = 0;
-    if (tid == 0) s_pairs = 0ull;
-    int32_t *diff = use_smem ? s_diff : ws.tile_diff;
-    const uint32_t n = (uint32_t)stats[SEELE_STAT_BINNED];
-    const uint32_t *srect = ws.drect[kDepthFinal];
-    const uint32_t n_etiles = (uint32_t)(cap / TILE) + 1u;  // tile_r0 entries kept (capacity)
-    unsigned long long my_pairs = 0ull;
-    while (true) {
-        const uint32_t t = take_ticket(&ws.counters[CNT_TICKET + kLookScan]);
-        if (t * TILE >= n) break;
-        const uint32_t r0 = t * TILE + tid * IPT;
-        uint32_t h[IPT], rr[IPT];
-        uint32_t sum = 0;
+// 2D inclusive prefix in place over rows [0, ny) x columns [0, nx) of a
+// row-major array with row stride `stride`, by one warp (rows lane-parallel,
+// then columns).
+template <typename T>
+__device__ __forceinline__ void warp_prefix2d(T *a, int nx, int ny, int stride) {
+    const int lane = threadIdx.x & 31;
+    const int per = (nx + 31) / 32;
+    for (int y = 0; y < ny; y++) {
+        T *row = a + y * stride;
+        T run = 0;
+        for (int j = 0; j < per; j++) {
+            const int x = lane * per + j;
+            if (x < nx) run += row[x];
+        }
+        T incl = run;
 #pragma unroll
-        for (int k = 0; k < IPT; k++) rr[k] = srect[min(r0 + k, n - 1)];  // coalesced: rects in rank order
-#pragma unroll
-        for (int k = 0; k < IPT; k++) {
-            h[k] = 0u;
-            const uint32_t r = r0 + k;
-            if (r < n) {
-                const short4 rc = unpack_rect(rr[k]);
-                const int w = rc.y - rc.x + 1, hh = rc.w - rc.z + 1;
-                const int nseg = (w + kSegW - 1) / kSegW;  // row entries are split into <= kSegW columns
-                h[k] = (uint32_t)(hh * nseg);
-                my_pairs += (unsigned long long)(w * hh);
-                atomicAdd(&diff[rc.z * tx1 + rc.x], 1);
-                atomicAdd(&diff[rc.z * tx1 + rc.y + 1], -1);
-                atomicAdd(&diff[(rc.w + 1) * tx1 + rc.x], -1);
-                atomicAdd(&diff[(rc.w + 1) * tx1 + rc.y + 1], 1);
-                atomicAdd(&s_row[rc.z], nseg);
-                atomicAdd(&s_row[rc.w + 1], -nseg);
+        for (int o = 1; o < 32; o <<= 1) {
+            const T v = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += v;
+        }
+        T acc = incl - run;
+        for (int j = 0; j < per; j++) {
+            const int x = lane * per + j;
+            if (x < nx) {
+                acc += row[x];
+                row[x] = acc;
             }
-            sum += h[k];
-        }
-        uint32_t agg;
-        const uint32_t ex = block_scan<uint32_t>(sum, agg);
-        if (tid < 32) {  // one warp: 32 predecessors per round trip
-            const uint32_t pv = lookback_warp(ws.look_region(kLookScan), t, *ws.epoch * 16u + kLookScan, agg, t == 0);
-            if (tid == 0) s_prev = pv;
-        }
-        __syncthreads();
-        uint32_t run = s_prev + ex;
-#pragma unroll
-        for (int k = 0; k < IPT; k++) {
-            const uint32_t r = r0 + k;
-            if (r >= n) break;
-            ws.poff[r] = run;
-            const uint32_t end = run + h[k];
-            for (uint32_t e = (run + TILE - 1) / TILE; e * TILE < end && e < n_etiles; e++) ws.tile_r0[e] = r;
-            if (r == n - 1) ws.poff[n] = end;
-            run = end;
         }
     }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) my_pairs += __shfl_xor_sync(0xffffffffu, my_pairs, o);
-    if ((tid & 31) == 0 && my_pairs) atomicAdd(&s_pairs, my_pairs);
+    __syncwarp();
+    for (int x = lane; x < nx; x += 32) {
+        T acc = 0;
+        for (int y = 0; y < ny; y++) {
+            acc += a[y * stride + x];
+            a[y * stride + x] = acc;
+        }
+    }
+    __syncwarp();
+}
+
+// One CTA per kCountChunks consecutive chunks (one warp each for the prefix).  Shared memory: per chunk a
+// 2D difference array over the super-tile grid (-> entries per super-tile), then (if it fits) the CTA's one
+// over the tile grid, flushed into the frame's by atomics on its nonzero cells.  Four shared-memory atomics
+// per splat each, whatever its size.  Chunk 0 is the head (k_bin_head): no super-tile entries.
+constexpr int kCountChunks = kCountThreads / 32;
+__global__ void __launch_bounds__(kCountThreads) k_bin_count(Workspace ws, BinGeom g, int diff_in_smem) {
+    extern __shared__ int32_t s_cnt[];  // [kCountChunks][(sty + 1) * (stx + 1)] then [(tiles_y + 1) * (tiles_x + 1)]
+    const int sx1 = g.stx + 1, n_sd = sx1 * (g.sty + 1);
+    int32_t *s_diff = s_cnt + kCountChunks * n_sd;
+    const int tid = threadIdx.x, warp = tid >> 5;
+    const int tx1 = g.tiles_x + 1, n_diff = tx1 * (g.tiles_y + 1);
+    for (int i = tid; i < kCountChunks * n_sd; i += kCountThreads) s_cnt[i] = 0;
+    if (diff_in_smem)
+        for (int i = tid; i < n_diff; i += kCountThreads) s_diff[i] = 0;
     __syncthreads();
-    if (tid == 0 && s_pairs) atomicAdd(ws.pairs64, s_pairs);
-    if (use_smem)
-        for (int i = tid; i < ndiff; i += NT)
+    int32_t *diff = diff_in_smem ? s_diff : ws.tile_diff;
+    const uint32_t n = (uint32_t)ws.stats_ptr[SEELE_STAT_BINNED];
+    const uint32_t C = (uint32_t)g.n_chunks, K = (n + C - 1) / C;
+    const uint32_t c0 = blockIdx.x * kCountChunks;
+    const uint32_t r0 = min(n, c0 * K), r1 = min(n, r0 + kCountChunks * K);
+    const uint32_t *srect = ws.drect[kDepthFinal];
+    unsigned long long pairs = 0ull;
+    for (uint32_t r = r0 + tid; r < r1; r += kCountThreads) {
+        const Rect rc = unpack_rect(srect[r]);
+        pairs += (unsigned long long)((rc.x1 - rc.x0 + 1) * (rc.y1 - rc.y0 + 1));
+        atomicAdd(&diff[rc.y0 * tx1 + rc.x0], 1);
+        atomicAdd(&diff[rc.y0 * tx1 + rc.x1 + 1], -1);
+        atomicAdd(&diff[(rc.y1 + 1) * tx1 + rc.x0], -1);
+        atomicAdd(&diff[(rc.y1 + 1) * tx1 + rc.x1 + 1], 1);
+        const uint32_t c = r / K;
+        if (c == 0) continue;  // the head: emitted per tile (k_bin_head), not in the lists
+        int32_t *sd = s_cnt + (c - c0) * n_sd;
+        const StRect sr = st_rect(rc);
+        atomicAdd(&sd[sr.y0 * sx1 + sr.x0], 1);
+        atomicAdd(&sd[sr.y0 * sx1 + sr.x1 + 1], -1);
+        atomicAdd(&sd[(sr.y1 + 1) * sx1 + sr.x0], -1);
+        atomicAdd(&sd[(sr.y1 + 1) * sx1 + sr.x1 + 1], 1);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) pairs += __shfl_xor_sync(0xffffffffu, pairs, o);
+    if ((tid & 31) == 0 && pairs) atomicAdd(ws.pairs64, pairs);
+    __syncthreads();
+    const uint32_t c = c0 + warp;
+    if (c < C) {
+        int32_t *sd = s_cnt + warp * n_sd;
+        warp_prefix2d(sd, g.stx, g.sty, sx1);
+        uint32_t *row = ws.cmat + (size_t)c * g.n_st;
+        for (int i = tid & 31; i < g.n_st; i += 32) row[i] = (uint32_t)sd[(i / g.stx) * sx1 + i % g.stx];
+    }
+    if (diff_in_smem)
+        for (int i = tid; i < n_diff; i += kCountThreads)
             if (s_diff[i]) atomicAdd(&ws.tile_diff[i], s_diff[i]);
-    for (int i = tid; i <= tiles_y; i += NT)
-        if (s_row[i]) atomicAdd(&ws.row_diff[i], s_row[i]);
+}
+
+// ---- scan ------------------------------------------------------------------------
+
+// raster launch order bucket of a tile with c pairs: 32 - bits(c), heavy tiles first
+__device__ __forceinline__ int heavy_bucket(uint32_t c) { return __clz(c); }
+
+// CTA b scans super-tiles [32 b, 32 b + 32) (lane = super-tile, coalesced rows of
+// the count matrix); its 16 warps take consecutive segments of the chunks.
+// The last CTA to finish does the frame-wide scans.
+__global__ void __launch_bounds__(kScanThreads) k_bin_scan(Workspace ws, BinGeom g, long long cap, int diff_in_smem) {
+    extern __shared__ int32_t s_diff[];  // [(tiles_y + 1) * (tiles_x + 1)] if diff_in_smem
+    __shared__ uint32_t s_seg[kScanThreads / 32][32];
+    __shared__ bool s_last;
+    __shared__ uint32_t s_bucket[33];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    constexpr int NW = kScanThreads / 32;
+    {
+        const int s = blockIdx.x * 32 + lane;
+        const bool ok = s < g.n_st;
+        const int C = g.n_chunks, per = (C + NW - 1) / NW;
+        const int c0 = min(C, warp * per), c1 = min(C, c0 + per);
+        uint32_t *col = ws.cmat + (ok ? s : 0);
+        uint32_t sum = 0;
+        {
+            int c = c0;
+            for (; c + 8 <= c1; c += 8) {
+                uint32_t v[8];
+#pragma unroll
+                for (int u = 0; u < 8; u++) v[u] = ok ? col[(size_t)(c + u) * g.n_st] : 0u;
+#pragma unroll
+                for (int u = 0; u < 8; u++) sum += v[u];
+            }
+            for (; c < c1; c++) sum += ok ? col[(size_t)c * g.n_st] : 0u;
+        }
+        s_seg[warp][lane] = sum;
+        __syncthreads();
+        if (warp == 0) {
+            uint32_t run = 0;
+            for (int w = 0; w < NW; w++) {
+                const uint32_t v = s_seg[w][lane];
+                s_seg[w][lane] = run;
+                run += v;
+            }
+            if (ok) ws.st_cnt[s] = run;
+        }
+        __syncthreads();
+        if (ok) {
+            uint32_t run = s_seg[warp][lane];
+            int c = c0;
+            for (; c + 8 <= c1; c += 8) {
+                uint32_t v[8];
+#pragma unroll
+                for (int u = 0; u < 8; u++) v[u] = col[(size_t)(c + u) * g.n_st];
+#pragma unroll
+                for (int u = 0; u < 8; u++) {
+                    col[(size_t)(c + u) * g.n_st] = run;
+                    run += v[u];
+                }
+            }
+            for (; c < c1; c++) {
+                const uint32_t v = col[(size_t)c * g.n_st];
+                col[(size_t)c * g.n_st] = run;
+                run += v;
+            }
+        }
+    }
     __threadfence();
     __syncthreads();
     if (tid == 0) s_last = atomicAdd(&ws.counters[CNT_DONE_SCAN], 1u) == gridDim.x - 1;
     __syncthreads();
     if (!s_last) return;
     __threadfence();
-    // ---- last CTA: per-tile counts -> ranges; row bases; chunk table
+    // ---- last CTA: super-tile list offsets and segments; tile counts -> ranges; launch order
     const unsigned long long total = *(volatile unsigned long long *)ws.pairs64;
     const bool over = total > (unsigned long long)cap;
-    int32_t *g = use_smem ? s_diff : ws.tile_diff;  // in shared memory when it fits
-    if (use_smem)
-        for (int i = tid; i < ndiff; i += NT) s_diff[i] = *(volatile int32_t *)&ws.tile_diff[i];
+    {
+        const int per = (g.n_st + kScanThreads - 1) / kScanThreads;
+        const int a0 = min(g.n_st, tid * per), a1 = min(g.n_st, a0 + per);
+        uint32_t part = 0, pseg = 0;
+        for (int i = a0; i < a1; i++) {
+            const uint32_t c = *(volatile uint32_t *)&ws.st_cnt[i];
+            part += c;
+            pseg += (c + kSeg - 1) / kSeg;
+        }
+        uint32_t all, all_seg;
+        uint32_t acc = sweep::block_scan<uint32_t>(part, all);
+        uint32_t sacc = sweep::block_scan<uint32_t>(pseg, all_seg);
+        for (int i = a0; i < a1; i++) {
+            const uint32_t c = *(volatile uint32_t *)&ws.st_cnt[i];
+            ws.st_start[i] = acc;
+            ws.seg_first[i] = sacc;
+            if (!over)  // (on overflow the lists are not built and may exceed the segment table)
+                for (uint32_t k = 0; k * kSeg < c; k++) ws.seg_st[sacc + k] = (uint32_t)i;
+            acc += c;
+            sacc += (c + kSeg - 1) / kSeg;
+        }
+        if (tid == 0) {
+            ws.st_start[g.n_st] = all;
+            ws.seg_first[g.n_st] = all_seg;
+            ws.counters[CNT_SEGS] = over ? 0u : all_seg;
+        }
+    }
+    const int tx1 = g.tiles_x + 1;
+    const int ndiff = tx1 * (g.tiles_y + 1);
+    int32_t *d = diff_in_smem ? s_diff : ws.tile_diff;  // in shared memory when it fits
+    if (diff_in_smem)
+        for (int i = tid; i < ndiff; i += kScanThreads) s_diff[i] = *(volatile int32_t *)&ws.tile_diff[i];
     __syncthreads();
     // 2D prefix sum in place: rows (one warp per row, lane-parallel scan), then columns
     {
-        const int lane = tid & 31, warp = tid >> 5;
-        const int per = (tiles_x + 31) / 32;
-        for (int y = warp; y < tiles_y; y += NT / 32) {
-            int32_t *row = g + y * tx1;
+        const int per = (g.tiles_x + 31) / 32;
+        for (int y = warp; y < g.tiles_y; y += NW) {
+            int32_t *row = d + y * tx1;
             int32_t run = 0;
             for (int j = 0; j < per; j++) {
                 const int x = lane * per + j;
-                if (x < tiles_x) run += row[x];
+                if (x < g.tiles_x) run += row[x];
             }
             int32_t incl = run;
 #pragma unroll
@@ -190,7 +305,7 @@ __global__ void __launch_bounds__(NT) k_pair_scan(Workspace ws, int tiles_x, int
             int32_t acc = incl - run;
             for (int j = 0; j < per; j++) {
                 const int x = lane * per + j;
-                if (x < tiles_x) {
+                if (x < g.tiles_x) {
                     acc += row[x];
                     row[x] = acc;
                 }
@@ -198,30 +313,29 @@ __global__ void __launch_bounds__(NT) k_pair_scan(Workspace ws, int tiles_x, int
         }
     }
     __syncthreads();
-    for (int x = tid; x < tiles_x; x += NT) {
+    for (int x = tid; x < g.tiles_x; x += kScanThreads) {
         int32_t acc = 0;
-        for (int y = 0; y < tiles_y; y++) {
-            acc += g[y * tx1 + x];
-            g[y * tx1 + x] = acc;
+        for (int y = 0; y < g.tiles_y; y++) {
+            acc += d[y * tx1 + x];
+            d[y * tx1 + x] = acc;
         }
     }
     __syncthreads();
-    // exclusive scan of the per-tile counts in linear tile order -> ranges
-    const int n_tiles = tiles_x * tiles_y;
-    const int per = (n_tiles + NT - 1) / NT;
-    const int a0 = tid * per, a1 = min(a0 + per, n_tiles);
+    // exclusive scan of the per-tile counts in linear tile order -> ranges; heavy-first raster order
+    const int n_tiles = g.tiles_x * g.tiles_y;
+    const int per = (n_tiles + kScanThreads - 1) / kScanThreads;
+    const int a0 = min(n_tiles, tid * per), a1 = min(n_tiles, a0 + per);
     uint32_t part = 0;
-    for (int i = a0; i < a1; i++) part += (uint32_t)g[(i / tiles_x) * tx1 + i % tiles_x];
+    for (int i = a0; i < a1; i++) part += (uint32_t)d[(i / g.tiles_x) * tx1 + i % g.tiles_x];
     uint32_t all;
-    uint32_t acc = block_scan<uint32_t>(part, all);
-    __shared__ uint32_t s_bucket[33];
+    uint32_t acc = sweep::block_scan<uint32_t>(part, all);
     if (tid < 33) s_bucket[tid] = 0u;
     __syncthreads();
     for (int i = a0; i < a1; i++) {
-        const uint32_t c = (uint32_t)g[(i / tiles_x) * tx1 + i % tiles_x];
+        const uint32_t c = (uint32_t)d[(i / g.tiles_x) * tx1 + i % g.tiles_x];
         ws.ranges[i] = over ? make_uint2(0u, 0u) : make_uint2(acc, acc + c);
         acc += c;
-        atomicAdd(&s_bucket[tile_bucket(c)], 1u);
+        atomicAdd(&s_bucket[heavy_bucket(c)], 1u);
     }
     __syncthreads();
     if (tid == 0) {  // exclusive scan over the 33 buckets
@@ -234,353 +348,326 @@ __global__ void __launch_bounds__(NT) k_pair_scan(Workspace ws, int tiles_x, int
     }
     __syncthreads();
     for (int i = a0; i < a1; i++) {  // raster launch order (within a bucket arbitrary; results do not depend on it)
-        const uint32_t c = (uint32_t)g[(i / tiles_x) * tx1 + i % tiles_x];
-        ws.tile_order[atomicAdd(&s_bucket[tile_bucket(c)], 1u)] = (uint32_t)i;
+        const uint32_t c = (uint32_t)d[(i / g.tiles_x) * tx1 + i % g.tiles_x];
+        ws.tile_order[atomicAdd(&s_bucket[heavy_bucket(c)], 1u)] = (uint32_t)i;
     }
-    // entries per row -> row bases (row pass digit bases) and column-pass chunks
-    for (int i = tid; i <= tiles_y; i += NT) s_row[i] = *(volatile int32_t *)&ws.row_diff[i];
-    __syncthreads();
     if (tid == 0) {
-        int32_t rc = 0;
-        uint32_t e = 0, c = 0;
-        for (int y = 0; y < tiles_y; y++) {
-            rc += s_row[y];
-            ws.row_start[y] = e;
-            ws.chunk_first[y] = c;
-            e += (uint32_t)rc;
-            c += ((uint32_t)rc + TILE - 1) / TILE;
-        }
-        ws.row_start[tiles_y] = e;
-        ws.chunk_first[tiles_y] = c;
-        stats[SEELE_STAT_TILE_PAIRS] = (int64_t)total;
-        stats[SEELE_STAT_OVERFLOW] = over ? 1 : 0;
+        ws.stats_ptr[SEELE_STAT_TILE_PAIRS] = (int64_t)total;
+        ws.stats_ptr[SEELE_STAT_OVERFLOW] = over ? 1 : 0;
         ws.counters[CNT_OVERFLOW] = over ? 1u : 0u;
         ws.counters[CNT_PAIRS] = over ? 0u : (uint32_t)total;
-        ws.counters[CNT_ENTRIES] = over ? 0u : e;
-        ws.counters[CNT_CHUNKS] = over ? 0u : c;
     }
 }
 
-// ---- row pass ----------------------------------------------------------------------
+// ---- split -------------------------------------------------------------------------
 
-struct RowSmem {
-    RankSmem rs;
-    uint32_t s_base[RADIX];
-    union {
-        struct {  // the ranks overlapping this tile
-            uint32_t off[TILE + 3];
-            uint32_t pos[TILE + 2];
-            uint32_t rect[TILE + 2];  // x0 | x1 << 8 | y0 << 16
-        } e;
-        struct {  // the row-sorted tile
-            uint32_t x[TILE];
-            uint32_t p[TILE];
-        } g;
-    } u;
-    uint32_t gx[TILE];  // generated entries in emission order
-    uint32_t gp[TILE];
-};
+// sub-rectangle of a tile rect inside super-tile (sx, sy): x0 | x1 << 2 | y0 << 4 | y1 << 6, in tiles
+// relative to the super-tile
+__device__ __forceinline__ uint32_t sub_rect(const Rect &rc, uint32_t sx, uint32_t sy) {
+    const uint32_t bx = sx * kSt, by = sy * kSt;
+    const uint32_t lx0 = max(rc.x0, bx) - bx, lx1 = min(rc.x1, bx + kSt - 1) - bx;
+    const uint32_t ly0 = max(rc.y0, by) - by, ly1 = min(rc.y1, by + kSt - 1) - by;
+    return lx0 | (lx1 << 2) | (ly0 << 4) | (ly1 << 6);
+}
 
-// Emits the row entries of 4096 consecutive entry slots in depth-rank order
-// (ty-major inside a splat, like bin_tiles) and scatters them stably by row:
-// one onesweep pass whose digit is the tile row.
-// One ticket of the row pass; false once the tickets run past the entries.
-__device__ __forceinline__ bool row_tile(const Workspace &ws, int64_t *stats, RowSmem &S, uint32_t t) {
-    const uint32_t E = ws.counters[CNT_ENTRIES];
-    const uint32_t base = t * TILE;
-    if (base >= E) return false;
+// One CTA per chunk, NW warps; warp w takes ranks [r0 + w Kw, r0 + (w + 1) Kw) of the chunk.
+// Shared memory, per warp, indexed like the super-tile difference array (row stride stx + 1): the entry
+// counts -> running entry slot of every super-tile, and the lane masks of the current item block.
+// A round of 32 ranks makes one work item per (rank, super-tile it touches), owner-major; items are
+// taken 32 at a time, so big splats cost work in proportion to their super-tiles.  Inside an item
+// block, an item's rank among the block's items of its super-tile is popc(mask & owners below);
+// blocks are consecutive in owner order, so the order is (rank, super-tile) stable.
+template <int NW>
+__global__ void __launch_bounds__(NW * 32) k_bin_split(Workspace ws, BinGeom g) {
+    extern __shared__ uint32_t s_sp[];  // cnt[NW][n_sd], mask[NW][n_sd]
+    if (ws.counters[CNT_OVERFLOW] || blockIdx.x == 0) return;  // (chunk 0: the head, k_bin_head)
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const uint32_t n = (uint32_t)stats[SEELE_STAT_BINNED];
-    const uint32_t *sorted = ws.dval[kDepthFinal];
-    const uint32_t end = min(base + (uint32_t)TILE, E);
-    const uint32_t r0 = ws.tile_r0[t];
-    const uint32_t r1 = end < E ? ws.tile_r0[t + 1] : n - 1;  // last rank overlapping
-    const int nr = (int)(r1 - r0 + 1);
-    for (int k = tid; k <= nr; k += NT) {
-        S.u.e.off[k] = ws.poff[r0 + k];
-        if (k < nr) {
-            S.u.e.pos[k] = sorted[r0 + k];
-            S.u.e.rect[k] = ws.drect[kDepthFinal][r0 + k] & 0xffffffu;  // x0 | x1 << 8 | y0 << 16
-        }
-    }
+    const int sx1 = g.stx + 1, n_sd = sx1 * (g.sty + 1);
+    uint32_t *cnt = s_sp + (size_t)warp * n_sd, *mask = s_sp + (size_t)(NW + warp) * n_sd;
+    for (int i = tid; i < 2 * NW * n_sd; i += NW * 32) s_sp[i] = 0u;
     __syncthreads();
-    const uint32_t i0 = base + (uint32_t)tid * IPT;
-    if (i0 < end) {
-        int lo = 0, hi = nr - 1;
-        while (lo < hi) {
-            const int mid = (lo + hi + 1) >> 1;
-            if (S.u.e.off[mid] <= i0) lo = mid; else hi = mid - 1;
-        }
-        uint32_t rc = S.u.e.rect[lo];
-        uint32_t xa = rc & 0xffu, xb = (rc >> 8) & 0xffu;
-        uint32_t nseg = (xb - xa + kSegW) / kSegW;
-        const uint32_t local = i0 - S.u.e.off[lo];
-        uint32_t y = (rc >> 16) + local / nseg, seg = local % nseg;
-        uint32_t next = S.u.e.off[lo + 1];
-        uint32_t p = S.u.e.pos[lo];
-        const uint32_t stop = min(i0 + (uint32_t)IPT, end);
-        for (uint32_t i = i0; i < stop; i++) {
-            if (i == next) {
-                lo++;
-                rc = S.u.e.rect[lo];
-                xa = rc & 0xffu;
-                xb = (rc >> 8) & 0xffu;
-                nseg = (xb - xa + kSegW) / kSegW;
-                y = rc >> 16;
-                seg = 0;
-                next = S.u.e.off[lo + 1];
-                p = S.u.e.pos[lo];
-            }
-            const uint32_t s0 = xa + seg * kSegW, s1 = min(xb, s0 + kSegW - 1);
-            S.gx[i - base] = s0 | (s1 << 8) | (y << 16);
-            S.gp[i - base] = p;
-            if (++seg == nseg) {
-                seg = 0;
-                y++;
-            }
-        }
-    }
-    __syncthreads();
-    const int nv = (int)(end - base);
-    uint32_t xk[IPT], pv[IPT], dig[IPT], pos[IPT];
-#pragma unroll
-    for (int r = 0; r < IPT; r++) {
-        const int i = warp * 32 * IPT + r * 32 + lane;
-        dig[r] = NO_DIGIT;
-        if (i < nv) {
-            xk[r] = S.gx[i];
-            pv[r] = S.gp[i];
-            dig[r] = xk[r] >> 16;
-        }
-    }
-    uint32_t count;
-#ifndef SEELE_ROW_BALLOT
-#define SEELE_ROW_BALLOT 1
-#endif
-    block_rank<SEELE_ROW_BALLOT>(dig, pos, S.rs, count);
-    if (tid < RADIX) {
-        const uint32_t ex =
-            lookback(ws.look_region(kLookRows) + tid, RADIX, t, *ws.epoch * 16u + kLookRows, count, t == 0);
-        S.s_base[tid] = ws.row_start[min(tid, kMaxTileAxis)] + ex - S.rs.start[tid];
-    }
-#pragma unroll
-    for (int r = 0; r < IPT; r++) {
-        if (dig[r] == NO_DIGIT) continue;
-        S.u.g.x[pos[r]] = xk[r];
-        S.u.g.p[pos[r]] = pv[r];
-    }
-    __syncthreads();
-    for (int i = tid; i < nv; i += NT) {
-        const uint32_t x = S.u.g.x[i];
-        const uint32_t dst = S.s_base[x >> 16] + (uint32_t)i;
-        ws.ent_x[dst] = x;
-        ws.ent_p[dst] = S.u.g.p[i];
-    }
-    return true;
-}
-
-// Persistent: each CTA takes tickets (in order over the grid) until none is left,
-// so the grid is sized to the machine, not to the pair capacity.
-#ifndef SEELE_ROW_MINB
-#define SEELE_ROW_MINB 2
-#endif
-__global__ void __launch_bounds__(NT, SEELE_ROW_MINB) k_row_pass(Workspace ws, int64_t *stats) {
-    extern __shared__ __align__(16) unsigned char smem[];
-    RowSmem &S = *reinterpret_cast<RowSmem *>(smem);
-    ticket_loop(&ws.counters[CNT_TICKET + kLookRows], [&](uint32_t t) { return row_tile(ws, stats, S, t); });
-
-}
-
-// ---- column pass ---------------------------------------------------------------------
-
-constexpr int kColW = kMaxTileAxis + 1;
-constexpr int kColStage = 12288;  // pairs staged per column group (48 KB + 12 KB)
-
-struct ColSmem {
-    int32_t cnt[NT / 32][kColW];      // per-warp counts -> per-warp staging offsets
-    uint32_t mask[NT / 32][kColW];    // per-round lanes covering each column
-    uint32_t cstart[kColW + 1];       // chunk-local first slot of each column
-    uint32_t gbase[kColW];            // global slot of the chunk's first pair of each column
-    uint32_t stage[kColStage];
-    uint8_t stx[kColStage];
-    uint32_t gfirst[kColW + 1];       // column groups that fit the staging buffer
-    uint32_t chunk_first[kColW + 1];
-    int n_groups;
-    uint32_t row;
-};
-
-// One chunk (<= 4096 entries) of one tile row: expands every entry into its
-// pairs and writes them to their final slots.  Inside the row, the pairs of
-// tile (ty, tx) come from the entries covering tx in entry (= depth-rank)
-// order, so slot = ranges[tile].x + (pairs of tx in earlier chunks of the
-// row: look-back along the row's chunks) + (entries covering tx earlier in
-// this chunk).  The last term: per-warp counts + exclusive scan over warps,
-// and inside a warp round (32 entries) every lane ORs its bit into the lane
-// mask of each column it covers, so its rank at column v is
-// popc(mask_v & lanes_below) -- work proportional to the entry's width.
-// Pairs are staged by column in shared memory and copied out as contiguous
-// runs.
-// One ticket (row chunk) of the column pass; false once the tickets run past the chunks.
-__device__ __forceinline__ bool col_tile(const Workspace &ws, int tiles_x, int tiles_y, ColSmem &S, uint32_t t) {
-    const uint32_t C = ws.counters[CNT_CHUNKS];
-    if (t >= C) return false;
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    for (int y = tid; y < tiles_y; y += NT) S.chunk_first[y] = ws.chunk_first[y];
-    __syncthreads();
-    if (tid == 0) {  // row of chunk t: last y with chunk_first[y] <= t
-        int lo = 0, hi = tiles_y - 1;
-        while (lo < hi) {
-            const int mid = (lo + hi + 1) >> 1;
-            if (S.chunk_first[mid] <= t) lo = mid; else hi = mid - 1;
-        }
-        S.row = (uint32_t)lo;
-    }
-    for (int i = lane; i < kColW; i += 32) {
-        S.cnt[warp][i] = 0;
-        S.mask[warp][i] = 0u;
-    }
-    __syncthreads();
-    const int ty = (int)S.row;
-    const uint32_t k = t - ws.chunk_first[ty];
-    const uint32_t s = ws.row_start[ty] + k * TILE, e = min(s + (uint32_t)TILE, ws.row_start[ty + 1]);
-    uint32_t x0[IPT], x1[IPT], pv[IPT];
-    const uint32_t wb = s + (uint32_t)(warp * 32 * IPT) + lane;
-#pragma unroll
-    for (int r = 0; r < IPT; r++) {
-        const uint32_t i = min(wb + r * 32, e - 1);
-        const uint32_t x = ws.ent_x[i];
-        pv[r] = ws.ent_p[i];
-        const bool valid = wb + r * 32 < e;
-        x0[r] = valid ? (x & 0xffu) : 1u;  // absent: empty interval [1, 0]
-        x1[r] = valid ? ((x >> 8) & 0xffu) : 0u;
-    }
-#pragma unroll
-    for (int r = 0; r < IPT; r++) {
-        if (x0[r] > x1[r]) continue;
-        atomicAdd(&S.cnt[warp][x0[r]], 1);
-        atomicAdd(&S.cnt[warp][x1[r] + 1], -1);
-    }
-    __syncwarp();
-    constexpr int PER = (kColW + 31) / 32;  // columns per lane in warp-wide scans
+    const uint32_t n = (uint32_t)ws.stats_ptr[SEELE_STAT_BINNED];
+    uint32_t r0, r1;
+    chunk_range(n, (uint32_t)g.n_chunks, blockIdx.x, r0, r1);
+    const uint32_t Kw = (r1 - r0 + NW - 1) / NW;
+    const uint32_t w0 = min(r1, r0 + warp * Kw), w1 = min(r1, w0 + Kw);
+    const uint32_t *srect = ws.drect[kDepthFinal];
+    const uint32_t *spos = ws.dval[kDepthFinal];
+    // per-warp entry counts per super-tile: difference array (four updates per rank) + 2D prefix
     {
-        int32_t v[PER], run = 0;
-#pragma unroll
-        for (int j = 0; j < PER; j++) {
-            const int c = lane * PER + j;
-            v[j] = c < kColW ? S.cnt[warp][c] : 0;
-            run += v[j];
+        int32_t *dw = reinterpret_cast<int32_t *>(cnt);
+        for (uint32_t r = w0 + lane; r < w1; r += 32) {
+            const StRect sr = st_rect(unpack_rect(srect[r]));
+            atomicAdd(&dw[sr.y0 * sx1 + sr.x0], 1);
+            atomicAdd(&dw[sr.y0 * sx1 + sr.x1 + 1], -1);
+            atomicAdd(&dw[(sr.y1 + 1) * sx1 + sr.x0], -1);
+            atomicAdd(&dw[(sr.y1 + 1) * sx1 + sr.x1 + 1], 1);
         }
-        int32_t incl = run;
+        __syncwarp();
+        warp_prefix2d(dw, g.stx, g.sty, sx1);
+    }
+    __syncthreads();
+    // -> each warp's first slot per super-tile: list start + chunk base + earlier warps
+    const uint32_t *cbase = ws.cmat + (size_t)blockIdx.x * g.n_st;
+    for (int s = tid; s < g.n_st; s += NW * 32) {
+        const int sd = (s / g.stx) * sx1 + s % g.stx;
+        uint32_t run = ws.st_start[s] + cbase[s];
+#pragma unroll
+        for (int w = 0; w < NW; w++) {
+            const uint32_t c = s_sp[(size_t)w * n_sd + sd];
+            s_sp[(size_t)w * n_sd + sd] = run;
+            run += c;
+        }
+    }
+    __syncthreads();
+    uint2 *ent = ws.ent;
+    uint32_t rc_next = w0 + lane < w1 ? srect[w0 + lane] : 0u, p_next = w0 + lane < w1 ? spos[w0 + lane] : 0u;
+    for (uint32_t b = w0; b < w1; b += 32) {
+        const uint32_t r = b + lane;
+        const bool valid = r < w1;
+        const uint32_t rcw = rc_next, p = p_next;
+        if (r + 32 < w1) {  // next round in flight
+            rc_next = srect[r + 32];
+            p_next = spos[r + 32];
+        }
+        const StRect sr = st_rect(unpack_rect(rcw));
+        const uint32_t sw = sr.x1 - sr.x0 + 1;
+        const uint32_t nst = valid ? sw * (sr.y1 - sr.y0 + 1) : 0u;
+        uint32_t incl = nst;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
-            const int32_t y = __shfl_up_sync(0xffffffffu, incl, o);
-            if (lane >= o) incl += y;
+            const uint32_t v = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += v;
         }
-        int32_t acc = incl - run;
+        const uint32_t excl = incl - nst;
+        const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
+        for (uint32_t ib = 0; ib < total; ib += 32) {
+            const uint32_t item = ib + lane;
+            // owner: the lane whose [excl, incl) holds the item (first lane with incl > item)
+            int owner = 0;
 #pragma unroll
-        for (int j = 0; j < PER; j++) {
-            const int c = lane * PER + j;
-            acc += v[j];
-            if (c < kColW) S.cnt[warp][c] = acc;
-        }
-    }
-    __syncthreads();
-    uint32_t tot = 0;
-    if (tid < kColW) {
-#pragma unroll
-        for (int w = 0; w < NT / 32; w++) {
-            const int32_t c = S.cnt[w][tid];
-            S.cnt[w][tid] = (int32_t)tot;
-            tot += (uint32_t)c;
-        }
-    }
-    uint32_t chunk_total;
-    const uint32_t cs = block_scan<uint32_t>(tid < tiles_x ? tot : 0u, chunk_total);
-    if (tid < tiles_x) {
-        S.cstart[tid] = cs;
-        const uint32_t ex = lookback(ws.look_region(kLookCols) + tid, RADIX, t, *ws.epoch * 16u + kLookCols, tot,
-                                     k == 0);
-        S.gbase[tid] = ws.ranges[ty * tiles_x + tid].x + ex;
-#pragma unroll
-        for (int w = 0; w < NT / 32; w++) S.cnt[w][tid] += (int32_t)cs;  // chunk-local staging offsets
-    }
-    if (tid == 0) S.cstart[tiles_x] = chunk_total;
-    __syncthreads();
-    if (tid == 0) {
-        int g = 0;
-        S.gfirst[0] = 0;
-        if (chunk_total > (uint32_t)kColStage) {  // rare: greedy column groups that fit the staging buffer
-            uint32_t gs = 0;
-            for (int c = 0; c < tiles_x; c++) {
-                if (S.cstart[c + 1] - gs > (uint32_t)kColStage) {
-                    S.gfirst[++g] = (uint32_t)c;
-                    gs = S.cstart[c];
-                }
+            for (int step = 16; step > 0; step >>= 1) {
+                const uint32_t v = __shfl_sync(0xffffffffu, incl, owner + step - 1);
+                if (v <= item) owner += step;
             }
-        }
-        S.gfirst[++g] = (uint32_t)tiles_x;
-        S.n_groups = g;
-    }
-    __syncthreads();
-    const unsigned lt = (1u << lane) - 1u;
-    for (int grp = 0; grp < S.n_groups; grp++) {
-        const uint32_t ca = S.gfirst[grp], cb = S.gfirst[grp + 1];
-        const uint32_t sbase = S.cstart[ca];
-#pragma unroll 1
-        for (int r = 0; r < IPT; r++) {
-            // columns of this entry inside the current group
-            const uint32_t a = max(x0[r], ca), b = min(x1[r] + 1u, cb);  // [a, b), at most kSegW columns
-            // (fixed-trip predicated loops: entries cover <= kSegW columns)
-#pragma unroll
-            for (uint32_t c = 0; c < kSegW; c++)
-                if (a + c < b) atomicOr(&S.mask[warp][a + c], 1u << lane);
+            owner = min(owner, 31);
+            const uint32_t o_excl = __shfl_sync(0xffffffffu, excl, owner);
+            const uint32_t o_rect = __shfl_sync(0xffffffffu, rcw, owner);
+            const uint32_t o_pos = __shfl_sync(0xffffffffu, p, owner);
+            const bool live = item < total;
+            const Rect orc = unpack_rect(o_rect);
+            const StRect osr = st_rect(orc);
+            const uint32_t osw = osr.x1 - osr.x0 + 1;
+            const uint32_t k = item - o_excl;
+            const uint32_t ky = k / osw;
+            const uint32_t sx = osr.x0 + (k - ky * osw), sy = osr.y0 + ky;
+            const uint32_t sd = sy * sx1 + sx;
+            const uint32_t obit = 1u << owner;
+            if (live) atomicOr(&mask[sd], obit);
             __syncwarp();
-            uint32_t adv = 0u;  // per covered column: this lane is the highest covering lane (advances it)
-            uint32_t n_cov[kSegW];
-#pragma unroll
-            for (uint32_t c = 0; c < kSegW; c++) {
-                n_cov[c] = 0u;
-                if (a + c >= b) continue;
-                const uint32_t v = a + c;
-                const uint32_t m = S.mask[warp][v];
-                const uint32_t slot = (uint32_t)S.cnt[warp][v] + __popc(m & lt) - sbase;
-                S.stage[slot] = pv[r];
-                S.stx[slot] = (uint8_t)v;
-                if ((m >> lane) == 1u) {
-                    adv |= 1u << c;
-                    n_cov[c] = __popc(m);
-                }
+            uint32_t m = 0u;
+            if (live) {
+                m = mask[sd];
+                ent[cnt[sd] + __popc(m & (obit - 1u))] = make_uint2(o_pos, sub_rect(orc, sx, sy));
             }
-            __syncwarp();  // every lane has read the masks and counters of its columns
-#pragma unroll
-            for (uint32_t c = 0; c < kSegW; c++) {
-                if (!((adv >> c) & 1u)) continue;
-                S.cnt[warp][a + c] += n_cov[c];
-                S.mask[warp][a + c] = 0u;
+            __syncwarp();  // every item has read the mask and slot of its super-tile
+            if (live && (m >> owner) == 1u) {  // the highest owner advances the super-tile
+                cnt[sd] += __popc(m);
+                mask[sd] = 0u;
             }
             __syncwarp();
         }
-        __syncthreads();
-        const uint32_t n_stage = S.cstart[cb] - sbase;
-        for (uint32_t i = tid; i < n_stage; i += NT) {
-            const uint32_t v = S.stx[i];
-            ws.pfinal[S.gbase[v] + (i + sbase - S.cstart[v])] = S.stage[i];
-        }
-        __syncthreads();
     }
-    return true;
 }
 
-// Persistent, like k_row_pass.
-#ifndef SEELE_COL_MINB
-#define SEELE_COL_MINB 2
-#endif
-__global__ void __launch_bounds__(NT, SEELE_COL_MINB) k_col_pass(Workspace ws, int tiles_x, int tiles_y) {
-    extern __shared__ __align__(16) unsigned char smem[];
-    ColSmem &S = *reinterpret_cast<ColSmem *>(smem);
-    ticket_loop(&ws.counters[CNT_TICKET + kLookCols],
-                [&](uint32_t t) { return col_tile(ws, tiles_x, tiles_y, S, t); });
+// ---- expand ------------------------------------------------------------------------
 
+// tiles of a sub-rectangle as a 16-bit mask (bit 4 ly + lx)
+__device__ __forceinline__ uint32_t sub_mask(uint32_t sub) {
+    const uint32_t lx0 = sub & 3u, lx1 = (sub >> 2) & 3u, ly0 = (sub >> 4) & 3u, ly1 = sub >> 6;
+    const uint32_t cols = (0xfu >> (3u - lx1 + lx0)) << lx0;  // bits lx0..lx1
+    const uint32_t rows = (0xfu >> (3u - ly1 + ly0)) << ly0;  // rows ly0..ly1
+    uint32_t m = 0u;
+#pragma unroll
+    for (int y = 0; y < kSt; y++)
+        if ((rows >> y) & 1u) m |= cols << (4 * y);
+    return m;
+}
+
+// entries [q0, q1) of super-tile s's list, segment `seg`
+__device__ __forceinline__ void seg_span(const Workspace &ws, uint32_t seg, uint32_t &s, uint32_t &e0, uint32_t &e1) {
+    s = ws.seg_st[seg];
+    const uint32_t q0 = (seg - ws.seg_first[s]) * (uint32_t)kSeg;
+    e0 = ws.st_start[s] + q0;
+    e1 = min(ws.st_start[s + 1], e0 + (uint32_t)kSeg);
+}
+
+// A segment is kSeg = kExpandThreads * kSegBatches entries; thread tid holds entries tid + b * kExpandThreads
+// (b < kSegBatches), all loaded up front.
+constexpr int kSegBatches = kSeg / kExpandThreads;
+static_assert(kSegBatches * kExpandThreads == kSeg, "segment tiling");
+
+__device__ __forceinline__ void load_segment(const Workspace &ws, uint32_t e0, uint32_t e1, uint32_t (&m)[kSegBatches],
+                                             uint32_t (&p)[kSegBatches]) {
+    uint2 e[kSegBatches];
+#pragma unroll
+    for (int b = 0; b < kSegBatches; b++) {
+        const uint32_t i = e0 + threadIdx.x + b * kExpandThreads;
+        e[b] = i < e1 ? ws.ent[i] : make_uint2(0u, 0u);
+    }
+#pragma unroll
+    for (int b = 0; b < kSegBatches; b++) {
+        const uint32_t i = e0 + threadIdx.x + b * kExpandThreads;
+        m[b] = i < e1 ? sub_mask(e[b].y) : 0u;
+        p[b] = e[b].x;
+    }
+}
+
+// Per list segment: its pairs per tile of the super-tile (one ballot per tile, batch and warp).
+__global__ void __launch_bounds__(kExpandThreads, 4) k_bin_segcount(Workspace ws) {
+    constexpr int NW = kExpandThreads / 32;
+    __shared__ uint32_t s_wc[NW][16];
+    const uint32_t n_seg = ws.counters[CNT_SEGS];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    for (uint32_t seg = blockIdx.x; seg < n_seg; seg += gridDim.x) {
+        uint32_t s, e0, e1;
+        seg_span(ws, seg, s, e0, e1);
+        uint32_t m[kSegBatches], p[kSegBatches];
+        load_segment(ws, e0, e1, m, p);
+        uint32_t c = 0;  // lane j < 16: this warp's pairs of tile j
+#pragma unroll
+        for (int b = 0; b < kSegBatches; b++)
+#pragma unroll
+            for (int j = 0; j < 16; j++) {
+                const uint32_t bb = __ballot_sync(0xffffffffu, (m[b] >> j) & 1u);
+                if (lane == j) c += __popc(bb);
+            }
+        if (lane < 16) s_wc[warp][lane] = c;
+        __syncthreads();
+        if (tid < 16) {
+            uint32_t t = 0;
+#pragma unroll
+            for (int w = 0; w < NW; w++) t += s_wc[w][tid];
+            ws.segcnt[(size_t)seg * 16 + tid] = t;
+        }
+        __syncthreads();
+    }
+}
+
+// a ballot the compiler may not merge with an identical earlier one (keeping 128 ballots live across the
+// barriers of k_bin_expand would spill)
+__device__ __forceinline__ uint32_t ballot_again(uint32_t pred) {
+    uint32_t r;
+    asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %1, 0;\n\tvote.sync.ballot.b32 %0, p, 0xffffffff;\n\t}"
+                 : "=r"(r)
+                 : "r"(pred));
+    return r;
+}
+
+// Per list segment: tile j's first slot = ranges[tile j].x + its head pairs + its pairs in the super-tile's
+// earlier segments.  The segment's entries are ordered (batch, warp, lane); per (batch, warp) tile counts
+// from one ballot each are scanned per tile, then every (batch, warp, tile) writes its pairs as one
+// coalesced run.
+__global__ void __launch_bounds__(kExpandThreads, 4) k_bin_expand(Workspace ws, BinGeom g) {
+    constexpr int NW = kExpandThreads / 32;
+    constexpr int NBW = kSegBatches * NW;  // (batch, warp) units of a segment
+    static_assert(NBW == 64, "the per-tile scan takes two units per lane");
+    __shared__ uint32_t s_cnt[16][NBW];  // [tile][batch * NW + warp]: pair count -> first slot
+    __shared__ uint32_t s_base[16];
+    __shared__ uint32_t s_part[kExpandThreads / 16][16];
+    const uint32_t n_seg = ws.counters[CNT_SEGS];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const unsigned lt = (1u << lane) - 1u;
+    for (uint32_t seg = blockIdx.x; seg < n_seg; seg += gridDim.x) {
+        uint32_t s, e0, e1;
+        seg_span(ws, seg, s, e0, e1);
+        uint32_t m[kSegBatches], p[kSegBatches];
+        load_segment(ws, e0, e1, m, p);
+        {  // pairs of tile j in earlier segments: thread (part, j) sums segments part, part + P, ...
+            constexpr int P = kExpandThreads / 16;
+            const int j = tid & 15, part = tid >> 4;
+            uint32_t t = 0;
+            for (uint32_t q = ws.seg_first[s] + part; q < seg; q += P) t += ws.segcnt[(size_t)q * 16 + j];
+            s_part[part][j] = t;
+        }
+#pragma unroll
+        for (int b = 0; b < kSegBatches; b++)
+#pragma unroll
+            for (int j = 0; j < 16; j++) {
+                const uint32_t bb = __ballot_sync(0xffffffffu, (m[b] >> j) & 1u);
+                if (lane == j) s_cnt[j][b * NW + warp] = __popc(bb);
+            }
+        __syncthreads();
+        if (tid < 16) {
+            uint32_t t = 0;
+#pragma unroll 8
+            for (int q = 0; q < kExpandThreads / 16; q++) t += s_part[q][tid];
+            const uint32_t tx = (s % g.stx) * kSt + (tid & 3), ty = (s / g.stx) * kSt + (tid >> 2);
+            const bool in = tx < (uint32_t)g.tiles_x && ty < (uint32_t)g.tiles_y;
+            const uint32_t t_id = ty * g.tiles_x + tx;
+            s_base[tid] = in ? ws.ranges[t_id].x + ws.head_cnt[t_id] + t : 0u;
+        }
+        __syncthreads();
+        // exclusive scan of every tile's 64 unit counts (warp w: tiles 2w, 2w + 1; lane: units 2l, 2l + 1)
+#pragma unroll
+        for (int h = 0; h < 2; h++) {
+            const int j = 2 * warp + h;
+            const uint32_t a0 = s_cnt[j][2 * lane], a1 = s_cnt[j][2 * lane + 1];
+            uint32_t incl = a0 + a1;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t v = __shfl_up_sync(0xffffffffu, incl, o);
+                if (lane >= o) incl += v;
+            }
+            const uint32_t ex = s_base[j] + incl - a0 - a1;
+            s_cnt[j][2 * lane] = ex;
+            s_cnt[j][2 * lane + 1] = ex + a0;
+        }
+        __syncthreads();
+#pragma unroll
+        for (int b = 0; b < kSegBatches; b++)
+#pragma unroll
+            for (int j = 0; j < 16; j++) {
+                const uint32_t bb = ballot_again((m[b] >> j) & 1u);
+                if ((m[b] >> j) & 1u) ws.pfinal[s_cnt[j][b * NW + warp] + __popc(bb & lt)] = p[b];
+            }
+        __syncthreads();  // s_cnt / s_base / s_part are rewritten by the next segment
+    }
+}
+
+// ---- head --------------------------------------------------------------------------
+
+// The nearest ranks (chunk 0) hold the scene's largest splats: on C3 its ~1.6K ranks carry 12 % of the
+// frame's pairs and 35x the average chunk's super-tile entries.  They precede every later rank in every
+// tile, so they are emitted per tile, not through the super-tile lists: one warp per tile walks the head
+// ranks in order (32 per ballot) and writes the ones covering its tile to ranges[tile].x + running count.
+__global__ void __launch_bounds__(256) k_bin_head(Workspace ws, BinGeom g) {
+    const int lane = threadIdx.x & 31;
+    const int t = blockIdx.x * 8 + (threadIdx.x >> 5);
+    const int n_tiles = g.tiles_x * g.tiles_y;
+    if (t >= n_tiles) return;
+    const bool over = ws.counters[CNT_OVERFLOW] != 0u;
+    const uint32_t n = (uint32_t)ws.stats_ptr[SEELE_STAT_BINNED];
+    uint32_t h0, h1;
+    chunk_range(n, (uint32_t)g.n_chunks, 0u, h0, h1);
+    const uint32_t tx = (uint32_t)(t % g.tiles_x), ty = (uint32_t)(t / g.tiles_x);
+    const uint32_t base = ws.ranges[t].x;
+    const uint32_t *srect = ws.drect[kDepthFinal];
+    const uint32_t *spos = ws.dval[kDepthFinal];
+    const unsigned lt = (1u << lane) - 1u;
+    uint32_t run = 0;
+    for (uint32_t r0 = h0; r0 < h1; r0 += 32) {
+        const uint32_t r = r0 + lane;
+        bool cov = false;
+        if (r < h1) {
+            const Rect rc = unpack_rect(srect[r]);
+            cov = tx >= rc.x0 && tx <= rc.x1 && ty >= rc.y0 && ty <= rc.y1;
+        }
+        const unsigned bb = __ballot_sync(0xffffffffu, cov);
+        if (cov && !over) ws.pfinal[base + run + __popc(bb & lt)] = spos[r];
+        run += __popc(bb);
+    }
+    if (lane == 0) ws.head_cnt[t] = run;
 }
 
 __global__ void k_fill_pair_tiles(const uint2 *ranges, int n_tiles, int32_t *pair_tile) {
@@ -590,27 +677,7 @@ __global__ void k_fill_pair_tiles(const uint2 *ranges, int n_tiles, int32_t *pai
     }
 }
 
-template <typename K>
-void set_smem(K kernel, size_t bytes) {
-    static bool done = false;  // per instantiation
-    if (!done) {
-        cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
-        done = true;
-    }
-}
-
-long long ceil_div(long long a, long long b) { return (a + b - 1) / b; }
-
-}  // namespace
-
-void launch_frame_begin(const Workspace &ws, const CamK &cam, int64_t *stats, cudaStream_t st) {
-    const int n_diff = (cam.tiles_x + 1) * (cam.tiles_y + 1);
-    const int grid = 256;  // (the depth histogram alone is 4 MB)
-    k_frame_begin<<<grid, 256, 0, st>>>(ws, stats, n_diff, cam.tiles_y);
-    note_launches(1);
-}
-
-static int sm_count_cached() {
+int sm_count_bin() {
     static int sms = 0;
     if (!sms) {
         int dev = 0;
@@ -621,41 +688,69 @@ static int sm_count_cached() {
     return sms;
 }
 
-void launch_binning(const Workspace &ws, long long n_max, long long cap, const CamK &cam, int64_t *stats,
-                    cudaStream_t st) {
-    const int sms = sm_count_cached();
-    const size_t diff_bytes = sizeof(int32_t) * (cam.tiles_x + 1) * (cam.tiles_y + 1);
-    const int use_smem = diff_bytes <= 160 * 1024;
-    const size_t scan_smem = use_smem ? diff_bytes : 0;
-    set_smem(k_pair_scan, 160 * 1024);
-#ifndef SEELE_SCAN_PER_SM2
-#define SEELE_SCAN_PER_SM2 2  // (half-SM units: one CTA per SM)
-#endif
-    const int scan_grid = (int)std::min<long long>(ceil_div(n_max, TILE), SEELE_SCAN_PER_SM2 * sms / 2);
-    k_pair_scan<<<scan_grid > 0 ? scan_grid : 1, NT, scan_smem, st>>>(ws, cam.tiles_x, cam.tiles_y, cap, use_smem,
-                                                                      stats);
-    set_smem(k_row_pass, sizeof(RowSmem));
-#ifndef SEELE_BIN_CTAS_PER_SM
-#define SEELE_BIN_CTAS_PER_SM 1  // one per SM: room for another frame's raster CTAs (pipelined 983 -> 994 FPS)
-#endif
-#ifndef SEELE_ROW_CTAS_PER_SM
-#define SEELE_ROW_CTAS_PER_SM SEELE_BIN_CTAS_PER_SM
-#endif
-#ifndef SEELE_COL_CTAS_PER_SM
-#define SEELE_COL_CTAS_PER_SM SEELE_BIN_CTAS_PER_SM
-#endif
-    const int persist = (int)(SEELE_ROW_CTAS_PER_SM * sms);  // resident CTAs (launch bounds allow two per SM)
-    k_row_pass<<<(int)std::min<long long>(ceil_div(cap, TILE), persist), NT, sizeof(RowSmem), st>>>(ws, stats);
-    set_smem(k_col_pass, sizeof(ColSmem));
-    const int persist_col = (int)(SEELE_COL_CTAS_PER_SM * sms);
-    k_col_pass<<<(int)std::min<long long>(ceil_div(cap, TILE) + cam.tiles_y, persist_col), NT, sizeof(ColSmem), st>>>(
-        ws, cam.tiles_x, cam.tiles_y);
-    note_launches(3);
+template <typename K>
+void set_smem(K kernel, size_t bytes) {
+    if (bytes > 48 * 1024) cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
 }
 
-#ifdef SEELE_SORT_TRACE
-void debug_trace(void *dst) { cudaMemcpyFromSymbol(dst, g_trace, sizeof(g_trace)); }
+}  // namespace
+
+BinGeom bin_geometry(long long n_max, int width, int height) {
+    BinGeom g;
+    g.tiles_x = (width + kTile - 1) / kTile;
+    g.tiles_y = (height + kTile - 1) / kTile;
+    g.stx = (g.tiles_x + kSt - 1) / kSt;
+    g.sty = (g.tiles_y + kSt - 1) / kSt;
+    g.n_st = g.stx * g.sty;
+    // chunks of ~2K ranks (fixed by n_max, not by the device, so the workspace size is too)
+    long long c = (n_max + kBinChunkRanks - 1) / kBinChunkRanks;
+    g.n_chunks = (int)(c < kBinChunksMin ? kBinChunksMin : (c > kBinChunksMax ? kBinChunksMax : c));
+    return g;
+}
+
+void launch_frame_begin(const Workspace &ws, const CamK &cam, int64_t *stats, cudaStream_t st) {
+    const int n_diff = (cam.tiles_x + 1) * (cam.tiles_y + 1);
+    const int grid = 256;  // (the depth histogram alone is 4 MB)
+    k_frame_begin<<<grid, 256, 0, st>>>(ws, stats, n_diff);
+    note_launches(1);
+}
+
+void launch_binning(const Workspace &ws, long long n_max, long long cap, const CamK &cam, int64_t *stats,
+                    cudaStream_t st) {
+    (void)stats;
+    const BinGeom g = bin_geometry(n_max, cam.width, cam.height);
+    const int sms = sm_count_bin();
+    const size_t n_sd = (size_t)(g.stx + 1) * (g.sty + 1);
+    const size_t diff_bytes = sizeof(int32_t) * (g.tiles_x + 1) * (g.tiles_y + 1);
+    const size_t sd_bytes = sizeof(int32_t) * n_sd;
+    const int count_diff_smem = kCountChunks * sd_bytes + diff_bytes <= 160 * 1024;
+    const size_t count_smem = kCountChunks * sd_bytes + (count_diff_smem ? diff_bytes : 0);
+    set_smem(k_bin_count, count_smem);
+    k_bin_count<<<(g.n_chunks + kCountChunks - 1) / kCountChunks, kCountThreads, count_smem, st>>>(ws, g,
+                                                                                                  count_diff_smem);
+    const int scan_diff_smem = diff_bytes <= 160 * 1024;
+    const size_t scan_smem = scan_diff_smem ? diff_bytes : 0;
+    set_smem(k_bin_scan, scan_smem);
+    k_bin_scan<<<(g.n_st + 31) / 32, kScanThreads, scan_smem, st>>>(ws, g, cap, scan_diff_smem);
+    const size_t split8 = 2 * 8 * sd_bytes;
+    if (split8 <= 128 * 1024) {
+        set_smem(k_bin_split<8>, split8);
+        k_bin_split<8><<<g.n_chunks, 8 * 32, split8, st>>>(ws, g);
+    } else {
+        const size_t split4 = 2 * 4 * sd_bytes;
+        set_smem(k_bin_split<4>, split4);
+        k_bin_split<4><<<g.n_chunks, 4 * 32, split4, st>>>(ws, g);
+    }
+#ifndef SEELE_EXPAND_PER_SM
+#define SEELE_EXPAND_PER_SM 4
 #endif
+    const long long max_seg = cap / kSeg + g.n_st + 1;
+    const int xgrid = (int)std::min<long long>(max_seg, (long long)SEELE_EXPAND_PER_SM * sms);
+    k_bin_head<<<(g.tiles_x * g.tiles_y + 7) / 8, 256, 0, st>>>(ws, g);
+    k_bin_segcount<<<xgrid, kExpandThreads, 0, st>>>(ws);
+    k_bin_expand<<<xgrid, kExpandThreads, 0, st>>>(ws, g);
+    note_launches(6);
+}
 
 void launch_fill_pair_tiles(const uint2 *ranges, int n_tiles, int32_t *pair_tile, cudaStream_t st) {
     k_fill_pair_tiles<<<n_tiles < 4096 ? n_tiles : 4096, 256, 0, st>>>(ranges, n_tiles, pair_tile);

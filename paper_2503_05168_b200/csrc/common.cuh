@@ -38,11 +38,10 @@ struct SceneK {
 // Scalar counters living in the workspace (device), zeroed by every frame.
 enum {
     CNT_WS = 0,           // assembled splats
-    CNT_ENTRIES = 1,      // row entries (one per binned splat and tile row it covers)
     CNT_PAIRS = 2,        // tile pairs (0 on overflow; the u64 count is in stats)
     CNT_OVERFLOW = 3,
-    CNT_DONE_SCAN = 6,    // last-block ticket of the pair scan
-    CNT_CHUNKS = 7,       // row chunks of the column pass
+    CNT_SEGS = 5,         // super-tile list segments of the expand pass
+    CNT_DONE_SCAN = 6,    // last-block ticket of the binning scan
     CNT_TICKET = 8,       // 16 per-pass tile tickets
     CNT_COUNT = 32
 };
@@ -53,12 +52,18 @@ enum {
 #ifndef SEELE_SORT_IPT
 #define SEELE_SORT_IPT 8
 #endif
-constexpr int kSortTile = SEELE_SORT_NT * SEELE_SORT_IPT;  // items per onesweep CTA tile (onesweep.cuh TILE)
-constexpr int kMaxTileAxis = 256;  // tiles per image axis (row / column digits fit one pass)
-constexpr int kLookScan = 0;       // look-back regions (pass ids)
-constexpr int kLookRows = 1;
-constexpr int kLookCols = 2;
-constexpr int kLookBuckets = 3;
+constexpr int kMaxTileAxis = 256;  // tiles per image axis (packed 8-bit tile rects)
+constexpr int kLookBuckets = 3;    // look-back region / epoch tag of the depth bucket scan
+
+// Binning (binning.cu): depth ranks cut into chunks of ~kBinChunkRanks, super-tiles of 4 x 4 tiles.
+constexpr long long kBinChunkRanks = 2048;
+constexpr int kBinChunksMin = 64;
+constexpr int kBinChunksMax = 4096;
+constexpr int kSeg = 2048;  // entries per super-tile list segment (expand pass)
+struct BinGeom {
+    int tiles_x, tiles_y, stx, sty, n_st, n_chunks;
+};
+BinGeom bin_geometry(long long n_max, int width, int height);
 
 // Depth order (depth.cu): buckets of the order-preserving fp64 bit pattern of
 // z above the near plane, 2^(52 - kDepthShift) = 65,536 per binade over 16
@@ -112,24 +117,22 @@ struct Workspace {
     uint32_t *gfirst;    // [n_max / kDepthGroup + 2]
     uint32_t *dval[2];
     uint32_t *drect[2];
-    // first row entry of each depth-ranked binned splat (+ sentinel) and first
-    // rank of each 4096-entry tile of the row pass
-    uint32_t *poff;
-    uint32_t *tile_r0;
-    // row entries grouped by tile row (row pass output): packed x0 | x1 << 8 |
-    // ty << 16, and the splat's assembled position
-    uint32_t *ent_x;
-    uint32_t *ent_p;
+    // binning (binning.cu): chunk x super-tile entry counts -> exclusive chunk bases; entries per super-tile,
+    // list offsets, heavy-first order; entries (position, sub-rectangle) grouped by super-tile in depth order
+    uint32_t *cmat;      // [n_chunks][n_st]
+    uint32_t *st_cnt;    // [n_st]
+    uint32_t *st_start;  // [n_st + 1]
+    uint32_t *seg_first; // [n_st + 1] first list segment of each super-tile
+    uint32_t *seg_st;    // [cap / kSeg + n_st + 1] super-tile of each segment
+    uint32_t *segcnt;    // [cap / kSeg + n_st + 1][16] pairs per tile of each segment
+    uint32_t *head_cnt;  // [tiles] pairs of the head ranks (chunk 0) per tile
+    uint2 *ent;          // [cap]
     uint32_t *pfinal;    // sorted pair -> assembled position (sort_intersections order)
     uint2 *ranges;       // per tile [start, end)
     uint32_t *tile_order;  // raster launch order: tiles by descending pair count (heavy tiles first)
     // scratch
-    unsigned long long *look;  // epoch-tagged look-back status words
-    long long look_tiles_d, look_tiles_p;  // tiles per depth / pair pass region
-    uint32_t *row_start; // [kMaxTileAxis + 1] first entry of each tile row
-    uint32_t *chunk_first;  // [kMaxTileAxis + 1] first column-pass chunk of each row
+    unsigned long long *look;  // epoch-tagged look-back status words (depth bucket scan)
     int32_t *tile_diff;  // [(tiles_y + 1) x (tiles_x + 1)] 2D difference array of tile counts
-    int32_t *row_diff;   // [tiles_y + 1] entries per row (difference array)
     uint32_t *counters;  // CNT_COUNT
     uint32_t *epoch;     // frame epoch (never cleared)
     unsigned long long *pairs64;  // total tile pairs (u64)
@@ -138,11 +141,7 @@ struct Workspace {
     int64_t *stats_ptr;  // the frame's stats vector (set by seele_render)
     __device__ __forceinline__ long long counters_binned() const { return stats_ptr[SEELE_STAT_BINNED]; }
 
-    __device__ __forceinline__ unsigned long long *look_region(int pass) const {
-        if (pass == kLookScan) return look;
-        if (pass == kLookBuckets) return look + look_tiles_d + 2 * (size_t)look_tiles_p * 256;
-        return look + look_tiles_d + (size_t)(pass - kLookRows) * look_tiles_p * 256;
-    }
+    __device__ __forceinline__ unsigned long long *look_region(int) const { return look; }
 };
 
 Workspace carve_workspace(void *base, long long n_max, long long cap, int width, int height);
@@ -158,7 +157,7 @@ void launch_select(const CamK &cam, const double *centroids, int n, int m, doubl
 void launch_frame_begin(const Workspace &ws, const CamK &cam, int64_t *stats, cudaStream_t st);
 // exact (depth, position) order of the binned splats (depth.cu).
 void launch_depth_sort(const Workspace &ws, const CamK &cam, long long n_max, int64_t *stats, cudaStream_t st);
-// pair offsets, emission + tile sort, ranges; final pair -> position in ws.pfinal.
+// tile pairs in sort_intersections order: ranges, final pair -> position in ws.pfinal.
 void launch_binning(const Workspace &ws, long long n_max, long long cap, const CamK &cam, int64_t *stats,
                     cudaStream_t st);
 void launch_raster(const Workspace &ws, const uint32_t *pair_pos, const CamK &cam,
