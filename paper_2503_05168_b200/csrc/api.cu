@@ -158,7 +158,7 @@ Workspace carve_workspace(void *base, long long n_max, long long cap, int width,
     w.st_start = c.take<uint32_t>(g.n_st + 1);
     w.seg_first = c.take<uint32_t>(g.n_st + 1);
     w.seg_st = c.take<uint32_t>(cap / kSeg + g.n_st + 1);
-    w.segcnt = c.take<uint32_t>((cap / kSeg + g.n_st + 1) * 16);
+    w.seg_look = c.take<unsigned long long>((cap / kSeg + g.n_st + 1) * 16);
     w.ent = c.take<uint2>(cap);
     w.head_cnt = c.take<uint32_t>(tiles);
     w.pfinal = c.take<uint32_t>(cap);

@@ -26,12 +26,13 @@
 //   head    k_bin_head: chunk 0 -- the nearest, largest splats -- is not put
 //           in the lists; one warp per tile pulls its pairs (they precede
 //           every later rank in the tile).
-//   expand  k_bin_segcount counts every segment's pairs per tile (ballots);
-//           k_bin_expand walks a segment in batches: every entry covers a
-//           subset of the super-tile's 16 tiles, one ballot per tile ranks it
-//           among the batch's warps, and the pairs are written with one
-//           coalesced store per tile into ranges[tile].x + head pairs + pairs
-//           of that tile in earlier segments + running count.
+//   expand  k_bin_expand takes the lists in segments of kSeg entries: every
+//           entry covers a subset of the super-tile's 16 tiles, one ballot
+//           per tile ranks it among the segment's warps, a decoupled look-back
+//           along the super-tile's segments adds the pairs of earlier
+//           segments, and the pairs are written with one coalesced store per
+//           tile into ranges[tile].x + head pairs + earlier segments' pairs +
+//           running count.
 //
 // Every size is read from device memory: a frame needs no host round trip.
 #include <algorithm>
@@ -125,50 +126,64 @@ __device__ __forceinline__ void warp_prefix2d(T *a, int nx, int ny, int stride) 
     __syncwarp();
 }
 
-// One CTA per kCountChunks consecutive chunks (one warp each for the prefix).  Shared memory: per chunk a
-// 2D difference array over the super-tile grid (-> entries per super-tile), then (if it fits) the CTA's one
-// over the tile grid, flushed into the frame's by atomics on its nonzero cells.  Four shared-memory atomics
-// per splat each, whatever its size.  Chunk 0 is the head (k_bin_head): no super-tile entries.
-constexpr int kCountChunks = kCountThreads / 32;
+// One CTA per g.count_group (<= kCountMaxGroup) consecutive chunks, one warp per chunk for the prefix.
+// Shared memory: per chunk a 2D difference array over the super-tile grid (-> entries per super-tile),
+// then (if it fits) the CTA's one over the tile grid, flushed into the frame's by atomics on its nonzero
+// cells.  Four shared-memory atomics per splat each, whatever its size.  Chunk 0 is the head
+// (k_bin_head): no super-tile entries.
+constexpr int kCountMaxGroup = kCountThreads / 32;
+constexpr int kCountUnroll = 4;  // rects in flight per thread
 __global__ void __launch_bounds__(kCountThreads) k_bin_count(Workspace ws, BinGeom g, int diff_in_smem) {
-    extern __shared__ int32_t s_cnt[];  // [kCountChunks][(sty + 1) * (stx + 1)] then [(tiles_y + 1) * (tiles_x + 1)]
+    extern __shared__ int32_t s_cnt[];  // [group][(sty + 1) * (stx + 1)] then [(tiles_y + 1) * (tiles_x + 1)]
+    const int G = g.count_group;
     const int sx1 = g.stx + 1, n_sd = sx1 * (g.sty + 1);
-    int32_t *s_diff = s_cnt + kCountChunks * n_sd;
+    int32_t *s_diff = s_cnt + G * n_sd;
     const int tid = threadIdx.x, warp = tid >> 5;
     const int tx1 = g.tiles_x + 1, n_diff = tx1 * (g.tiles_y + 1);
-    for (int i = tid; i < kCountChunks * n_sd; i += kCountThreads) s_cnt[i] = 0;
+    for (int i = tid; i < G * n_sd; i += kCountThreads) s_cnt[i] = 0;
     if (diff_in_smem)
         for (int i = tid; i < n_diff; i += kCountThreads) s_diff[i] = 0;
     __syncthreads();
     int32_t *diff = diff_in_smem ? s_diff : ws.tile_diff;
     const uint32_t n = (uint32_t)ws.stats_ptr[SEELE_STAT_BINNED];
     const uint32_t C = (uint32_t)g.n_chunks, K = (n + C - 1) / C;
-    const uint32_t c0 = blockIdx.x * kCountChunks;
-    const uint32_t r0 = min(n, c0 * K), r1 = min(n, r0 + kCountChunks * K);
+    const uint32_t c0 = blockIdx.x * (uint32_t)G;
+    const uint32_t r0 = min(n, c0 * K), r1 = min(n, r0 + (uint32_t)G * K);
     const uint32_t *srect = ws.drect[kDepthFinal];
     unsigned long long pairs = 0ull;
-    for (uint32_t r = r0 + tid; r < r1; r += kCountThreads) {
-        const Rect rc = unpack_rect(srect[r]);
-        pairs += (unsigned long long)((rc.x1 - rc.x0 + 1) * (rc.y1 - rc.y0 + 1));
-        atomicAdd(&diff[rc.y0 * tx1 + rc.x0], 1);
-        atomicAdd(&diff[rc.y0 * tx1 + rc.x1 + 1], -1);
-        atomicAdd(&diff[(rc.y1 + 1) * tx1 + rc.x0], -1);
-        atomicAdd(&diff[(rc.y1 + 1) * tx1 + rc.x1 + 1], 1);
-        const uint32_t c = r / K;
-        if (c == 0) continue;  // the head: emitted per tile (k_bin_head), not in the lists
-        int32_t *sd = s_cnt + (c - c0) * n_sd;
-        const StRect sr = st_rect(rc);
-        atomicAdd(&sd[sr.y0 * sx1 + sr.x0], 1);
-        atomicAdd(&sd[sr.y0 * sx1 + sr.x1 + 1], -1);
-        atomicAdd(&sd[(sr.y1 + 1) * sx1 + sr.x0], -1);
-        atomicAdd(&sd[(sr.y1 + 1) * sx1 + sr.x1 + 1], 1);
+    for (uint32_t rb = r0 + tid; rb < r1; rb += kCountUnroll * kCountThreads) {
+        uint32_t v[kCountUnroll];
+#pragma unroll
+        for (int u = 0; u < kCountUnroll; u++) {
+            const uint32_t r = rb + u * kCountThreads;
+            v[u] = r < r1 ? srect[r] : 0u;
+        }
+#pragma unroll
+        for (int u = 0; u < kCountUnroll; u++) {
+            const uint32_t r = rb + u * kCountThreads;
+            if (r >= r1) break;
+            const Rect rc = unpack_rect(v[u]);
+            pairs += (unsigned long long)((rc.x1 - rc.x0 + 1) * (rc.y1 - rc.y0 + 1));
+            atomicAdd(&diff[rc.y0 * tx1 + rc.x0], 1);
+            atomicAdd(&diff[rc.y0 * tx1 + rc.x1 + 1], -1);
+            atomicAdd(&diff[(rc.y1 + 1) * tx1 + rc.x0], -1);
+            atomicAdd(&diff[(rc.y1 + 1) * tx1 + rc.x1 + 1], 1);
+            const uint32_t c = r / K;
+            if (c == 0) continue;  // the head: emitted per tile (k_bin_head), not in the lists
+            int32_t *sd = s_cnt + (c - c0) * n_sd;
+            const StRect sr = st_rect(rc);
+            atomicAdd(&sd[sr.y0 * sx1 + sr.x0], 1);
+            atomicAdd(&sd[sr.y0 * sx1 + sr.x1 + 1], -1);
+            atomicAdd(&sd[(sr.y1 + 1) * sx1 + sr.x0], -1);
+            atomicAdd(&sd[(sr.y1 + 1) * sx1 + sr.x1 + 1], 1);
+        }
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) pairs += __shfl_xor_sync(0xffffffffu, pairs, o);
     if ((tid & 31) == 0 && pairs) atomicAdd(ws.pairs64, pairs);
     __syncthreads();
     const uint32_t c = c0 + warp;
-    if (c < C) {
+    if (warp < G && c < C) {
         int32_t *sd = s_cnt + warp * n_sd;
         warp_prefix2d(sd, g.stx, g.sty, sx1);
         uint32_t *row = ws.cmat + (size_t)c * g.n_st;
@@ -203,12 +218,12 @@ __global__ void __launch_bounds__(kScanThreads) k_bin_scan(Workspace ws, BinGeom
         uint32_t sum = 0;
         {
             int c = c0;
-            for (; c + 8 <= c1; c += 8) {
-                uint32_t v[8];
+            for (; c + 16 <= c1; c += 16) {
+                uint32_t v[16];
 #pragma unroll
-                for (int u = 0; u < 8; u++) v[u] = ok ? col[(size_t)(c + u) * g.n_st] : 0u;
+                for (int u = 0; u < 16; u++) v[u] = ok ? col[(size_t)(c + u) * g.n_st] : 0u;
 #pragma unroll
-                for (int u = 0; u < 8; u++) sum += v[u];
+                for (int u = 0; u < 16; u++) sum += v[u];
             }
             for (; c < c1; c++) sum += ok ? col[(size_t)c * g.n_st] : 0u;
         }
@@ -227,12 +242,12 @@ __global__ void __launch_bounds__(kScanThreads) k_bin_scan(Workspace ws, BinGeom
         if (ok) {
             uint32_t run = s_seg[warp][lane];
             int c = c0;
-            for (; c + 8 <= c1; c += 8) {
-                uint32_t v[8];
+            for (; c + 16 <= c1; c += 16) {
+                uint32_t v[16];
 #pragma unroll
-                for (int u = 0; u < 8; u++) v[u] = col[(size_t)(c + u) * g.n_st];
+                for (int u = 0; u < 16; u++) v[u] = col[(size_t)(c + u) * g.n_st];
 #pragma unroll
-                for (int u = 0; u < 8; u++) {
+                for (int u = 0; u < 16; u++) {
                     col[(size_t)(c + u) * g.n_st] = run;
                     run += v[u];
                 }
@@ -443,14 +458,14 @@ __global__ void __launch_bounds__(NW * 32) k_bin_split(Workspace ws, BinGeom g) 
         const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
         for (uint32_t ib = 0; ib < total; ib += 32) {
             const uint32_t item = ib + lane;
-            // owner: the lane whose [excl, incl) holds the item (first lane with incl > item)
-            int owner = 0;
-#pragma unroll
-            for (int step = 16; step > 0; step >>= 1) {
-                const uint32_t v = __shfl_sync(0xffffffffu, incl, owner + step - 1);
-                if (v <= item) owner += step;
-            }
-            owner = min(owner, 31);
+            // owner: the lane whose [excl, incl) holds the item.  Lanes own consecutive item ranges
+            // (every valid rank touches >= 1 super-tile; the invalid lanes are the last ones), so the owner
+            // of item ib is the number of lanes ending at or before ib, and each later item of the block
+            // advances it by the lanes starting in between.
+            const uint32_t owner0 = __popc(__ballot_sync(0xffffffffu, incl <= ib));
+            const uint32_t starts =
+                __reduce_or_sync(0xffffffffu, (excl > ib && excl < ib + 32u && nst) ? 1u << (excl - ib) : 0u);
+            const int owner = (int)min(31u, owner0 + __popc(starts & ((2u << lane) - 1u)));
             const uint32_t o_excl = __shfl_sync(0xffffffffu, excl, owner);
             const uint32_t o_rect = __shfl_sync(0xffffffffu, rcw, owner);
             const uint32_t o_pos = __shfl_sync(0xffffffffu, p, owner);
@@ -459,7 +474,8 @@ __global__ void __launch_bounds__(NW * 32) k_bin_split(Workspace ws, BinGeom g) 
             const StRect osr = st_rect(orc);
             const uint32_t osw = osr.x1 - osr.x0 + 1;
             const uint32_t k = item - o_excl;
-            const uint32_t ky = k / osw;
+            // k / osw: exact in float (k < 2^16, osw <= 64: the error is far below the 0.5 / osw margin)
+            const uint32_t ky = (uint32_t)(((float)k + 0.5f) * __frcp_rn((float)osw));
             const uint32_t sx = osr.x0 + (k - ky * osw), sy = osr.y0 + ky;
             const uint32_t sd = sy * sx1 + sx;
             const uint32_t obit = 1u << owner;
@@ -523,37 +539,6 @@ __device__ __forceinline__ void load_segment(const Workspace &ws, uint32_t e0, u
     }
 }
 
-// Per list segment: its pairs per tile of the super-tile (one ballot per tile, batch and warp).
-__global__ void __launch_bounds__(kExpandThreads, 4) k_bin_segcount(Workspace ws) {
-    constexpr int NW = kExpandThreads / 32;
-    __shared__ uint32_t s_wc[NW][16];
-    const uint32_t n_seg = ws.counters[CNT_SEGS];
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    for (uint32_t seg = blockIdx.x; seg < n_seg; seg += gridDim.x) {
-        uint32_t s, e0, e1;
-        seg_span(ws, seg, s, e0, e1);
-        uint32_t m[kSegBatches], p[kSegBatches];
-        load_segment(ws, e0, e1, m, p);
-        uint32_t c = 0;  // lane j < 16: this warp's pairs of tile j
-#pragma unroll
-        for (int b = 0; b < kSegBatches; b++)
-#pragma unroll
-            for (int j = 0; j < 16; j++) {
-                const uint32_t bb = __ballot_sync(0xffffffffu, (m[b] >> j) & 1u);
-                if (lane == j) c += __popc(bb);
-            }
-        if (lane < 16) s_wc[warp][lane] = c;
-        __syncthreads();
-        if (tid < 16) {
-            uint32_t t = 0;
-#pragma unroll
-            for (int w = 0; w < NW; w++) t += s_wc[w][tid];
-            ws.segcnt[(size_t)seg * 16 + tid] = t;
-        }
-        __syncthreads();
-    }
-}
-
 // a ballot the compiler may not merge with an identical earlier one (keeping 128 ballots live across the
 // barriers of k_bin_expand would spill)
 __device__ __forceinline__ uint32_t ballot_again(uint32_t pred) {
@@ -564,32 +549,33 @@ __device__ __forceinline__ uint32_t ballot_again(uint32_t pred) {
     return r;
 }
 
-// Per list segment: tile j's first slot = ranges[tile j].x + its head pairs + its pairs in the super-tile's
-// earlier segments.  The segment's entries are ordered (batch, warp, lane); per (batch, warp) tile counts
+// Per list segment (taken by ticket, so every lower segment is running or done): tile j's first slot =
+// ranges[tile j].x + its head pairs + its pairs in the super-tile's earlier segments, the last by a
+// decoupled look-back (16 columns, one per tile) along the super-tile's segments -- its first segment
+// starts the chain.  The segment's entries are ordered (batch, warp, lane); per (batch, warp) tile counts
 // from one ballot each are scanned per tile, then every (batch, warp, tile) writes its pairs as one
 // coalesced run.
 __global__ void __launch_bounds__(kExpandThreads, 4) k_bin_expand(Workspace ws, BinGeom g) {
     constexpr int NW = kExpandThreads / 32;
     constexpr int NBW = kSegBatches * NW;  // (batch, warp) units of a segment
     static_assert(NBW == 64, "the per-tile scan takes two units per lane");
-    __shared__ uint32_t s_cnt[16][NBW];  // [tile][batch * NW + warp]: pair count -> first slot
+    __shared__ uint32_t s_cnt[16][NBW];  // [tile][batch * NW + warp]: pair count -> offset in the segment
+    __shared__ uint32_t s_tot[16];
     __shared__ uint32_t s_base[16];
-    __shared__ uint32_t s_part[kExpandThreads / 16][16];
+    __shared__ uint32_t s_seg;
     const uint32_t n_seg = ws.counters[CNT_SEGS];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const unsigned lt = (1u << lane) - 1u;
-    for (uint32_t seg = blockIdx.x; seg < n_seg; seg += gridDim.x) {
+    const uint32_t epoch = *ws.epoch * 16u + kLookSegs;
+    while (true) {
+        if (tid == 0) s_seg = atomicAdd(&ws.counters[CNT_TICKET], 1u);
+        __syncthreads();
+        const uint32_t seg = s_seg;
+        if (seg >= n_seg) break;
         uint32_t s, e0, e1;
         seg_span(ws, seg, s, e0, e1);
         uint32_t m[kSegBatches], p[kSegBatches];
         load_segment(ws, e0, e1, m, p);
-        {  // pairs of tile j in earlier segments: thread (part, j) sums segments part, part + P, ...
-            constexpr int P = kExpandThreads / 16;
-            const int j = tid & 15, part = tid >> 4;
-            uint32_t t = 0;
-            for (uint32_t q = ws.seg_first[s] + part; q < seg; q += P) t += ws.segcnt[(size_t)q * 16 + j];
-            s_part[part][j] = t;
-        }
 #pragma unroll
         for (int b = 0; b < kSegBatches; b++)
 #pragma unroll
@@ -597,16 +583,6 @@ __global__ void __launch_bounds__(kExpandThreads, 4) k_bin_expand(Workspace ws, 
                 const uint32_t bb = __ballot_sync(0xffffffffu, (m[b] >> j) & 1u);
                 if (lane == j) s_cnt[j][b * NW + warp] = __popc(bb);
             }
-        __syncthreads();
-        if (tid < 16) {
-            uint32_t t = 0;
-#pragma unroll 8
-            for (int q = 0; q < kExpandThreads / 16; q++) t += s_part[q][tid];
-            const uint32_t tx = (s % g.stx) * kSt + (tid & 3), ty = (s / g.stx) * kSt + (tid >> 2);
-            const bool in = tx < (uint32_t)g.tiles_x && ty < (uint32_t)g.tiles_y;
-            const uint32_t t_id = ty * g.tiles_x + tx;
-            s_base[tid] = in ? ws.ranges[t_id].x + ws.head_cnt[t_id] + t : 0u;
-        }
         __syncthreads();
         // exclusive scan of every tile's 64 unit counts (warp w: tiles 2w, 2w + 1; lane: units 2l, 2l + 1)
 #pragma unroll
@@ -619,9 +595,25 @@ __global__ void __launch_bounds__(kExpandThreads, 4) k_bin_expand(Workspace ws, 
                 const uint32_t v = __shfl_up_sync(0xffffffffu, incl, o);
                 if (lane >= o) incl += v;
             }
-            const uint32_t ex = s_base[j] + incl - a0 - a1;
+            const uint32_t ex = incl - a0 - a1;
             s_cnt[j][2 * lane] = ex;
             s_cnt[j][2 * lane + 1] = ex + a0;
+            if (lane == 31) s_tot[j] = incl;
+        }
+        __syncthreads();
+        if (tid < 16) {
+            const uint32_t prev = sweep::lookback(ws.seg_look + tid, 16, seg, epoch, s_tot[tid], seg == ws.seg_first[s]);
+            const uint32_t tx = (s % g.stx) * kSt + (tid & 3), ty = (s / g.stx) * kSt + (tid >> 2);
+            const bool in = tx < (uint32_t)g.tiles_x && ty < (uint32_t)g.tiles_y;
+            const uint32_t t_id = ty * g.tiles_x + tx;
+            s_base[tid] = in ? ws.ranges[t_id].x + ws.head_cnt[t_id] + prev : 0u;
+        }
+        __syncthreads();
+#pragma unroll
+        for (int h = 0; h < 2; h++) {  // unit offsets -> absolute slots
+            const int j = 2 * warp + h;
+            s_cnt[j][2 * lane] += s_base[j];
+            s_cnt[j][2 * lane + 1] += s_base[j];
         }
         __syncthreads();
 #pragma unroll
@@ -631,43 +623,88 @@ __global__ void __launch_bounds__(kExpandThreads, 4) k_bin_expand(Workspace ws, 
                 const uint32_t bb = ballot_again((m[b] >> j) & 1u);
                 if ((m[b] >> j) & 1u) ws.pfinal[s_cnt[j][b * NW + warp] + __popc(bb & lt)] = p[b];
             }
-        __syncthreads();  // s_cnt / s_base / s_part are rewritten by the next segment
+        __syncthreads();  // s_cnt / s_base / s_seg are rewritten by the next segment
     }
 }
 
 // ---- head --------------------------------------------------------------------------
 
-// The nearest ranks (chunk 0) hold the scene's largest splats: on C3 its ~1.6K ranks carry 12 % of the
-// frame's pairs and 35x the average chunk's super-tile entries.  They precede every later rank in every
+// The nearest ranks (chunk 0) hold the scene's largest splats: on C3 its ~3.3K ranks carry 12 % of the
+// frame's pairs and 22x the average chunk's super-tile entries.  They precede every later rank in every
 // tile, so they are emitted per tile, not through the super-tile lists: one warp per tile walks the head
-// ranks in order (32 per ballot) and writes the ones covering its tile to ranges[tile].x + running count.
-__global__ void __launch_bounds__(256) k_bin_head(Workspace ws, BinGeom g) {
-    const int lane = threadIdx.x & 31;
-    const int t = blockIdx.x * 8 + (threadIdx.x >> 5);
-    const int n_tiles = g.tiles_x * g.tiles_y;
-    if (t >= n_tiles) return;
+// ranks in order (32 per ballot) and writes the ones covering its tile to ranges[tile].x + running count,
+// after its CTA (one per super-tile) compacted the head ranks touching the super-tile into shared memory.
+constexpr int kHeadThreads = 512;   // one CTA per super-tile, one warp per tile
+constexpr int kHeadWindow = 4096;   // head ranks compacted per window
+__global__ void __launch_bounds__(kHeadThreads) k_bin_head(Workspace ws, BinGeom g) {
+    __shared__ uint32_t s_rect[kHeadWindow];  // the window's ranks touching this super-tile, in rank order
+    __shared__ uint32_t s_idx[kHeadWindow];
+    __shared__ uint32_t s_wn[kHeadThreads / 32];
+    __shared__ uint32_t s_n;
+    constexpr int NW = kHeadThreads / 32;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const uint32_t sx = blockIdx.x % (uint32_t)g.stx, sy = blockIdx.x / (uint32_t)g.stx;
+    const uint32_t bx0 = sx * kSt, by0 = sy * kSt, bx1 = bx0 + kSt - 1, by1 = by0 + kSt - 1;
+    const uint32_t tx = bx0 + (warp & 3), ty = by0 + (warp >> 2);  // this warp's tile
+    const bool tile_ok = tx < (uint32_t)g.tiles_x && ty < (uint32_t)g.tiles_y;
+    const uint32_t t = ty * g.tiles_x + tx;
     const bool over = ws.counters[CNT_OVERFLOW] != 0u;
     const uint32_t n = (uint32_t)ws.stats_ptr[SEELE_STAT_BINNED];
     uint32_t h0, h1;
     chunk_range(n, (uint32_t)g.n_chunks, 0u, h0, h1);
-    const uint32_t tx = (uint32_t)(t % g.tiles_x), ty = (uint32_t)(t / g.tiles_x);
-    const uint32_t base = ws.ranges[t].x;
     const uint32_t *srect = ws.drect[kDepthFinal];
     const uint32_t *spos = ws.dval[kDepthFinal];
+    const uint32_t base = tile_ok ? ws.ranges[t].x : 0u;
     const unsigned lt = (1u << lane) - 1u;
     uint32_t run = 0;
-    for (uint32_t r0 = h0; r0 < h1; r0 += 32) {
-        const uint32_t r = r0 + lane;
-        bool cov = false;
-        if (r < h1) {
-            const Rect rc = unpack_rect(srect[r]);
-            cov = tx >= rc.x0 && tx <= rc.x1 && ty >= rc.y0 && ty <= rc.y1;
+    for (uint32_t w0 = h0; w0 < h1; w0 += kHeadWindow) {
+        const uint32_t w1 = min(h1, w0 + kHeadWindow);
+        // compact the window's ranks touching the super-tile (rank order: rounds of NW x 32 ranks)
+        uint32_t cnt = 0;
+        for (uint32_t r0 = w0; r0 < w1; r0 += kHeadThreads) {
+            const uint32_t r = r0 + tid;
+            uint32_t v = 0u;
+            bool hit = false;
+            if (r < w1) {
+                v = srect[r];
+                const Rect rc = unpack_rect(v);
+                hit = rc.x0 <= bx1 && rc.x1 >= bx0 && rc.y0 <= by1 && rc.y1 >= by0;
+            }
+            const unsigned bb = __ballot_sync(0xffffffffu, hit);
+            if (lane == 0) s_wn[warp] = __popc(bb);
+            __syncthreads();
+            uint32_t before = 0, all = 0;
+#pragma unroll
+            for (int w = 0; w < NW; w++) {
+                const uint32_t c = s_wn[w];
+                before += w < warp ? c : 0u;
+                all += c;
+            }
+            if (hit) {
+                const uint32_t k = cnt + before + __popc(bb & lt);
+                s_rect[k] = v;
+                s_idx[k] = r;
+            }
+            cnt += all;
+            __syncthreads();
         }
-        const unsigned bb = __ballot_sync(0xffffffffu, cov);
-        if (cov && !over) ws.pfinal[base + run + __popc(bb & lt)] = spos[r];
-        run += __popc(bb);
+        // every tile walks the compacted list
+        if (tile_ok) {
+            for (uint32_t i0 = 0; i0 < cnt; i0 += 32) {
+                const uint32_t i = i0 + lane;
+                bool cov = false;
+                if (i < cnt) {
+                    const Rect rc = unpack_rect(s_rect[i]);
+                    cov = tx >= rc.x0 && tx <= rc.x1 && ty >= rc.y0 && ty <= rc.y1;
+                }
+                const unsigned bb = __ballot_sync(0xffffffffu, cov);
+                if (cov && !over) ws.pfinal[base + run + __popc(bb & lt)] = spos[s_idx[i]];
+                run += __popc(bb);
+            }
+        }
+        __syncthreads();  // the lists are rewritten by the next window
     }
-    if (lane == 0) ws.head_cnt[t] = run;
+    if (tile_ok && lane == 0) ws.head_cnt[t] = run;
 }
 
 __global__ void k_fill_pair_tiles(const uint2 *ranges, int n_tiles, int32_t *pair_tile) {
@@ -688,6 +725,8 @@ int sm_count_bin() {
     return sms;
 }
 
+long long ceil_div(long long a, long long b) { return (a + b - 1) / b; }
+
 template <typename K>
 void set_smem(K kernel, size_t bytes) {
     if (bytes > 48 * 1024) cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
@@ -705,6 +744,7 @@ BinGeom bin_geometry(long long n_max, int width, int height) {
     // chunks of ~2K ranks (fixed by n_max, not by the device, so the workspace size is too)
     long long c = (n_max + kBinChunkRanks - 1) / kBinChunkRanks;
     g.n_chunks = (int)(c < kBinChunksMin ? kBinChunksMin : (c > kBinChunksMax ? kBinChunksMax : c));
+    g.count_group = 1;
     return g;
 }
 
@@ -723,11 +763,12 @@ void launch_binning(const Workspace &ws, long long n_max, long long cap, const C
     const size_t n_sd = (size_t)(g.stx + 1) * (g.sty + 1);
     const size_t diff_bytes = sizeof(int32_t) * (g.tiles_x + 1) * (g.tiles_y + 1);
     const size_t sd_bytes = sizeof(int32_t) * n_sd;
-    const int count_diff_smem = kCountChunks * sd_bytes + diff_bytes <= 160 * 1024;
-    const size_t count_smem = kCountChunks * sd_bytes + (count_diff_smem ? diff_bytes : 0);
+    BinGeom gc = g;  // count: groups of chunks per CTA, ~2 CTAs per SM (fewer flushes of the tile difference array)
+    gc.count_group = (int)std::max<long long>(1, std::min<long long>(kCountMaxGroup, ceil_div(g.n_chunks, 2 * sms)));
+    const int count_diff_smem = gc.count_group * sd_bytes + diff_bytes <= 160 * 1024;
+    const size_t count_smem = gc.count_group * sd_bytes + (count_diff_smem ? diff_bytes : 0);
     set_smem(k_bin_count, count_smem);
-    k_bin_count<<<(g.n_chunks + kCountChunks - 1) / kCountChunks, kCountThreads, count_smem, st>>>(ws, g,
-                                                                                                  count_diff_smem);
+    k_bin_count<<<(int)ceil_div(g.n_chunks, gc.count_group), kCountThreads, count_smem, st>>>(ws, gc, count_diff_smem);
     const int scan_diff_smem = diff_bytes <= 160 * 1024;
     const size_t scan_smem = scan_diff_smem ? diff_bytes : 0;
     set_smem(k_bin_scan, scan_smem);
@@ -746,10 +787,9 @@ void launch_binning(const Workspace &ws, long long n_max, long long cap, const C
 #endif
     const long long max_seg = cap / kSeg + g.n_st + 1;
     const int xgrid = (int)std::min<long long>(max_seg, (long long)SEELE_EXPAND_PER_SM * sms);
-    k_bin_head<<<(g.tiles_x * g.tiles_y + 7) / 8, 256, 0, st>>>(ws, g);
-    k_bin_segcount<<<xgrid, kExpandThreads, 0, st>>>(ws);
+    k_bin_head<<<g.n_st, kHeadThreads, 0, st>>>(ws, g);
     k_bin_expand<<<xgrid, kExpandThreads, 0, st>>>(ws, g);
-    note_launches(6);
+    note_launches(5);
 }
 
 void launch_fill_pair_tiles(const uint2 *ranges, int n_tiles, int32_t *pair_tile, cudaStream_t st) {

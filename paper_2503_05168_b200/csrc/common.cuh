@@ -53,15 +53,18 @@ enum {
 #define SEELE_SORT_IPT 8
 #endif
 constexpr int kMaxTileAxis = 256;  // tiles per image axis (packed 8-bit tile rects)
-constexpr int kLookBuckets = 3;    // look-back region / epoch tag of the depth bucket scan
+constexpr int kLookBuckets = 3;    // look-back epoch tag of the depth bucket scan
+constexpr int kLookSegs = 4;       // look-back epoch tag of the binning expand pass
 
-// Binning (binning.cu): depth ranks cut into chunks of ~kBinChunkRanks, super-tiles of 4 x 4 tiles.
-constexpr long long kBinChunkRanks = 2048;
+// Binning (binning.cu): depth ranks cut into chunks of ~kBinChunkRanks (at least kBinChunksMin), super-tiles
+// of 4 x 4 tiles.
+constexpr long long kBinChunkRanks = 4096;
 constexpr int kBinChunksMin = 64;
 constexpr int kBinChunksMax = 4096;
 constexpr int kSeg = 2048;  // entries per super-tile list segment (expand pass)
 struct BinGeom {
     int tiles_x, tiles_y, stx, sty, n_st, n_chunks;
+    int count_group;  // chunks per k_bin_count CTA
 };
 BinGeom bin_geometry(long long n_max, int width, int height);
 
@@ -124,7 +127,7 @@ struct Workspace {
     uint32_t *st_start;  // [n_st + 1]
     uint32_t *seg_first; // [n_st + 1] first list segment of each super-tile
     uint32_t *seg_st;    // [cap / kSeg + n_st + 1] super-tile of each segment
-    uint32_t *segcnt;    // [cap / kSeg + n_st + 1][16] pairs per tile of each segment
+    unsigned long long *seg_look;  // [cap / kSeg + n_st + 1][16] epoch-tagged look-back words (never cleared)
     uint32_t *head_cnt;  // [tiles] pairs of the head ranks (chunk 0) per tile
     uint2 *ent;          // [cap]
     uint32_t *pfinal;    // sorted pair -> assembled position (sort_intersections order)
