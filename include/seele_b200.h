@@ -65,7 +65,10 @@ typedef struct seele_config {
 
 enum {
     SEELE_PRECISION_FAST = 0,  /* fp32 blend + guard bands + fp64 re-decision (default) */
-    SEELE_PRECISION_EXACT = 1  /* every alpha / transmittance in fp64 */
+    SEELE_PRECISION_EXACT = 1, /* every alpha / transmittance in fp64 */
+    /* flag OR-ed into precision: also keep the projected splats that bin to no tile (depth, mean, conic,
+     * colour) for seele_plan_export; a frame's own stages never read them, so they are skipped by default */
+    SEELE_KEEP_UNBINNED = 0x100
 };
 
 /* Scene in HBM.  Two layouts:

@@ -40,6 +40,7 @@ LAYOUT_F64 = 0
 LAYOUT_PLANES = 1
 PRECISION_FAST = 0
 PRECISION_EXACT = 1
+KEEP_UNBINNED = 0x100  # SEELE_KEEP_UNBINNED, OR-ed into precision
 MAX_RANGES = 64
 
 EXPORTED_SYMBOLS = (
@@ -176,7 +177,7 @@ def camera_struct(cam) -> Camera:
     return c
 
 
-def config_struct(cfg) -> Config:
+def config_struct(cfg, keep_unbinned: bool = False) -> Config:
     c = Config()
     c.engine = 0 if cfg.engine == "ref" else 1
     c.group_w = int(cfg.group_w)
@@ -186,5 +187,7 @@ def config_struct(cfg) -> Config:
     c.gamma_threshold = float(cfg.gamma_threshold)
     c.background[:] = [float(v) for v in cfg.background]
     c.precision = PRECISION_EXACT if getattr(cfg, "precision", "fast") == "exact" else PRECISION_FAST
+    if keep_unbinned:  # plan export: every projected splat's record, not only the binned ones
+        c.precision |= KEEP_UNBINNED
     c.tile_size = int(cfg.tile_size)
     return c

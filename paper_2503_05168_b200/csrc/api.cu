@@ -115,7 +115,8 @@ int check_config(const seele_config *c) {
     if (c->sh_degree < 0 || c->sh_degree > 3)
         return fail(SEELE_ERR_INVALID_ARGUMENT, "SH degree must lie in [0, 3], got %d", c->sh_degree);
     if (c->tile_size != kTile) return fail(SEELE_ERR_INVALID_ARGUMENT, "tile size must be 16, got %d", c->tile_size);
-    if (c->precision != SEELE_PRECISION_FAST && c->precision != SEELE_PRECISION_EXACT)
+    const int prec = c->precision & ~SEELE_KEEP_UNBINNED;
+    if (prec != SEELE_PRECISION_FAST && prec != SEELE_PRECISION_EXACT)
         return fail(SEELE_ERR_INVALID_ARGUMENT, "unknown precision %d", c->precision);
     if (!(c->alpha_theta > 0.0) || !(c->gamma_threshold > 0.0))
         return fail(SEELE_ERR_INVALID_ARGUMENT, "thresholds must be positive");
@@ -267,7 +268,8 @@ int seele_render_split(const seele_scene *scene, const int64_t *ranges_dev, int3
     cf.group_w = cfg->group_w;
     cf.sh_degree = cfg->sh_degree;
     cf.opacity_aware = cfg->opacity_aware;
-    cf.precision = cfg->precision;
+    cf.precision = cfg->precision & ~SEELE_KEEP_UNBINNED;
+    cf.keep_unbinned = (cfg->precision & SEELE_KEEP_UNBINNED) != 0;
     cf.alpha_theta = cfg->alpha_theta;
     cf.gamma = cfg->gamma_threshold;
     for (int i = 0; i < 3; i++) cf.bg[i] = cfg->background[i];

@@ -273,7 +273,7 @@ __global__ void __launch_bounds__(kScanThreads) k_bin_scan(Workspace ws, BinGeom
         const int a0 = min(g.n_st, tid * per), a1 = min(g.n_st, a0 + per);
         uint32_t part = 0, pseg = 0;
         for (int i = a0; i < a1; i++) {
-            const uint32_t c = *(volatile uint32_t *)&ws.st_cnt[i];
+            const uint32_t c = __ldcg(&ws.st_cnt[i]);
             part += c;
             pseg += (c + kSeg - 1) / kSeg;
         }
@@ -281,7 +281,7 @@ __global__ void __launch_bounds__(kScanThreads) k_bin_scan(Workspace ws, BinGeom
         uint32_t acc = sweep::block_scan<uint32_t>(part, all);
         uint32_t sacc = sweep::block_scan<uint32_t>(pseg, all_seg);
         for (int i = a0; i < a1; i++) {
-            const uint32_t c = *(volatile uint32_t *)&ws.st_cnt[i];
+            const uint32_t c = __ldcg(&ws.st_cnt[i]);
             ws.st_start[i] = acc;
             ws.seg_first[i] = sacc;
             if (!over)  // (on overflow the lists are not built and may exceed the segment table)
@@ -299,7 +299,7 @@ __global__ void __launch_bounds__(kScanThreads) k_bin_scan(Workspace ws, BinGeom
     const int ndiff = tx1 * (g.tiles_y + 1);
     int32_t *d = diff_in_smem ? s_diff : ws.tile_diff;  // in shared memory when it fits
     if (diff_in_smem)
-        for (int i = tid; i < ndiff; i += kScanThreads) s_diff[i] = *(volatile int32_t *)&ws.tile_diff[i];
+        for (int i = tid; i < ndiff; i += kScanThreads) s_diff[i] = __ldcg(&ws.tile_diff[i]);  // (L2: other CTAs' atomics)
     __syncthreads();
     // 2D prefix sum in place: rows (one warp per row, lane-parallel scan), then columns
     {
@@ -474,8 +474,8 @@ __global__ void __launch_bounds__(NW * 32) k_bin_split(Workspace ws, BinGeom g) 
             const StRect osr = st_rect(orc);
             const uint32_t osw = osr.x1 - osr.x0 + 1;
             const uint32_t k = item - o_excl;
-            // k / osw: exact in float (k < 2^16, osw <= 64: the error is far below the 0.5 / osw margin)
-            const uint32_t ky = (uint32_t)(((float)k + 0.5f) * __frcp_rn((float)osw));
+            // k / osw: exact in float (k < 2^16, osw <= 64: a few ulp of error stay far below the 0.5 / osw margin)
+            const uint32_t ky = (uint32_t)__fdividef((float)k + 0.5f, (float)osw);
             const uint32_t sx = osr.x0 + (k - ky * osw), sy = osr.y0 + ky;
             const uint32_t sd = sy * sx1 + sx;
             const uint32_t obit = 1u << owner;

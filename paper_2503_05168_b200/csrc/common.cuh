@@ -23,6 +23,7 @@ struct CamK {
 
 struct CfgK {
     int engine, group_w, sh_degree, opacity_aware, precision;
+    int keep_unbinned;  // SEELE_KEEP_UNBINNED: records of projected splats that bin to no tile (plan export)
     double alpha_theta, gamma;
     double bg[3];
 };

@@ -107,18 +107,22 @@ __device__ __forceinline__ void normalize4(double q[4]) {
     q[3] *= r;
 }
 
+// planes layout: xyz + opacity logit, log scale, raw quaternion (container record, io.py:22-25)
+__device__ __forceinline__ void splat_from_planes(float4 p0, float4 p1, float4 p2, Splat &g) {
+    g.p[0] = p0.x; g.p[1] = p0.y; g.p[2] = p0.z;
+    g.o = sigmoid_clip((double)p0.w);
+    g.s[0] = p1.x; g.s[1] = p1.y; g.s[2] = p1.z;
+    g.q[0] = p2.x; g.q[1] = p2.y; g.q[2] = p2.z; g.q[3] = p2.w;
+    normalize4(g.q);  // container decode (io.py:226-229)
+    normalize4(g.q);  // Gaussian3D.__post_init__ (model.py:122, 76-80)
+}
+
 template <int LAYOUT>
 __device__ __forceinline__ void load_splat(const SceneK &sc, long long i, int sh_planes, Splat &g) {
     if (LAYOUT == SEELE_LAYOUT_PLANES) {
         const long long st = sc.plane_stride;
-        float4 p0 = __ldg(sc.planes + 0 * st + i);
-        float4 p1 = __ldg(sc.planes + 1 * st + i);
-        float4 p2 = __ldg(sc.planes + 2 * st + i);
-        g.p[0] = p0.x; g.p[1] = p0.y; g.p[2] = p0.z;
-        g.o = sigmoid_clip((double)p0.w);
-        g.s[0] = p1.x; g.s[1] = p1.y; g.s[2] = p1.z;
-        g.q[0] = p2.x; g.q[1] = p2.y; g.q[2] = p2.z; g.q[3] = p2.w;
-        normalize4(g.q);  // container decode (io.py:226-229)
+        splat_from_planes(__ldg(sc.planes + 0 * st + i), __ldg(sc.planes + 1 * st + i), __ldg(sc.planes + 2 * st + i), g);
+        return;
     } else {
         for (int k = 0; k < 3; k++) {
             g.p[k] = sc.pos[3 * i + k];
@@ -153,8 +157,7 @@ __device__ __forceinline__ void load_splat(const SceneK &sc, long long i, int sh
 // bbox = axis-aligned box of {q' <= q_hi'}; the raster refines it with the
 // exact minimum of q' over each warp's pixel rectangle.
 __device__ __forceinline__ void write_raster_record(const Workspace &ws, long long p, double m0, double m1, double ca,
-                                                    double cb, double cc, double o, double qth, float qth_err,
-                                                    float4 col) {
+                                                    double cb, double cc, double o, double qth, float qth_err) {
     const double K = 0.72134752044448170368;  // log2(e) / 2
     const double det = ca * cc - cb * cb;
     float4 rq = make_float4(-INFINITY, -INFINITY, 0.f, 0.f);
@@ -208,7 +211,6 @@ __device__ __forceinline__ void write_raster_record(const Workspace &ws, long lo
     const float q_up = nextafterf(rq.y, INFINITY);
     const float w_up = rq.x == -INFINITY ? 0.0f : __double2float_ru(__dsub_ru((double)q_up, (double)rq.x));
     rec[2] = make_float4(rq.x, w_up, rq.z * (1.0f + 1.0f / 1024.0f), rq.w * (1.0f + 1.0f / 1024.0f));
-    rec[3] = make_float4(col.x, col.y, col.z, __uint_as_float((uint32_t)p));
     ws.bbox[p] = bb;
 }
 
@@ -281,20 +283,6 @@ __global__ void __launch_bounds__(kPre, SEELE_PRE_MINB) k_preprocess(SceneK sc, 
             int r = 0;
             while (r + 1 < n_ranges && s_prefix[r + 1] <= p) r++;
             const long long i = s_start[r] + (p - s_prefix[r]);
-            if (LAYOUT == SEELE_LAYOUT_PLANES) {
-                // slot ch * sh_planes + k <- plane 3 + 4 ch + k (no runtime division: the full SH3 case unrolled)
-                const float4 *src = sc.planes + 3 * sc.plane_stride + i;
-                float4 *dst = s_sh + threadIdx.x;
-                if (sh_planes == 4) {
-#pragma unroll
-                    for (int k = 0; k < 12; k++) cp_async16(dst + k * kPre, src + k * sc.plane_stride);
-                } else {
-                    for (int ch = 0; ch < 3; ch++)
-                        for (int k = 0; k < sh_planes; k++)
-                            cp_async16(dst + (ch * sh_planes + k) * kPre, src + (4 * ch + k) * sc.plane_stride);
-                }
-                cp_async_commit();
-            }
             Splat g;
             load_splat<LAYOUT>(sc, i, sh_planes, g);
             const double d[3] = {__dsub_rn(g.p[0], cam.pos[0]), __dsub_rn(g.p[1], cam.pos[1]), __dsub_rn(g.p[2], cam.pos[2])};
@@ -347,37 +335,6 @@ __global__ void __launch_bounds__(kPre, SEELE_PRE_MINB) k_preprocess(SceneK sc, 
                     status = 0;
                     const double rdet = 1.0 / det;
                     const double ca = s11 * rdet, cb = -s01 * rdet, cc = s00 * rdet;
-                    // view direction for SH (preprocess.py:129-130), fp32 like the colour
-                    const float rn = rsqrtf((float)(d[0] * d[0] + d[1] * d[1] + d[2] * d[2]));
-                    const float vx = (float)d[0] * rn, vy = (float)d[1] * rn, vz = (float)d[2] * rn;
-                    float4 col;
-                    if (LAYOUT == SEELE_LAYOUT_PLANES) {
-                        // SH planes are read only for projected splats, one channel (4 x float4) at a time
-                        float cc3[3];
-                        cp_async_wait_all();
-#pragma unroll
-                        for (int ch = 0; ch < 3; ch++) {
-                            float shc[16];
-#pragma unroll
-                            for (int k = 0; k < 4; k++) {
-                                float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-                                if (k < sh_planes) v = s_sh[(ch * sh_planes + k) * kPre + threadIdx.x];
-                                shc[4 * k] = v.x;
-                                shc[4 * k + 1] = v.y;
-                                shc[4 * k + 2] = v.z;
-                                shc[4 * k + 3] = v.w;
-                            }
-                            cc3[ch] = sh_channel([&](int k) { return shc[k]; }, vx, vy, vz, cfg.sh_degree);
-                        }
-                        col.x = cc3[0];
-                        col.y = cc3[1];
-                        col.z = cc3[2];
-                    } else {
-                        const double *shp = sc.sh + 48 * i;
-                        col.x = sh_channel([&](int k) { return (float)shp[k]; }, vx, vy, vz, cfg.sh_degree);
-                        col.y = sh_channel([&](int k) { return (float)shp[16 + k]; }, vx, vy, vz, cfg.sh_degree);
-                        col.z = sh_channel([&](int k) { return (float)shp[32 + k]; }, vx, vy, vz, cfg.sh_degree);
-                    }
                     // alpha >= theta <=> q <= qth = 2 ln(o / theta).  qth >= 9 (o >= theta e^4.5) only feeds the
                     // alpha bracket (r2 clips at 9), which tolerates an fp32 log with its error added to the
                     // bracket; below that qth sets the opacity-aware radius and is taken in fp64.
@@ -407,18 +364,66 @@ __global__ void __launch_bounds__(kPre, SEELE_PRE_MINB) k_preprocess(SceneK sc, 
                             n_tiles = (uint32_t)(x1 - x0 + 1) * (uint32_t)(y1 - y0 + 1);
                         }
                     }
-                    ws.depth[p] = z;
-                    // depth-order bucket (depth.cu) of a binned splat: count it and keep its index in the bucket
-                    if (n_tiles > 0) ws.bidx[p] = atomicAdd(&ws.bhist[depth_bucket_of_key(depth_order_key(z), zbase)], 1u);
-                    ws.mean[p] = make_double2(m0, m1);
-                    ws.conic_op[p] = make_double4(ca, cb, cc, g.o);
-                    write_raster_record(ws, p, m0, m1, ca, cb, cc, g.o, qth, qth_err, col);
+                    // Records are written for binned splats only (a splat no tile bins is never read by the
+                    // frame), unless the plan export asked for every projected splat: its SH planes are read
+                    // only then, by cp.async overlapping the raster-record arithmetic.
+                    if (n_tiles > 0 || cfg.keep_unbinned) {
+                        if (LAYOUT == SEELE_LAYOUT_PLANES) {
+                            // slot ch * sh_planes + k <- plane 3 + 4 ch + k (the full SH3 case unrolled)
+                            const float4 *src = sc.planes + 3 * sc.plane_stride + i;
+                            float4 *dst = s_sh + threadIdx.x;
+                            if (sh_planes == 4) {
+#pragma unroll
+                                for (int k = 0; k < 12; k++) cp_async16(dst + k * kPre, src + k * sc.plane_stride);
+                            } else {
+                                for (int ch = 0; ch < 3; ch++)
+                                    for (int k = 0; k < sh_planes; k++)
+                                        cp_async16(dst + (ch * sh_planes + k) * kPre, src + (4 * ch + k) * sc.plane_stride);
+                            }
+                            cp_async_commit();
+                        }
+                        ws.depth[p] = z;
+                        // depth-order bucket (depth.cu) of a binned splat: count it and keep its index in the bucket
+                        if (n_tiles > 0)
+                            ws.bidx[p] = atomicAdd(&ws.bhist[depth_bucket_of_key(depth_order_key(z), zbase)], 1u);
+                        ws.mean[p] = make_double2(m0, m1);
+                        ws.conic_op[p] = make_double4(ca, cb, cc, g.o);
+                        write_raster_record(ws, p, m0, m1, ca, cb, cc, g.o, qth, qth_err);
+                        // view direction for SH (preprocess.py:129-130), fp32 like the colour
+                        const float rn = rsqrtf((float)(d[0] * d[0] + d[1] * d[1] + d[2] * d[2]));
+                        const float vx = (float)d[0] * rn, vy = (float)d[1] * rn, vz = (float)d[2] * rn;
+                        float4 col;
+                        if (LAYOUT == SEELE_LAYOUT_PLANES) {
+                            float cc3[3];
+                            cp_async_wait_all();
+#pragma unroll
+                            for (int ch = 0; ch < 3; ch++) {
+                                float shc[16];
+#pragma unroll
+                                for (int k = 0; k < 4; k++) {
+                                    float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+                                    if (k < sh_planes) v = s_sh[(ch * sh_planes + k) * kPre + threadIdx.x];
+                                    shc[4 * k] = v.x;
+                                    shc[4 * k + 1] = v.y;
+                                    shc[4 * k + 2] = v.z;
+                                    shc[4 * k + 3] = v.w;
+                                }
+                                cc3[ch] = sh_channel([&](int k) { return shc[k]; }, vx, vy, vz, cfg.sh_degree);
+                            }
+                            col = make_float4(cc3[0], cc3[1], cc3[2], 0.f);
+                        } else {
+                            const double *shp = sc.sh + 48 * i;
+                            col.x = sh_channel([&](int k) { return (float)shp[k]; }, vx, vy, vz, cfg.sh_degree);
+                            col.y = sh_channel([&](int k) { return (float)shp[16 + k]; }, vx, vy, vz, cfg.sh_degree);
+                            col.z = sh_channel([&](int k) { return (float)shp[32 + k]; }, vx, vy, vz, cfg.sh_degree);
+                        }
+                        reinterpret_cast<float4 *>(ws.rec + p)[3] = make_float4(col.x, col.y, col.z, __uint_as_float((uint32_t)p));
+                    }
                 }
             }
             ws.status[p] = (uint8_t)status;
             ws.rect[p] = rect;
         }
-        if (LAYOUT == SEELE_LAYOUT_PLANES) cp_async_wait_all();  // slots are reused next iteration
         cnt[0] += status == 1;
         cnt[1] += status == 2;
         cnt[2] += status == 0;

@@ -11,9 +11,13 @@
 // A hardware warp covers a 16x8 pixel region (tile rows 0-7 / 8-15).
 //
 // Contribution-aware engine (rasterize.py:249-322): for w = 2 the group IS
-// the thread's quad, so the leader test is one alpha per thread and the
-// member alphas run only if some leader of the warp passed; for w = 4 the
-// group is 4 threads and the leader thread's verdict is broadcast by ballot.
+// the thread's quad, so the leader verdict is the sign of the quad's first
+// pixel's d; for w = 4 the group is 4 threads and the leader thread's verdict
+// is broadcast by ballot.  The members' alphas are evaluated together with
+// the leader's (packed fp32x2) and masked by the verdict: a warp-step in
+// which no leader of the warp passes is rare once the warp-region cull below
+// has run (5 % of C3's relevant warp-steps, SEELE_RASTER_PROFILE), so a
+// leader-first branch would not pay for itself.
 //
 // Work skipping (exact): every staged splat carries the box of pixel centres
 // that can pass its alpha test (preprocess write_raster_record).  A warp

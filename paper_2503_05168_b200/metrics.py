@@ -5,7 +5,12 @@ device.  Inputs are (H, W, 3) arrays (numpy, or torch tensors on the device);
 results are Python floats like the reference's."""
 from __future__ import annotations
 
-from dataclasses import dataclass
+import csv
+import json
+import math
+import time
+from dataclasses import dataclass, replace
+from pathlib import Path
 
 import numpy as np
 
@@ -106,3 +111,98 @@ def contribution_cdf(scene, cam, cfg=None, *, keep_per_pixel: bool = False) -> C
         curves = [cum_h[:max(int(c), 1), pix] if c else np.zeros(0) for pix, c in enumerate(cnt_h)]
     return ContributionCurve(aggregate=cumulative.mean(dim=1).cpu().numpy(), per_pixel_totals=totals.cpu().numpy(),
                              fraction_for_99=fraction_for_99, per_pixel_curves=curves)
+
+
+# ---- comparative benchmark harness (metrics.py:164-266) -------------------------------------------------
+
+REPORT_COLUMNS = ["config", "psnr_db", "ssim", "lpips", "warp_steps", "alpha_evals", "blend_steps",
+                  "leader_evals", "peak_resident_bytes", "stalls", "wall_ms"]
+
+
+def _fmt(value) -> str:
+    if isinstance(value, float):
+        return "inf" if math.isinf(value) else f"{value:.6f}"
+    return "" if value is None else str(value)
+
+
+def bench_compare(configs: list[dict], poses: list, *, flat_scene=None, clustered=None, base_cfg=None,
+                  m: int | None = None) -> list[dict]:
+    """metrics.bench_compare (metrics.py:172-243) on the GPU: render a
+    trajectory under each configuration ({"engine": "ref"|"cr", "scene":
+    "flat"|"clustered"}) and report quality (GPU PSNR / SSIM against the flat
+    scene under the reference engine, rendered once up front) and the
+    lockstep cost counters.  Clustered configurations stream the container
+    through :class:`~.streaming.StreamingRenderer` (the reference
+    ResidentRenderer's state machine: its stall count and peak resident bytes,
+    same defaults).  ``wall_ms`` is this host's wall clock."""
+    from .container import BYTES_PER_GAUSSIAN
+    from .render import EngineConfig, render_frame
+    from .streaming import StreamingRenderer
+
+    base_cfg = base_cfg or EngineConfig()
+    if flat_scene is None:
+        raise InvalidArgumentError("bench requires the flat scene for the baseline")
+    baseline_cfg = replace(base_cfg, engine="ref")
+    baseline = [render_frame(flat_scene, pose, baseline_cfg, output="torch").image for pose in poses]
+    flat_bytes = len(flat_scene) * BYTES_PER_GAUSSIAN
+
+    def score(res, base, totals, psnrs, ssims):
+        st = res.stats
+        totals["warp"] += st.warp_steps
+        totals["alpha"] += st.alpha_eval_steps
+        totals["blend"] += st.blend_steps
+        totals["leader"] += st.leader_eval_steps
+        psnrs.append(psnr(res.image, base))
+        ssims.append(ssim(res.image, base))
+
+    rows = []
+    for entry in configs:
+        engine, scene_mode = entry["engine"], entry["scene"]
+        cfg = replace(base_cfg, engine=engine)
+        t0 = time.perf_counter()
+        totals = {"warp": 0, "alpha": 0, "blend": 0, "leader": 0, "stalls": 0}
+        peak_bytes = flat_bytes
+        psnrs, ssims = [], []
+        if scene_mode == "clustered":
+            if clustered is None:
+                raise InvalidArgumentError("no clustered scene supplied for a clustered config")
+            with StreamingRenderer(clustered, m) as renderer:
+                for pose, base in zip(poses, baseline):
+                    score(renderer.render_frame(pose, cfg, output="torch"), base, totals, psnrs, ssims)
+                peak_bytes = renderer.peak_resident_bytes
+                totals["stalls"] = renderer.stall_count
+        else:
+            for pose, base in zip(poses, baseline):
+                score(render_frame(flat_scene, pose, cfg, output="torch"), base, totals, psnrs, ssims)
+        wall_ms = (time.perf_counter() - t0) * 1000.0
+        finite = [v for v in psnrs if not math.isinf(v)]
+        rows.append({
+            "config": f"{engine}:{scene_mode}",
+            "psnr_db": math.inf if not finite else float(np.mean(finite)),
+            "ssim": float(np.mean(ssims)),
+            "lpips": None,
+            "warp_steps": totals["warp"],
+            "alpha_evals": totals["alpha"],
+            "blend_steps": totals["blend"],
+            "leader_evals": totals["leader"],
+            "peak_resident_bytes": peak_bytes,
+            "stalls": totals["stalls"],
+            "wall_ms": wall_ms,
+        })
+    return rows
+
+
+def write_report(rows: list[dict], csv_path) -> None:
+    """metrics.write_report (metrics.py:246-266): the table as CSV plus a JSON
+    mirror next to it (same columns, number formatting and "inf" spelling)."""
+    csv_path = Path(csv_path)
+    with csv_path.open("w", newline="") as fh:
+        writer = csv.writer(fh)
+        writer.writerow(REPORT_COLUMNS)
+        for row in rows:
+            writer.writerow([_fmt(row[c]) for c in REPORT_COLUMNS])
+    json_rows = []
+    for row in rows:
+        json_rows.append({c: ("inf" if isinstance(row[c], float) and math.isinf(row[c]) else row[c])
+                          for c in REPORT_COLUMNS})
+    csv_path.with_suffix(".json").write_text(json.dumps(json_rows, indent=1))

@@ -213,7 +213,7 @@ class FrameRenderer:
                n_ranges: int = 1, n_max: int | None = None, image: torch.Tensor | None = None,
                contrib: torch.Tensor | bool = True, stats: torch.Tensor | None = None,
                stream: torch.cuda.Stream | None = None,
-               raster_stream: torch.cuda.Stream | None = None) -> FrameOutput:
+               raster_stream: torch.cuda.Stream | None = None, keep_unbinned: bool = False) -> FrameOutput:
         """Asynchronous frame on ``stream`` (default: current stream); with
         ``raster_stream`` the raster is issued there after the plan stages."""
         w, h = int(cam.width), int(cam.height)
@@ -244,7 +244,7 @@ class FrameRenderer:
         st = stream if stream is not None else torch.cuda.current_stream(self.device)
         sc = scene.struct()
         camc = _native.camera_struct(cam)
-        cfgc = _native.config_struct(cfg)
+        cfgc = _native.config_struct(cfg, keep_unbinned)
         _native.check(self.lib.seele_render_split(
             ctypes.byref(sc), ranges.data_ptr(), int(n_ranges), ctypes.byref(camc), ctypes.byref(cfgc),
             self.workspace.data_ptr(), self.workspace.numel(), self.n_max, self.pair_capacity, image.data_ptr(),
@@ -442,7 +442,7 @@ def plan_frame(scene, cam: CameraPose, cfg: EngineConfig) -> FramePlan:
     """Drop-in for render.plan_frame (render.py:90-141), computed on the GPU."""
     dscene = _as_device_scene(scene)
     renderer = get_renderer(dscene.device)
-    _, host = renderer.render_checked(dscene, cam, cfg)
+    _, host = renderer.render_checked(dscene, cam, cfg, keep_unbinned=True)
     return renderer.export_plan(dscene, cam, host)
 
 
