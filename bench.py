@@ -59,6 +59,8 @@ def parse():
     ap.add_argument("--depth", type=int, default=3, help="frames in flight (streams)")
     ap.add_argument("--raster-first", action="store_true",
                     help="raster on a high-priority stream, the plan stages of the frames in flight below it")
+    ap.add_argument("--plan-first", action="store_true",
+                    help="plan stages on a high-priority stream, the raster of the frames in flight below it")
     ap.add_argument("--gather", action="store_true",
                     help="also time the run with an NCCL all-gather of every frame (uint8) + stats inside the timed "
                          "region (value_gather)")
@@ -298,7 +300,7 @@ def run_ours(args):
 
     serial_ms = timed_serial()
     pipe = FramePipeline(rr, args.width, args.height, depth=args.depth, pair_capacity=cap,
-                         split=args.raster_first, raster_priority=args.raster_first)
+                         split=args.raster_first or args.plan_first, raster_priority=args.raster_first)
     clocks = ClockSampler(device) if rank == 0 else None
     if clocks:
         clocks.start()

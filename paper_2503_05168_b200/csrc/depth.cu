@@ -60,43 +60,6 @@ __device__ __forceinline__ bool rec_before(const uint4 &a, const uint4 &b) {
     return before(rec_key(a), a.z, rec_key(b), b.z);
 }
 
-// Block-wide (kSortThreads) exclusive max-scan (identity 0) and exclusive min-scan from the right (identity
-// `none`) of one value per thread.
-__device__ __forceinline__ uint32_t block_max_scan_excl(uint32_t v) {
-    __shared__ uint32_t s_w[kSortThreads / 32];
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    uint32_t x = v;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-        const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
-        if (lane >= o) x = max(x, y);
-    }
-    if (lane == 31) s_w[warp] = x;
-    __syncthreads();
-    uint32_t before = 0;
-    for (int w = 0; w < warp; w++) before = max(before, s_w[w]);
-    const uint32_t ex = __shfl_up_sync(0xffffffffu, x, 1);
-    __syncthreads();
-    return max(before, lane ? ex : 0u);
-}
-__device__ __forceinline__ uint32_t block_min_scan_excl_rev(uint32_t v, uint32_t none) {
-    __shared__ uint32_t s_w[kSortThreads / 32];
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    uint32_t x = v;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-        const uint32_t y = __shfl_down_sync(0xffffffffu, x, o);
-        if (lane + o < 32) x = min(x, y);
-    }
-    if (lane == 0) s_w[warp] = x;
-    __syncthreads();
-    uint32_t after = none;
-    for (int w = warp + 1; w < kSortThreads / 32; w++) after = min(after, s_w[w]);
-    const uint32_t ex = __shfl_down_sync(0xffffffffu, x, 1);
-    __syncthreads();
-    return min(after, lane < 31 ? ex : none);
-}
-
 // Exclusive bucket offsets: CTA t scans buckets [t K, (t + 1) K), K = kDepthScanItems, and resolves its prefix
 // by look-back over the lower CTAs.  Bucket c with items [lo, hi) starts every sort group g with
 // lo < g G <= hi at bucket c + 1 (gfirst[g] = c + 1 = the first bucket whose offset is >= g G).
@@ -257,13 +220,6 @@ __device__ void global_merge_sort(const Workspace &ws, SortSmem &S, uint32_t s, 
     __syncthreads();
 }
 
-// Bucket of group item i (its record re-read from global memory: L1 hits, the group was just loaded).
-__device__ __forceinline__ uint32_t bucket_at(const SortSmem &, const uint4 *in, uint32_t s, uint32_t i,
-                                              unsigned long long base) {
-    const uint4 r = in[s + i];
-    return depth_bucket_of_key(rec_key(r), base);
-}
-
 __global__ void __launch_bounds__(kSortThreads) k_bucket_sort(Workspace ws, CamK cam, const int64_t *stats) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     SortSmem &S = *reinterpret_cast<SortSmem *>(smem_raw);
@@ -283,6 +239,7 @@ __global__ void __launch_bounds__(kSortThreads) k_bucket_sort(Workspace ws, CamK
             continue;
         }
         constexpr int U = kDepthSmem / kSortThreads;
+        uint32_t bk[U];  // each item's depth bucket
         {
             uint4 r[U];
 #pragma unroll
@@ -293,6 +250,7 @@ __global__ void __launch_bounds__(kSortThreads) k_bucket_sort(Workspace ws, CamK
 #pragma unroll
             for (int u = 0; u < U; u++) {
                 const uint32_t i = threadIdx.x + u * kSortThreads;
+                bk[u] = i < m ? depth_bucket_of_key(rec_key(r[u]), base) : 0u;
                 if (i < m) {
                     // inside one bucket (< the clamped last one) the keys share every bit above bit 36 of
                     // key - base, so (low 36 bits, position) orders them; positions < 2^28
@@ -303,55 +261,24 @@ __global__ void __launch_bounds__(kSortThreads) k_bucket_sort(Workspace ws, CamK
             }
         }
         __syncthreads();
-        // bucket bounds: each thread scans U consecutive items for bucket changes, then a block-wide max-scan
-        // (begin) and min-scan from the right (end) across threads
+        // bucket bounds: the scanned bucket offsets (bhist, exclusive, bhist[kDepthBuckets] = n) give every
+        // item its bucket's [begin, end) inside the group directly
         bool small = n_ws < (1u << 28);  // (positions fit the packed key)
         {
-            const uint32_t i0 = threadIdx.x * U;
-            uint32_t bk[U];
+            uint32_t lo[U], hi[U];
 #pragma unroll
             for (int u = 0; u < U; u++) {
-                const uint32_t i = i0 + u;
-                bk[u] = i < m ? bucket_at(S, in, s, i, base) : 0xffffffffu;
+                const uint32_t i = threadIdx.x + u * kSortThreads;
+                lo[u] = i < m ? ws.bhist[bk[u]] : s;
+                hi[u] = i < m ? ws.bhist[bk[u] + 1] : s;
             }
-            const uint32_t prev = i0 > 0 && i0 - 1 < m ? bucket_at(S, in, s, i0 - 1, base) : 0xfffffffeu;
-            const uint32_t next = i0 + U < m ? bucket_at(S, in, s, i0 + U, base) : 0xfffffffdu;
-            uint32_t beg[U], end[U];
-            uint32_t run = 0;  // begin of the current run, local (0 = unknown: may continue from the left)
-            bool open_left = true;
 #pragma unroll
             for (int u = 0; u < U; u++) {
-                if (u == 0 ? bk[0] != prev : bk[u] != bk[u - 1]) {
-                    run = i0 + u;
-                    open_left = false;
-                }
-                beg[u] = open_left ? 0xffffffffu : run;
-            }
-            uint32_t rrun = 0xffffffffu;
-            bool open_right = true;
-#pragma unroll
-            for (int u = U - 1; u >= 0; u--) {
-                if (u == U - 1 ? bk[u] != next : bk[u] != bk[u + 1]) {
-                    rrun = i0 + u + 1;
-                    open_right = false;
-                }
-                end[u] = open_right ? 0xffffffffu : rrun;
-            }
-            // carry across threads: begin = last run start at or before (max-scan of run starts), end = first
-            // run end at or after (min-scan from the right)
-            const uint32_t my_last_start = open_left ? 0u : run;  // the run start that continues to the right
-            const uint32_t my_first_end = open_right ? m : rrun;  // the run end that continues to the left
-            __syncthreads();  // every bucket id is read before b0 is overwritten
-            const uint32_t carry_beg = block_max_scan_excl(my_last_start);
-            const uint32_t carry_end = block_min_scan_excl_rev(my_first_end, m);
-#pragma unroll
-            for (int u = 0; u < U; u++) {
-                const uint32_t b = beg[u] == 0xffffffffu ? carry_beg : beg[u];
-                const uint32_t e = end[u] == 0xffffffffu ? carry_end : end[u];
-                if (i0 + u < m) {
-                    S.r.b0[i0 + u] = (uint16_t)b;
-                    S.r.b1[i0 + u] = (uint16_t)e;
-                    small &= e - b <= (uint32_t)kRankMaxBucket && bk[u] != (uint32_t)(kDepthBuckets - 1);
+                const uint32_t i = threadIdx.x + u * kSortThreads;
+                if (i < m) {
+                    S.r.b0[i] = (uint16_t)(lo[u] - s);
+                    S.r.b1[i] = (uint16_t)(hi[u] - s);
+                    small &= hi[u] - lo[u] <= (uint32_t)kRankMaxBucket && bk[u] != (uint32_t)(kDepthBuckets - 1);
                 }
             }
         }

@@ -454,20 +454,20 @@ __global__ void k_select(CamK cam, const double *__restrict__ centroids, int n, 
         d2[c] = s;
     }
     __syncthreads();
+    // the m + 1 nearest in np.lexsort((arange, d2)) order: centroid c goes to slot rank(c) = the number of
+    // centroids before it in (d2, id) order (one thread per centroid, no serial selection)
     if (threadIdx.x == 0) {
         ranges_out[0] = chunks[0];
         ranges_out[1] = chunks[1];
-        unsigned long long used[16] = {0};
-        for (int s = 0; s <= m; s++) {
-            int best = -1;
-            for (int c = 0; c < n; c++) {
-                if ((used[c >> 6] >> (c & 63)) & 1ull) continue;
-                if (best < 0 || d2[c] < d2[best]) best = c;  // np.lexsort((arange, d2)): ties -> smaller id
-            }
-            used[best >> 6] |= 1ull << (best & 63);
-            out_ids[s] = best;
-            ranges_out[2 * (s + 1)] = chunks[2 * (best + 1)];
-            ranges_out[2 * (s + 1) + 1] = chunks[2 * (best + 1) + 1];
+    }
+    for (int c = threadIdx.x; c < n; c += blockDim.x) {
+        const double v = d2[c];
+        int rank = 0;
+        for (int o = 0; o < n; o++) rank += (d2[o] < v || (d2[o] == v && o < c)) ? 1 : 0;
+        if (rank <= m) {
+            out_ids[rank] = c;
+            ranges_out[2 * (rank + 1)] = chunks[2 * (c + 1)];
+            ranges_out[2 * (rank + 1) + 1] = chunks[2 * (c + 1) + 1];
         }
     }
 }
