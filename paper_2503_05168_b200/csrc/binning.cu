@@ -46,7 +46,16 @@ namespace {
 constexpr int kSt = 4;  // super-tile edge in tiles
 constexpr int kCountThreads = 256;
 constexpr int kScanThreads = sweep::NT;  // 512 (block_scan)
-constexpr int kExpandThreads = 256;
+#ifndef SEELE_EXPAND_THREADS
+#define SEELE_EXPAND_THREADS 256
+#endif
+constexpr int kExpandThreads = SEELE_EXPAND_THREADS;  // 8 batches of 8 warps / 4 of 16 / 2 of 32 per segment
+#ifndef SEELE_EXPAND_MINB
+#define SEELE_EXPAND_MINB (1024 / SEELE_EXPAND_THREADS)
+#endif
+#ifndef SEELE_SPLIT_NW
+#define SEELE_SPLIT_NW 8
+#endif
 
 // ---- frame start ---------------------------------------------------------------
 
@@ -555,7 +564,7 @@ __device__ __forceinline__ uint32_t ballot_again(uint32_t pred) {
 // starts the chain.  The segment's entries are ordered (batch, warp, lane); per (batch, warp) tile counts
 // from one ballot each are scanned per tile, then every (batch, warp, tile) writes its pairs as one
 // coalesced run.
-__global__ void __launch_bounds__(kExpandThreads, 4) k_bin_expand(Workspace ws, BinGeom g) {
+__global__ void __launch_bounds__(kExpandThreads, SEELE_EXPAND_MINB) k_bin_expand(Workspace ws, BinGeom g) {
     constexpr int NW = kExpandThreads / 32;
     constexpr int NBW = kSegBatches * NW;  // (batch, warp) units of a segment
     static_assert(NBW == 64, "the per-tile scan takes two units per lane");
@@ -588,6 +597,7 @@ __global__ void __launch_bounds__(kExpandThreads, 4) k_bin_expand(Workspace ws, 
 #pragma unroll
         for (int h = 0; h < 2; h++) {
             const int j = 2 * warp + h;
+            if (j >= 16) break;  // (more than 8 warps: the 16 tiles are taken by the first 8)
             const uint32_t a0 = s_cnt[j][2 * lane], a1 = s_cnt[j][2 * lane + 1];
             uint32_t incl = a0 + a1;
 #pragma unroll
@@ -612,6 +622,7 @@ __global__ void __launch_bounds__(kExpandThreads, 4) k_bin_expand(Workspace ws, 
 #pragma unroll
         for (int h = 0; h < 2; h++) {  // unit offsets -> absolute slots
             const int j = 2 * warp + h;
+            if (j >= 16) break;
             s_cnt[j][2 * lane] += s_base[j];
             s_cnt[j][2 * lane + 1] += s_base[j];
         }
@@ -773,10 +784,11 @@ void launch_binning(const Workspace &ws, long long n_max, long long cap, const C
     const size_t scan_smem = scan_diff_smem ? diff_bytes : 0;
     set_smem(k_bin_scan, scan_smem);
     k_bin_scan<<<(g.n_st + 31) / 32, kScanThreads, scan_smem, st>>>(ws, g, cap, scan_diff_smem);
-    const size_t split8 = 2 * 8 * sd_bytes;
+    constexpr int NWS = SEELE_SPLIT_NW;
+    const size_t split8 = 2 * NWS * sd_bytes;
     if (split8 <= 128 * 1024) {
-        set_smem(k_bin_split<8>, split8);
-        k_bin_split<8><<<g.n_chunks, 8 * 32, split8, st>>>(ws, g);
+        set_smem(k_bin_split<NWS>, split8);
+        k_bin_split<NWS><<<g.n_chunks, NWS * 32, split8, st>>>(ws, g);
     } else {
         const size_t split4 = 2 * 4 * sd_bytes;
         set_smem(k_bin_split<4>, split4);

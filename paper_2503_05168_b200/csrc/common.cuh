@@ -59,7 +59,10 @@ constexpr int kLookSegs = 4;       // look-back epoch tag of the binning expand 
 
 // Binning (binning.cu): depth ranks cut into chunks of ~kBinChunkRanks (at least kBinChunksMin), super-tiles
 // of 4 x 4 tiles.
-constexpr long long kBinChunkRanks = 4096;
+#ifndef SEELE_BIN_CHUNK_RANKS
+#define SEELE_BIN_CHUNK_RANKS 4096
+#endif
+constexpr long long kBinChunkRanks = SEELE_BIN_CHUNK_RANKS;
 constexpr int kBinChunksMin = 64;
 constexpr int kBinChunksMax = 4096;
 constexpr int kSeg = 2048;  // entries per super-tile list segment (expand pass)

@@ -184,6 +184,29 @@ __device__ __noinline__ double exact_transmittance(const Workspace &ws, const ui
     return T;
 }
 
+// fp64 re-decision of the quad pixels in `need` (alpha inside its bracket): the reference's alpha and
+// its verdict alpha >= theta.  Out of line: the fp64 state stays out of the hot loop's registers.
+struct Redecided {
+    float al[4];
+    bool pass[4];
+};
+__device__ __noinline__ Redecided redecide(const Workspace &ws, uint32_t p, int x0, int y0, uint32_t need, double th) {
+    Redecided r;
+    const double2 m = ws.mean[p];
+    const double4 co = ws.conic_op[p];
+#pragma unroll
+    for (int s = 0; s < 4; s++) {
+        r.al[s] = 0.0f;
+        r.pass[s] = false;
+        if (!((need >> s) & 1u)) continue;
+        const double a64 =
+            alpha64((double)(x0 + (s & 1)) + 0.5, (double)(y0 + (s >> 1)) + 0.5, m.x, m.y, co.x, co.y, co.z, co.w);
+        r.al[s] = (float)a64;
+        r.pass[s] = a64 >= th;
+    }
+    return r;
+}
+
 // Pixel slot s of a quad array (s = 2 * row + column).
 __device__ __forceinline__ float &slot(float2 (&v)[2], int s) { return (s & 1) ? v[s >> 1].y : v[s >> 1].x; }
 
@@ -335,19 +358,22 @@ __global__ void __launch_bounds__(64, SEELE_RASTER_MINB) k_raster_quad(Workspace
                 // inside the bracket: decide with the reference formula in fp64 (rare); needed for live pixels
                 // and for the group leader pixel while its group is live
                 const bool glive = W == 4 ? (lb & gmask) != 0u : qlive;
+                uint32_t need = 0;
 #pragma unroll
                 for (int s = 0; s < 4; s++) {
-                    const int r = s >> 1;
-                    const bool need = slot(Lf, s) != 0.0f || (W >= 2 && s == 0 && leader_thread && glive);
-                    if (!need || fbits(slot(d, s)) > wb) continue;
-                    const double2 m = ws.mean[sg.p];
-                    const double4 co = ws.conic_op[sg.p];
-                    const double a64 = alpha64((double)(x0 + (s & 1)) + 0.5, (double)(y0 + r) + 0.5, m.x, m.y, co.x,
-                                               co.y, co.z, co.w);
-                    slot(al, s) = (float)a64;
-                    slot(d, s) = a64 >= th64 ? -1.0f : 1.0f;
-                    slot(E, s) = 6.2e-8f;  // rounding of a64 to float
-                    n_redecide++;
+                    const bool nd = slot(Lf, s) != 0.0f || (W >= 2 && s == 0 && leader_thread && glive);
+                    if (nd && fbits(slot(d, s)) <= wb) need |= 1u << s;
+                }
+                if (need) {
+                    const Redecided rd = redecide(ws, sg.p, x0, y0, need, th64);
+#pragma unroll
+                    for (int s = 0; s < 4; s++) {
+                        if (!((need >> s) & 1u)) continue;
+                        slot(al, s) = rd.al[s];
+                        slot(d, s) = rd.pass[s] ? -1.0f : 1.0f;
+                        slot(E, s) = 6.2e-8f;  // rounding of a64 to float
+                    }
+                    n_redecide += __popc(need);
                 }
             }
             uint32_t my = ~0u;  // all-ones if this thread's group leader passed (ref / w = 1: no leader test)
