@@ -1,4 +1,4 @@
-"""Runs bench.py over the BASELINE configs (C1-C5) and writes profiles/r01/configs.json."""
+"""Runs bench.py over the BASELINE configs (C1-C5) and writes profiles/r02/configs.json."""
 import json
 import subprocess
 import sys
