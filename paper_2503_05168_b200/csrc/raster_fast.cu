@@ -440,6 +440,13 @@ __global__ void __launch_bounds__(64, SEELE_RASTER_MINB) k_raster_quad(Workspace
                         n_skip -= (uint32_t)__popc(skipped >> j >> 1);
                     } else {
                         ambT |= 1u << s;
+#ifdef SEELE_AMB_PROFILE
+                        {  // (debug build: histogram of the relative bound D / T at T-ambiguous events)
+                            const float rel = slot(D, s) / fmaxf(slot(T, s), 1e-30f);
+                            const int bk = rel < 1e-5f ? 0 : rel < 1e-4f ? 1 : rel < 1e-3f ? 2 : rel < 1e-2f ? 3 : 4;
+                            atomicAdd((unsigned long long *)stats + 11 + bk, 1ull);
+                        }
+#endif
                     }
                 }
                 unsigned ambw = __ballot_sync(0xffffffffu, ambT != 0u);
@@ -510,6 +517,8 @@ __global__ void __launch_bounds__(64, SEELE_RASTER_MINB) k_raster_quad(Workspace
         atomicAdd(sp + 15, (unsigned long long)pr_death);
     }
     if (false) {
+#elif defined(SEELE_AMB_PROFILE)
+    if (false) {  // (debug build: counters 11..15 hold the D / T histogram of T-ambiguous events)
 #else
     if (lane == 0) {
 #endif

@@ -252,10 +252,16 @@ class FrameRenderer:
             raster_stream.cuda_stream if raster_stream is not None else None))
         return FrameOutput(image=image, contrib=contrib, stats=stats)
 
-    def render_checked(self, scene: DeviceScene, cam: CameraPose, cfg: EngineConfig, **kw) -> tuple[FrameOutput, np.ndarray]:
-        """Render, synchronise, and re-render with a larger workspace on overflow."""
+    def render_checked(self, scene: DeviceScene, cam: CameraPose, cfg: EngineConfig, *, before_sync=None,
+                       **kw) -> tuple[FrameOutput, np.ndarray]:
+        """Render, synchronise, and re-render with a larger workspace on overflow.
+        ``before_sync()`` runs once, after the first render is issued and before
+        the host waits for it (host work that overlaps the frame)."""
         for _ in range(4):
             out = self.render(scene, cam, cfg, **kw)
+            if before_sync is not None:
+                before_sync()
+                before_sync = None
             host = out.stats.cpu().numpy()
             if not host[_native.STAT_OVERFLOW]:
                 out.n_ws = int(host[_native.STAT_WORKING_SET])
@@ -264,7 +270,7 @@ class FrameRenderer:
             self.reserve(self.n_max, self.size[0], self.size[1], pair_capacity=int(need * 1.25) + 1024)
         raise DeviceError("tile-pair workspace could not be grown enough")
 
-    def render_to_host(self, scene: DeviceScene, cam: CameraPose, cfg: EngineConfig, **kw):
+    def render_to_host(self, scene: DeviceScene, cam: CameraPose, cfg: EngineConfig, *, before_sync=None, **kw):
         """Render and download image (float32), contributor counts and stats
         into pinned host buffers with one synchronisation; grows the workspace
         and re-renders on overflow.  The returned arrays are views into a
@@ -284,6 +290,9 @@ class FrameRenderer:
             st_h.copy_(out.stats, non_blocking=True)
             img_h.copy_(out.image, non_blocking=True)
             cnt_h.copy_(out.contrib, non_blocking=True)
+            if before_sync is not None:
+                before_sync()
+                before_sync = None
             torch.cuda.current_stream(self.device).synchronize()
             host = st_h.numpy()
             if not host[_native.STAT_OVERFLOW]:

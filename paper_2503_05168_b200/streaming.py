@@ -40,7 +40,7 @@ from .device import N_PLANES, DeviceScene
 from .errors import InvalidArgumentError
 from .model import CameraPose
 from .render import EngineConfig, RenderResult, _finish, get_renderer
-from .residency import select_clusters
+from .residency import _select_on_device
 
 
 def _slerp_extrapolate(q0: np.ndarray, q1: np.ndarray) -> np.ndarray:
@@ -120,6 +120,16 @@ class StreamingRenderer:
         counts = ch[1:, 1]
         self.n_max = int(self.shared_count + np.sort(counts)[::-1][:self.m + 1].sum())
         self.ranges = torch.empty((self.m + 2, 2), dtype=torch.int64, device=self.device)
+        self._rows_h = torch.empty((self.m + 2, 2), dtype=torch.int64).pin_memory()
+        # K0 state: centroids resident once, fixed buffers, its own stream
+        if self.m >= handle.num_clusters:
+            raise InvalidArgumentError(f"m must be < {handle.num_clusters}, got {self.m}")
+        self.sel_stream = torch.cuda.Stream(self.device)
+        self.sel_centroids = torch.from_numpy(np.ascontiguousarray(handle.centroids, dtype=np.float64)).to(self.device)
+        self.sel_chunks = torch.zeros((handle.num_clusters + 1, 2), dtype=torch.int64, device=self.device)
+        self.sel_ids = torch.empty(self.m + 1, dtype=torch.int32, device=self.device)
+        self.sel_ranges = torch.empty((self.m + 2, 2), dtype=torch.int64, device=self.device)
+        self.sel_host = torch.empty(self.m + 1, dtype=torch.int32).pin_memory()
 
     # -- residency ---------------------------------------------------------------
     def _copy(self, dst: int, src: int, count: int) -> None:
@@ -166,7 +176,14 @@ class StreamingRenderer:
 
     # -- reference API -----------------------------------------------------------
     def select(self, cam: CameraPose) -> list[int]:
-        return select_clusters(cam, self.container.centroids, self.m, self.beta, self.normalization)
+        """select_clusters (residency.py:38-54) by K0 on the device, on a stream of its own: the host needs
+        the ids to drive the copies, and the read-back must not wait for a frame rendering meanwhile."""
+        with torch.cuda.stream(self.sel_stream):
+            _select_on_device(cam, self.sel_centroids, self.m, self.beta, self.normalization, self.sel_chunks,
+                              self.sel_ids, self.sel_ranges, self.sel_stream)
+            self.sel_host.copy_(self.sel_ids, non_blocking=True)
+        self.sel_stream.synchronize()
+        return [int(v) for v in self.sel_host.numpy()]
 
     def render_frame(self, cam: CameraPose, cfg: EngineConfig, output: str = "numpy") -> RenderResult:
         """residency.py:222-264."""
@@ -180,15 +197,30 @@ class StreamingRenderer:
         st = torch.cuda.current_stream(self.device)
         rows = [[0, self.shared_count]] + [[self.shared_count + self.slot_of[c] * self.slot_size,
                                             int(self.container.chunks[c + 1, 1])] for c in needed]
-        self.ranges.copy_(torch.tensor(rows, dtype=torch.int64), non_blocking=False)
+        rows_h = self._rows_h
+        rows_h[:len(rows)] = torch.tensor(rows, dtype=torch.int64)
+        self.ranges[:len(rows)].copy_(rows_h[:len(rows)], non_blocking=True)  # (reused after this frame's sync)
         for c in needed:
             st.wait_event(self.ready[c])
         r = get_renderer(self.device)
-        kw = dict(ranges=self.ranges, n_ranges=len(rows), n_max=self.n_max)
+
+        def after_issue():
+            # prediction, prefetch and eviction on the host while the GPU renders the frame
+            self._last_render = torch.cuda.Event()
+            self._last_render.record(st)
+            self._advance(cam, needed)
+
+        kw = dict(ranges=self.ranges, n_ranges=len(rows), n_max=self.n_max, before_sync=after_issue)
         res = _finish(r, lambda **k: r.render_checked(self.scene, cam, cfg, **k),
                       lambda **k: r.render_to_host(self.scene, cam, cfg, **k), output, t0, kw)
-        self._last_render = torch.cuda.Event()
-        self._last_render.record(st)
+        self._recount()
+        res.stats.resident_bytes = self.resident_bytes
+        res.stats.stalls = self.stall_count
+        res.stats.prefetch_hits = self.prefetch_hit_count
+        return res
+
+    def _advance(self, cam: CameraPose, needed) -> None:
+        """residency.py:241-259: prefetch the clusters of the predicted next pose, evict the rest."""
         predicted = self.select(predict_pose(self.prev_pose if self.prev_pose is not None else cam, cam))
         self.prev_pose = cam
         if self.prefetch_enabled:
@@ -214,11 +246,6 @@ class StreamingRenderer:
                 self.slot_busy[slot] = self._last_render
                 self.free_slots.append(slot)
                 self.ready.pop(cid, None)
-        self._recount()
-        res.stats.resident_bytes = self.resident_bytes
-        res.stats.stalls = self.stall_count
-        res.stats.prefetch_hits = self.prefetch_hit_count
-        return res
 
     def close(self) -> None:
         pass
