@@ -88,3 +88,52 @@ def test_no_binned_splat():
     rng = np.random.default_rng(2)
     scene = random_scene(rng, 50, camera=cam, opacity_range=(0.0005, 0.003))  # all below alpha_theta: r^2 = 0
     _check(scene, cam, CFGS[:1])
+
+
+# ---- binning (binning.cu) geometry edges ----------------------------------------------------------------
+
+def _plan_check(scene, cam, cfg):
+    """The GPU plan's (tile, id) sequence and ranges against the oracle's sort_intersections."""
+    plan = plan_frame(DeviceScene.from_arrays(scene), cam, cfg)
+    want = O.plan(scene, cam, cfg)
+    pairs = plan.sorted_pairs
+    assert len(pairs) == want["tile_pairs"]
+    np.testing.assert_array_equal(pairs["tile_id"], want["pair_tile"])
+    np.testing.assert_array_equal(pairs["gaussian_ref"], want["pair_ref"])
+    got_r = {r.tile_id: (r.start, r.end) for r in plan.ranges}
+    for t in np.flatnonzero(want["range_end"] > want["range_start"]):
+        assert got_r[int(t)] == (int(want["range_start"][t]), int(want["range_end"][t]))
+
+
+def test_max_tile_axis_and_partial_super_tiles():
+    # 4096 x 200 px: 256 tile columns (the 8-bit packed rect at its limit, 64 super-tile columns), 13 tile rows
+    # (the last super-tile row holds one tile row); splats of every size down to single tiles
+    cam = make_camera(4096, 200)
+    rng = np.random.default_rng(44)
+    scene = random_scene(rng, 30_000, sh_degree=1, camera=cam, scale_range=(0.002, 0.3))
+    _plan_check(scene, cam, EngineConfig())
+    _check(scene, cam, (EngineConfig(engine="cr", group_w=2),))
+
+
+def test_odd_size_super_tile_edges():
+    # 1000 x 600 px: 63 x 38 tiles, partial super-tiles on the right and bottom edges
+    cam = make_camera(1000, 600)
+    rng = np.random.default_rng(45)
+    scene = random_scene(rng, 40_000, sh_degree=1, camera=cam, scale_range=(0.005, 0.25))
+    _plan_check(scene, cam, EngineConfig())
+
+
+def test_large_splats_beyond_the_head():
+    # screen-covering splats at every depth (not only the nearest ranks, which the per-tile head pass takes):
+    # their super-tile entries span the whole grid in every chunk
+    cam = make_camera(640, 384)
+    rng = np.random.default_rng(46)
+    scene = random_scene(rng, 20_000, sh_degree=1, camera=cam, scale_range=(0.01, 0.1))
+    big = rng.choice(len(scene.positions), 400, replace=False)
+    ls = scene.log_scales.copy()
+    ls[big] = np.log(rng.uniform(0.8, 2.5, size=(400, 3)))
+    op = scene.opacities.copy()
+    op[big] = rng.uniform(0.02, 0.08, size=400)  # faint, so the pixels behind them still blend
+    scene = SceneArrays(scene.positions, ls, scene.rotations, op, scene.sh, scene.ids)
+    _plan_check(scene, cam, EngineConfig())
+    _check(scene, cam, (EngineConfig(), EngineConfig(engine="cr", group_w=2)))
