@@ -96,7 +96,9 @@ __device__ __forceinline__ uint32_t depth_bucket_of_key(unsigned long long key, 
 // q' = q log2(e) / 2, so alpha = o 2^-q'; one 64-byte line, staged into
 // shared memory by four 16-byte cp.async per splat.
 struct __align__(16) RasterRec {
-    float mxh, mxl, myh, myl;  // mean in pixel coordinates as hi + lo floats
+    // mean in pixel coordinates: hi floats, the lo parts (m - hi, ~2^-24 |m|) folded into the Cholesky
+    // coordinates: u = l11 (x - mxh) + l21 (y - myh) - cu, w = l22 (y - myh) - cw
+    float mxh, cu, myh, cw;
     float l11, l21, l22, o;    // Cholesky factor of the conic in q' units; opacity
     float q_lo, w_up, e0, e1;  // pass: q' < q_lo; in the bracket (re-decided): 0 <= q' - q_lo <= w_up, else
                                // fail; alpha relative error <= e0 + e1 q'

@@ -138,9 +138,14 @@ __device__ __forceinline__ void load_splat(const SceneK &sc, long long i, int sh
 //
 // The raster evaluates q' = k q, k = log2(e) / 2, in fp32 in Cholesky form
 // q' = (l11 dx + l21 dy)^2 + (l22 dy)^2, with (l11, l21, l22) = fl32 of the
-// factor of k C (C = conic), and the tile-relative mean as a hi + lo float
-// pair:  dx = fl(fl(px - mx_hi) - mx_lo), dx1 = fl(dx + 1),
-// u1 = fma(l11, dx, fl(l21 dy)), q' = fma(u1, u1, fl(fl(l22 dy)^2)).
+// factor of k C (C = conic), and the mean as hi floats with the lo parts folded
+// into the coordinates: dx = fl(px - mx_hi), t = fma(l21, dy, -cu),
+// u1 = fma(l11, dx, t), w = fma(l22, dy, -cw), q' = fma(u1, u1, fl(w^2)),
+// cu = fl(l11 mx_lo + l21 my_lo), cw = fl(l22 my_lo).  The bound below was
+// derived for the hi + lo form dx = fl(fl(px - mx_hi) - mx_lo) (one more
+// rounding of each coordinate); the folded form has every rounding it has
+// except that one (cu, cw are ~2^-24 |m| |l|, their own rounding ~2^-48), so
+// the bound covers it.
 // With u = 2^-24, P = sqrt(trace(k C)) and |d| the pixel-to-mean distance:
 // |eta_dx|, |eta_dy| <= 3u (|d| + 1) and the coefficient / product roundings
 // give |q'32 - q'| <= 2u (5|d| + 3) P sqrt(q') + 4u q'.  With |d|^2 <=
@@ -199,13 +204,18 @@ __device__ __forceinline__ void write_raster_record(const Workspace &ws, long lo
     const double l11 = sqrt(K * ca);
     const double l21 = K * cb / l11;
     const double l22 = sqrt(fmax(K * det / ca, 0.0));
-    // raster record: the mean as hi + lo floats (|m - hi - lo| ~ 2^-48 |m|); q_up = the first float above
+    // raster record: the mean as hi floats + the folded lo parts (below); q_up = the first float above
     // the bracket top, so q' <= q_hi' <=> q' < q_up; the error model is widened by 2^-10 for the fp32
     // bound arithmetic of the raster (products with T rounded upward)
     const float mxh = (float)m0, myh = (float)m1;
     float4 *rec = reinterpret_cast<float4 *>(ws.rec + p);
-    rec[0] = make_float4(mxh, (float)(m0 - (double)mxh), myh, (float)(m1 - (double)myh));
-    rec[1] = make_float4((float)l11, (float)l21, (float)l22, (float)o);
+    // lo parts of the mean (exact in fp64) folded into the Cholesky coordinates with the float factors the
+    // raster uses; |cu|, |cw| ~ 2^-24 |m| |l|, so their own rounding is ~2^-48 |m| |l|: the raster's u, w
+    // carry no rounding of x - mxh - mxl (one fewer than the hi + lo form the error model was derived for)
+    const float l11f = (float)l11, l21f = (float)l21, l22f = (float)l22;
+    const double mxl = m0 - (double)mxh, myl = m1 - (double)myh;
+    rec[0] = make_float4(mxh, (float)((double)l11f * mxl + (double)l21f * myl), myh, (float)((double)l22f * myl));
+    rec[1] = make_float4(l11f, l21f, l22f, (float)o);
     // (q_lo, w_up): the bracket [q_lo, q_up) as its width rounded upward, so the raster tests it on
     // d = q' - q_lo alone (0 <= d <= w_up, compared as bit patterns); an empty bracket (o < theta) has w_up = 0
     const float q_up = nextafterf(rq.y, INFINITY);

@@ -27,7 +27,7 @@
 // warp adds per skipped splat from its (unchanged) live mask.
 //
 // Exactness (same discrete result as the fp64 reference), everything in fp32:
-//  * alpha test: q' = log2(e) q / 2 evaluated in fp32 (Cholesky form, hi/lo
+//  * alpha test: q' = log2(e) q / 2 evaluated in fp32 (Cholesky form, folded
 //    mean) has |q'32 - q'| <= e0q + e1q q' (derivation at
 //    write_raster_record), giving the bracket [q_lo, q_up): q'32 < q_lo
 //    passes, q'32 >= q_up fails, in between the pixel is re-decided with the
@@ -75,14 +75,6 @@ __device__ __forceinline__ void count_any(uint32_t &c, unsigned ballot, unsigned
         : "+r"(c)
         : "r"(ballot), "r"(mask));
 }
-// lf & (sign of d ? ~0 : 0) & g as a shift + one LOP3 (kept out of predicate/select form)
-__device__ __forceinline__ uint32_t sign_and(float d, uint32_t lf, uint32_t g) {
-    uint32_t r;
-    asm("{\n\t.reg .b32 t;\n\tshr.s32 t, %1, 31;\n\tlop3.b32 %0, t, %2, %3, 0x80;\n\t}"
-        : "=r"(r)
-        : "r"(__float_as_uint(d)), "r"(lf), "r"(g));
-    return r;
-}
 // sqrt within a few ulp (MUFU), for bounds that are widened anyway
 __device__ __forceinline__ float sqrt_approx(float x) {
     float y;
@@ -100,10 +92,10 @@ __device__ __forceinline__ float lane_of(const float2 &v, int c) { return c ? v.
 // preprocess.cu write_raster_record), pixel centres and mean in absolute
 // pixel coordinates: q[r] = (q of (x0, y0 + r), q of (x0 + 1, y0 + r)).
 __device__ __forceinline__ void quad_q(const Staged &sg, float2 lxp, float2 lyp, float2 q[2]) {
-    const float2 dx = __fadd2_rn(__fadd2_rn(lxp, f2(-sg.mxh)), f2(-sg.mxl));
-    const float2 dy = __fadd2_rn(__fadd2_rn(lyp, f2(-sg.myh)), f2(-sg.myl));
-    const float2 t = __fmul2_rn(f2(sg.l21), dy);
-    const float2 w = __fmul2_rn(f2(sg.l22), dy);
+    const float2 dx = __fadd2_rn(lxp, f2(-sg.mxh));
+    const float2 dy = __fadd2_rn(lyp, f2(-sg.myh));
+    const float2 t = __ffma2_rn(f2(sg.l21), dy, f2(-sg.cu));  // (the mean's lo parts, write_raster_record)
+    const float2 w = __ffma2_rn(f2(sg.l22), dy, f2(-sg.cw));
     const float2 ww = __fmul2_rn(w, w);
     const float2 u0 = __ffma2_rn(f2(sg.l11), dx, f2(t.x)), u1 = __ffma2_rn(f2(sg.l11), dx, f2(t.y));
     q[0] = __ffma2_rn(u0, u0, f2(ww.x));
@@ -145,6 +137,8 @@ __device__ __forceinline__ bool rect_reaches(float mx, float my, float l11, floa
 // alpha_k >= theta (a live pixel keeps its group live).  alpha >= theta is
 // decided from fp64 q against the fp32 bracket (valid a fortiori), with the
 // reference formula inside it.
+// (NeedAlpha = false: only the verdict, e.g. of a CR group leader; alpha is not computed when the bracket decides)
+template <bool NeedAlpha>
 __device__ __forceinline__ bool exact_test(double px, double py, const double2 &m, const double4 &co, float q_lo,
                                            float w_up, double th, double &a) {
     const double dx = px - m.x, dy = py - m.y;
@@ -152,7 +146,7 @@ __device__ __forceinline__ bool exact_test(double px, double py, const double2 &
     const double qp = kQ * q;
     if (qp > (double)q_lo + (double)w_up) return false;  // (an empty bracket: q_lo = -inf, w_up = 0)
     if (qp < (double)q_lo) {
-        a = fmin(co.w * exp(-0.5 * q), kAlphaClamp);
+        if (NeedAlpha) a = fmin(co.w * exp(-0.5 * q), kAlphaClamp);
         return true;
     }
     a = alpha64(px, py, m.x, m.y, co.x, co.y, co.z, co.w);
@@ -164,19 +158,47 @@ __device__ __forceinline__ bool exact_test(double px, double py, const double2 &
 // reference's running product: relative difference ~1e-15, far inside any
 // decision margin that reaches this path).
 template <int W>
-__device__ __noinline__ double exact_transmittance(const Workspace &ws, const uint32_t *__restrict__ pair_pos,
+__device__ __forceinline__ double exact_transmittance(const Workspace &ws, const uint32_t *__restrict__ pair_pos,
                                                    uint32_t k0, uint32_t k1, int px, int py, int lx, int ly,
                                                    double th) {
     const int lane = threadIdx.x & 31;
     double T = 1.0;
-    for (uint32_t k = k0 + lane; k <= k1; k += 32) {
+    // kWalkU splats per lane and round, their loads issued before any is used: a long walk (C4: ~1-2K
+    // splats per event) pays the dependent-load latency (position, then record) once per round
+#ifndef SEELE_WALK_U
+#define SEELE_WALK_U 1
+#endif
+    constexpr int kU = SEELE_WALK_U;
+    uint32_t k = k0 + lane;
+    for (; k + 32 * (kU - 1) <= k1; k += 32 * kU) {
+        uint32_t p[kU];
+#pragma unroll
+        for (int u = 0; u < kU; u++) p[u] = pair_pos[k + 32 * u];
+        double2 m[kU];
+        double4 co[kU];
+        float2 f[kU];
+#pragma unroll
+        for (int u = 0; u < kU; u++) {
+            m[u] = ws.mean[p[u]];
+            co[u] = ws.conic_op[p[u]];
+            f[u] = reinterpret_cast<const float2 *>(ws.rec + p[u])[4];  // (q_lo, w_up)
+        }
+#pragma unroll
+        for (int u = 0; u < kU; u++) {
+            double a;
+            if (W >= 2 && !exact_test<false>(lx + 0.5, ly + 0.5, m[u], co[u], f[u].x, f[u].y, th, a)) continue;
+            if (!exact_test<true>(px + 0.5, py + 0.5, m[u], co[u], f[u].x, f[u].y, th, a)) continue;
+            T = __dmul_rn(T, __dsub_rn(1.0, a));
+        }
+    }
+    for (; k <= k1; k += 32) {
         const uint32_t p = pair_pos[k];
         const double2 m = ws.mean[p];
         const double4 co = ws.conic_op[p];
-        const float4 f = reinterpret_cast<const float4 *>(ws.rec + p)[2];  // (q_lo, w_up, e0, e1)
+        const float2 f = reinterpret_cast<const float2 *>(ws.rec + p)[4];  // (q_lo, w_up)
         double a;
-        if (W >= 2 && !exact_test(lx + 0.5, ly + 0.5, m, co, f.x, f.y, th, a)) continue;
-        if (!exact_test(px + 0.5, py + 0.5, m, co, f.x, f.y, th, a)) continue;
+        if (W >= 2 && !exact_test<false>(lx + 0.5, ly + 0.5, m, co, f.x, f.y, th, a)) continue;
+        if (!exact_test<true>(px + 0.5, py + 0.5, m, co, f.x, f.y, th, a)) continue;
         T = __dmul_rn(T, __dsub_rn(1.0, a));
     }
 #pragma unroll
@@ -210,21 +232,31 @@ __device__ __noinline__ Redecided redecide(const Workspace &ws, uint32_t p, int 
 // Pixel slot s of a quad array (s = 2 * row + column).
 __device__ __forceinline__ float &slot(float2 (&v)[2], int s) { return (s & 1) ? v[s >> 1].y : v[s >> 1].x; }
 
+// SEELE_RASTER_WARPS = 1: one warp (half tile) per CTA, so a warp that finishes early frees its slot
+// instead of waiting for the other half of its tile; 2: one CTA of two warps per tile
+#ifndef SEELE_RASTER_WARPS
+#define SEELE_RASTER_WARPS 2
+#endif
+constexpr int kRWarps = SEELE_RASTER_WARPS;
 #ifndef SEELE_RASTER_MINB
-#define SEELE_RASTER_MINB 7  // (8 CTAs still fit at 128 registers; 7 schedules better: 0.584 -> 0.567 ms)
+#define SEELE_RASTER_MINB (14 / kRWarps)  // (8 two-warp CTAs still fit at 128 registers; 7 schedules better: 0.584 -> 0.567 ms)
 #endif
 template <int W>
-__global__ void __launch_bounds__(64, SEELE_RASTER_MINB) k_raster_quad(Workspace ws, const uint32_t *__restrict__ pair_pos, CamK cam,
+__global__ void __launch_bounds__(32 * kRWarps, SEELE_RASTER_MINB) k_raster_quad(Workspace ws, const uint32_t *__restrict__ pair_pos, CamK cam,
                                                         CfgK cfg, float *image, int32_t *contrib, int64_t *stats) {
     // per warp, double-buffered: each warp stages and walks the list on its own; batch b + 1 is in flight
     // (cp.async) while batch b is rasterized
-    __shared__ Staged s_stage[2][2][kBatch];
-    __shared__ float4 s_box[2][2][kBatch];
+    __shared__ Staged s_stage[kRWarps][2][kBatch];
+    __shared__ float4 s_box[kRWarps][2][kBatch];
     // per pixel: tile splats it was live for (written at its death)
-    __shared__ uint32_t s_di[64][4];
-    __shared__ float s_T[64][4];  // per pixel: transmittance at its death
-    const int tile = (int)ws.tile_order[blockIdx.x];  // heavy tiles first (binning.cu k_pair_scan)
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    __shared__ uint32_t s_di[32 * kRWarps][4];
+    __shared__ float s_T[32 * kRWarps][4];  // per pixel: transmittance at its death
+    // heavy tiles first (binning.cu k_bin_scan); with one warp per CTA, CTAs 2t and 2t + 1 are the halves of tile t
+    const int tile = (int)ws.tile_order[kRWarps == 2 ? blockIdx.x : blockIdx.x >> 1];
+    const int lid = threadIdx.x;  // thread within the CTA (shared-memory slot)
+    const int wslot = lid >> 5;   // warp within the CTA (shared-memory slot)
+    const int tid = kRWarps == 2 ? lid : (int)((blockIdx.x & 1u) << 5) + lid;  // thread within the tile
+    const int lane = tid & 31, warp = tid >> 5;
     const int mw = tid >> 3, i = tid & 7;
     const unsigned bm = 0xffu << (lane & 24);  // this model-warp's byte of a warp ballot
     int bx, by;
@@ -240,7 +272,7 @@ __global__ void __launch_bounds__(64, SEELE_RASTER_MINB) k_raster_quad(Workspace
     // Liveness as 0 / 1 float factors (1.0f = 0x3f800000): a pixel's blend factor is its pass sign mask & live
     // & its group leader's verdict, one LOP3 per pixel.  Out-of-image pixels start dead.
     float2 Lf[2];
-    uint32_t *di = s_di[tid];
+    uint32_t *di = s_di[lid];
 #pragma unroll
     for (int s = 0; s < 4; s++) {
         const bool v = x0 + (s & 1) < cam.width && y0 + (s >> 1) < cam.height;
@@ -280,10 +312,10 @@ __global__ void __launch_bounds__(64, SEELE_RASTER_MINB) k_raster_quad(Workspace
     auto stage = [&](uint32_t idx, uint32_t p, int buf) {
         if (idx < rg.y) {
             const float4 *src = reinterpret_cast<const float4 *>(ws.rec + p);
-            float4 *dst = reinterpret_cast<float4 *>(&s_stage[warp][buf][lane]);
+            float4 *dst = reinterpret_cast<float4 *>(&s_stage[wslot][buf][lane]);
 #pragma unroll
             for (int k = 0; k < 4; k++) cp_async16(dst + k, src + k);
-            cp_async16(&s_box[warp][buf][lane], ws.bbox + p);
+            cp_async16(&s_box[wslot][buf][lane], ws.bbox + p);
         }
         cp_async_commit();
     };
@@ -298,20 +330,21 @@ __global__ void __launch_bounds__(64, SEELE_RASTER_MINB) k_raster_quad(Workspace
         p_next = i2 < rg.y ? pair_pos[i2] : 0u;
         cp_async_wait<1>();  // this lane's part of batch b has landed
         __syncwarp();
-        const Staged *s_g = s_stage[warp][buf];
+        const Staged *s_g = s_stage[wslot][buf];
         bool rel = false;
         if (b0 + lane < rg.y) {
             const Staged &sv = s_g[lane];
-            const float4 bb = s_box[warp][buf][lane];
+            const float4 bb = s_box[wslot][buf][lane];
             rel = bb.y >= ox + 0.5f && bb.x <= ox + 15.5f && bb.w >= oy + ry0 && bb.z <= oy + ry1;
             if (rel) {
                 // exact refinement in tile-relative floats; the margin covers the fp32 evaluation (twice the
                 // bracket width) and the float mean, |error| <= ep = 2^-23 (|d| + 32) px, times
                 // |grad q'| <= 2 P sqrt(q')
-                const float mx = (sv.mxh - (float)ox) + sv.mxl, my = (sv.myh - (float)oy) + sv.myl;
+                const float mx = sv.mxh - (float)ox, my = sv.myh - (float)oy;
                 // (margin terms only need upper bounds: approximate square roots, widened by 1e-4)
                 const float P = 1.0001f * sqrt_approx(fmaf(sv.l11, sv.l11, fmaf(sv.l21, sv.l21, sv.l22 * sv.l22)));
-                const float ep = 1.2e-7f * (fabsf(mx) + fabsf(my) + 32.0f);
+                // (the hi mean alone: its lo part, <= 2^-24 |m|, joins the tile-relative rounding)
+                const float ep = 1.2e-7f * (fabsf(mx) + fabsf(my) + fabsf(sv.mxh) + fabsf(sv.myh) + 32.0f);
                 const float qh = __fadd_ru(sv.q_lo, sv.w_up), pe = P * ep;  // top of the alpha bracket
                 const float qm = qh + 2.0f * (qh - sv.q_lo) + 1e-6f * qh + 2.2f * pe * (1.0001f * sqrt_approx(fmaxf(qh, 0.f))) +
                                  1.1f * pe * pe + 1e-6f;
@@ -345,16 +378,21 @@ __global__ void __launch_bounds__(64, SEELE_RASTER_MINB) k_raster_quad(Workspace
                 amb |= fbits(d[r].x) <= wb;
                 amb |= fbits(d[r].y) <= wb;
             }
-            // alpha = min(o 2^-q', 0.99): the clamp can only bind for o > 0.99 (the error model covers
-            // 0.99f vs 0.99 and a clamp of the exact value)
-            if (sg.o > 0.99f) {
+            // pass masks: all ones <=> q' < q_lo (surely passes), from the sign of d
+            uint32_t sgn[4];
 #pragma unroll
-                for (int r = 0; r < 2; r++) al[r] = make_float2(fminf(al[r].x, 0.99f), fminf(al[r].y, 0.99f));
-            }
+            for (int s = 0; s < 4; s++) sgn[s] = (uint32_t)((int)fbits(slot(d, s)) >> 31);
+            // alpha = min(o 2^-q', 0.99): the clamp can only bind for o > 0.99 (the error model covers
+            // 0.99f vs 0.99 and a clamp of the exact value); such splats (warp-uniform) take the rare path
+            const bool hi_o = sg.o > 0.99f;
 #ifdef SEELE_RASTER_PROFILE
             pr_amb += __any_sync(0xffffffffu, amb);
 #endif
-            if (__any_sync(0xffffffffu, amb)) {
+            if (__any_sync(0xffffffffu, amb || hi_o)) {
+                if (hi_o) {
+#pragma unroll
+                    for (int r = 0; r < 2; r++) al[r] = make_float2(fminf(al[r].x, 0.99f), fminf(al[r].y, 0.99f));
+                }
                 // inside the bracket: decide with the reference formula in fp64 (rare); needed for live pixels
                 // and for the group leader pixel while its group is live
                 const bool glive = W == 4 ? (lb & gmask) != 0u : qlive;
@@ -370,7 +408,7 @@ __global__ void __launch_bounds__(64, SEELE_RASTER_MINB) k_raster_quad(Workspace
                     for (int s = 0; s < 4; s++) {
                         if (!((need >> s) & 1u)) continue;
                         slot(al, s) = rd.al[s];
-                        slot(d, s) = rd.pass[s] ? -1.0f : 1.0f;
+                        sgn[s] = rd.pass[s] ? ~0u : 0u;
                         slot(E, s) = 6.2e-8f;  // rounding of a64 to float
                     }
                     n_redecide += __popc(need);
@@ -380,20 +418,21 @@ __global__ void __launch_bounds__(64, SEELE_RASTER_MINB) k_raster_quad(Workspace
             if (W == 2 || W == 4) {
                 // the leader's alpha counts even if the leader pixel is done (rasterize.py:281)
                 const bool glive = W == 4 ? (lb & gmask) != 0u : qlive;
-                const bool lp = leader_thread && glive && (int)fbits(d[0].x) < 0;
+                const bool lp = leader_thread && glive && sgn[0] != 0u;
                 const unsigned pb = __ballot_sync(0xffffffffu, lp);
 #ifdef SEELE_RASTER_PROFILE
                 pr_nolead += pb == 0u;
 #endif
                 count_any(c_alpha, pb, bm);
                 // w = 2: the group is the thread's own quad, its leader verdict is lp itself
-                my = W == 2 ? (lp ? ~0u : 0u) : 0u - ((pb >> leader_lane) & 1u);
+                my = W == 2 ? (glive ? sgn[0] : 0u) : 0u - ((pb >> leader_lane) & 1u);
             }
+            // blend factors: pass mask & liveness (1.0f / 0) & the leader's verdict, one LOP3 per pixel
             float2 m[2];
 #pragma unroll
             for (int r = 0; r < 2; r++)
-                m[r] = make_float2(__uint_as_float(sign_and(d[r].x, fbits(Lf[r].x), my)),
-                                   __uint_as_float(sign_and(d[r].y, fbits(Lf[r].y), my)));
+                m[r] = make_float2(__uint_as_float(sgn[2 * r] & fbits(Lf[r].x) & my),
+                                   __uint_as_float(sgn[2 * r + 1] & fbits(Lf[r].y) & my));
             const unsigned bb =
                 __ballot_sync(0xffffffffu, (fbits(m[0].x) | fbits(m[0].y) | fbits(m[1].x) | fbits(m[1].y)) != 0u);
 #ifdef SEELE_RASTER_PROFILE
@@ -411,16 +450,19 @@ __global__ void __launch_bounds__(64, SEELE_RASTER_MINB) k_raster_quad(Workspace
                 C[r][0] = __ffma2_rn(wgt, f2(rc3.x), C[r][0]);
                 C[r][1] = __ffma2_rn(wgt, f2(rc3.y), C[r][1]);
                 C[r][2] = __ffma2_rn(wgt, f2(rc3.z), C[r][2]);
-                const float2 omm = __ffma2_rn(am, f2(-1.0f), f2(1.0f));  // 1 - alpha, or 1 (exact)
-                // |omm - (1 - alpha_ref)| <= alpha (e0 + e1 q') + 1e-7 (rounding of 1 - alpha and of T omm)
+                const float2 nam = make_float2(-am.x, -am.y);  // (a negated operand, no instruction)
+                const float2 omm = __fadd2_rn(f2(1.0f), nam);  // 1 - alpha, or 1
+                // |omm - (1 - alpha_ref)| <= alpha (e0 + e1 q'); the new T = T - T alpha has one rounding of
+                // the exact T (1 - alpha32) after the rounding of T alpha, together <= 2^-24 T: the 1e-7 T term
                 const float2 efm = __fmul2_rn(__ffma2_rn(al[r], E[r], f2(1.0e-7f)), m[r]);
-                const float2 t1 = __fmul2_rn(t0, omm);
+                const float2 t1 = __fadd2_rn(t0, make_float2(-wgt.x, -wgt.y));
                 const float2 d1 = __ffma2_ru(D[r], omm, __fmul2_ru(t0, efm));
                 T[r] = t1;
                 D[r] = d1;
                 // sign set <=> T32 - D < gamma (rounded so that a clear sign proves T >= gamma); done pixels carry
                 // T = 1e30 (their transmittance is parked in s_T) and never test positive
-                y[r] = __fadd2_rn(t1, __fmul2_rn(__fadd2_ru(d1, f2(gm)), f2(-1.0f)));
+                const float2 dg = __fadd2_ru(d1, f2(gm));
+                y[r] = __fadd2_rn(t1, make_float2(-dg.x, -dg.y));
                 cnt[r] = __fadd2_rn(cnt[r], m[r]);
             }
             if (__any_sync(0xffffffffu, (int)(fbits(y[0].x) | fbits(y[0].y) | fbits(y[1].x) | fbits(y[1].y)) < 0)) {
@@ -433,7 +475,7 @@ __global__ void __launch_bounds__(64, SEELE_RASTER_MINB) k_raster_quad(Workspace
                     if ((int)fbits(slot(y, s)) >= 0) continue;
                     if (__fadd_ru(slot(T, s), slot(D, s)) < gm) {  // surely below: done
                         slot(Lf, s) = 0.0f;
-                        s_T[tid][s] = slot(T, s);
+                        s_T[lid][s] = slot(T, s);
                         slot(T, s) = 1e30f;
                         di[s] = b0 + (uint32_t)j - rg.x + 1u;  // its death step: tile splats processed
                         nlive--;
@@ -471,7 +513,7 @@ __global__ void __launch_bounds__(64, SEELE_RASTER_MINB) k_raster_quad(Workspace
                             slot(D, ss) = 6.0e-8f * (float)Tx;
                             if (Tx < cfg.gamma) {
                                 slot(Lf, ss) = 0.0f;
-                                s_T[tid][ss] = slot(T, ss);
+                                s_T[lid][ss] = slot(T, ss);
                                 slot(T, ss) = 1e30f;
                                 di[ss] = b0 + (uint32_t)j - rg.x + 1u;
                                 nlive--;
@@ -534,7 +576,7 @@ __global__ void __launch_bounds__(64, SEELE_RASTER_MINB) k_raster_quad(Workspace
         if (x0 + (s & 1) >= cam.width || y0 + (s >> 1) >= cam.height) continue;
         const long long pix = (long long)(y0 + (s >> 1)) * cam.width + x0 + (s & 1);
         const int r = s >> 1, c = s & 1;
-        const float Ts = slot(Lf, s) != 0.0f ? slot(T, s) : s_T[tid][s];
+        const float Ts = slot(Lf, s) != 0.0f ? slot(T, s) : s_T[lid][s];
         image[3 * pix + 0] = fmaf(Ts, (float)cfg.bg[0], lane_of(C[r][0], c));  // background (rasterize.py:228-231)
         image[3 * pix + 1] = fmaf(Ts, (float)cfg.bg[1], lane_of(C[r][1], c));
         image[3 * pix + 2] = fmaf(Ts, (float)cfg.bg[2], lane_of(C[r][2], c));
@@ -551,12 +593,12 @@ __global__ void __launch_bounds__(64, SEELE_RASTER_MINB) k_raster_quad(Workspace
 
 void launch_raster_fast(int W, const Workspace &ws, const uint32_t *pair_pos, const CamK &cam, const CfgK &cfg,
                         float *image, int32_t *contrib, int64_t *stats, cudaStream_t st) {
-    const int n_tiles = cam.tiles_x * cam.tiles_y;
+    const int n_cta = cam.tiles_x * cam.tiles_y * (2 / kRWarps), nt = 32 * kRWarps;
     switch (W) {
-        case 0: k_raster_quad<0><<<n_tiles, 64, 0, st>>>(ws, pair_pos, cam, cfg, image, contrib, stats); break;
-        case 1: k_raster_quad<1><<<n_tiles, 64, 0, st>>>(ws, pair_pos, cam, cfg, image, contrib, stats); break;
-        case 2: k_raster_quad<2><<<n_tiles, 64, 0, st>>>(ws, pair_pos, cam, cfg, image, contrib, stats); break;
-        default: k_raster_quad<4><<<n_tiles, 64, 0, st>>>(ws, pair_pos, cam, cfg, image, contrib, stats); break;
+        case 0: k_raster_quad<0><<<n_cta, nt, 0, st>>>(ws, pair_pos, cam, cfg, image, contrib, stats); break;
+        case 1: k_raster_quad<1><<<n_cta, nt, 0, st>>>(ws, pair_pos, cam, cfg, image, contrib, stats); break;
+        case 2: k_raster_quad<2><<<n_cta, nt, 0, st>>>(ws, pair_pos, cam, cfg, image, contrib, stats); break;
+        default: k_raster_quad<4><<<n_cta, nt, 0, st>>>(ws, pair_pos, cam, cfg, image, contrib, stats); break;
     }
 }
 
