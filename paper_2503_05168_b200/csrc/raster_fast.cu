@@ -239,7 +239,7 @@ __device__ __forceinline__ float &slot(float2 (&v)[2], int s) { return (s & 1) ?
 #endif
 constexpr int kRWarps = SEELE_RASTER_WARPS;
 #ifndef SEELE_RASTER_MINB
-#define SEELE_RASTER_MINB (14 / kRWarps)  // (8 two-warp CTAs still fit at 128 registers; 7 schedules better: 0.584 -> 0.567 ms)
+#define SEELE_RASTER_MINB (18 / kRWarps)  // (nine two-warp CTAs: ~95 registers, no spills; C3 0.524 -> 0.515 ms vs 7, 8 and 10 measured)
 #endif
 template <int W>
 __global__ void __launch_bounds__(32 * kRWarps, SEELE_RASTER_MINB) k_raster_quad(Workspace ws, const uint32_t *__restrict__ pair_pos, CamK cam,
