@@ -271,7 +271,7 @@ int seele_render_split(const seele_scene *scene, const int64_t *ranges_dev, int3
     cf.precision = cfg->precision & ~SEELE_KEEP_UNBINNED;
     cf.keep_unbinned = (cfg->precision & SEELE_KEEP_UNBINNED) != 0;
     cf.alpha_theta = cfg->alpha_theta;
-    cf.gamma = cfg->gamma_threshold;
+    set_gamma(cf, cfg->gamma_threshold);
     for (int i = 0; i < 3; i++) cf.bg[i] = cfg->background[i];
     SceneK sk;
     sk.layout = scene->layout;
@@ -404,7 +404,7 @@ int seele_harvest_topk(void *workspace, int64_t n_max, int64_t pair_capacity, co
     cf.engine = cfg->engine;
     cf.group_w = cfg->group_w;
     cf.alpha_theta = cfg->alpha_theta;
-    cf.gamma = cfg->gamma_threshold;
+    set_gamma(cf, cfg->gamma_threshold);
     launch_harvest(cfg->engine == 0 ? 0 : cfg->group_w, ws, ws.pfinal, ck, cf, ids_dev, k, flags_dev,
                    static_cast<cudaStream_t>(stream));
     cudaError_t e;
@@ -426,7 +426,7 @@ int seele_contributions(void *workspace, int64_t n_max, int64_t pair_capacity, c
     cf.engine = cfg->engine;
     cf.group_w = cfg->group_w;
     cf.alpha_theta = cfg->alpha_theta;
-    cf.gamma = cfg->gamma_threshold;
+    set_gamma(cf, cfg->gamma_threshold);
     launch_contributions(cfg->engine == 0 ? 0 : cfg->group_w, ws, ws.pfinal, ck, cf, n_ws, row_of_pos_dev, out_dev,
                          static_cast<cudaStream_t>(stream));
     cudaError_t e;
@@ -447,7 +447,7 @@ int seele_skip_bound(void *workspace, int64_t n_max, int64_t pair_capacity, cons
     cf.engine = cfg->engine;
     cf.group_w = cfg->group_w;
     cf.alpha_theta = cfg->alpha_theta;
-    cf.gamma = cfg->gamma_threshold;
+    set_gamma(cf, cfg->gamma_threshold);
     launch_skip_bound(cfg->group_w, ws, ws.pfinal, ck, cf, bound_dev, static_cast<cudaStream_t>(stream));
     cudaError_t e;
     if ((e = cudaGetLastError()) != cudaSuccess) return cuda_fail(e, "seele_skip_bound");

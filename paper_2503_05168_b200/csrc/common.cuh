@@ -1,6 +1,7 @@
 // Internal declarations shared by the sm_100a kernels of the Seele render path.
 #pragma once
 #include <cuda_runtime.h>
+#include <math.h>
 #include <stdint.h>
 
 #include "../../include/seele_b200.h"
@@ -26,7 +27,18 @@ struct CfgK {
     int keep_unbinned;  // SEELE_KEEP_UNBINNED: records of projected splats that bin to no tile (plan export)
     double alpha_theta, gamma;
     double bg[3];
+    // gamma as floats rounded up / down (set_gamma): the FAST raster proves T >= gamma with gamma_up and
+    // T < gamma with gamma_dn
+    float gamma_up, gamma_dn;
 };
+inline void set_gamma(CfgK &c, double g) {
+    c.gamma = g;
+    float up = (float)g, dn = (float)g;
+    if ((double)up < g) up = nextafterf(up, INFINITY);
+    if ((double)dn > g) dn = nextafterf(dn, -INFINITY);
+    c.gamma_up = up;
+    c.gamma_dn = dn;
+}
 
 struct SceneK {
     int layout;

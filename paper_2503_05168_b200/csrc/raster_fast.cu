@@ -290,7 +290,6 @@ __global__ void __launch_bounds__(32 * kRWarps, SEELE_RASTER_MINB) k_raster_quad
     const unsigned gmask = 0x33u << ((lane & ~7) + g_off);
     const bool leader_thread = W != 4 || (i == g_off);
     const double th64 = cfg.alpha_theta;
-    const float gm = (float)cfg.gamma;
     float2 T[2], D[2], C[2][3], cnt[2];
 #pragma unroll
     for (int r = 0; r < 2; r++) {
@@ -382,63 +381,70 @@ __global__ void __launch_bounds__(32 * kRWarps, SEELE_RASTER_MINB) k_raster_quad
             uint32_t sgn[4];
 #pragma unroll
             for (int s = 0; s < 4; s++) sgn[s] = (uint32_t)((int)fbits(slot(d, s)) >> 31);
+            // group leader verdicts, blend factors (pass mask & liveness (1.0f / 0) & the leader's verdict,
+            // one LOP3 per pixel) and the warp's blend ballot, from the pass masks
+            const bool glive = W == 4 ? (lb & gmask) != 0u : qlive;
+            unsigned pb = 0u, bb;
+            float2 m[2];
+            auto verdicts = [&]() {
+                uint32_t my = ~0u;  // all-ones if this thread's group leader passed (ref / w = 1: no leader test)
+                if (W == 2 || W == 4) {
+                    // the leader's alpha counts even if the leader pixel is done (rasterize.py:281)
+                    pb = __ballot_sync(0xffffffffu, leader_thread && glive && sgn[0] != 0u);
+                    // w = 2: the group is the thread's own quad, its leader verdict is its own pass mask
+                    my = W == 2 ? (glive ? sgn[0] : 0u) : 0u - ((pb >> leader_lane) & 1u);
+                }
+#pragma unroll
+                for (int r = 0; r < 2; r++)
+                    m[r] = make_float2(__uint_as_float(sgn[2 * r] & fbits(Lf[r].x) & my),
+                                       __uint_as_float(sgn[2 * r + 1] & fbits(Lf[r].y) & my));
+                bb = __ballot_sync(0xffffffffu,
+                                   (fbits(m[0].x) | fbits(m[0].y) | fbits(m[1].x) | fbits(m[1].y)) != 0u);
+            };
             // alpha = min(o 2^-q', 0.99): the clamp can only bind for o > 0.99 (the error model covers
             // 0.99f vs 0.99 and a clamp of the exact value); such splats (warp-uniform) take the rare path
             const bool hi_o = sg.o > 0.99f;
+            const bool rare = __any_sync(0xffffffffu, amb || hi_o);
+            // the verdicts are formed before the rare branch resolves (its vote's latency overlaps them) and
+            // formed again on the rare path
+            verdicts();
 #ifdef SEELE_RASTER_PROFILE
             pr_amb += __any_sync(0xffffffffu, amb);
 #endif
-            if (__any_sync(0xffffffffu, amb || hi_o)) {
+            if (rare) {
                 if (hi_o) {
 #pragma unroll
                     for (int r = 0; r < 2; r++) al[r] = make_float2(fminf(al[r].x, 0.99f), fminf(al[r].y, 0.99f));
                 }
                 // inside the bracket: decide with the reference formula in fp64 (rare); needed for live pixels
                 // and for the group leader pixel while its group is live
-                const bool glive = W == 4 ? (lb & gmask) != 0u : qlive;
                 uint32_t need = 0;
 #pragma unroll
                 for (int s = 0; s < 4; s++) {
                     const bool nd = slot(Lf, s) != 0.0f || (W >= 2 && s == 0 && leader_thread && glive);
                     if (nd && fbits(slot(d, s)) <= wb) need |= 1u << s;
                 }
-                if (need) {
-                    const Redecided rd = redecide(ws, sg.p, x0, y0, need, th64);
+                if (__any_sync(0xffffffffu, need != 0u)) {
+                    if (need) {
+                        const Redecided rd = redecide(ws, sg.p, x0, y0, need, th64);
 #pragma unroll
-                    for (int s = 0; s < 4; s++) {
-                        if (!((need >> s) & 1u)) continue;
-                        slot(al, s) = rd.al[s];
-                        sgn[s] = rd.pass[s] ? ~0u : 0u;
-                        slot(E, s) = 6.2e-8f;  // rounding of a64 to float
+                        for (int s = 0; s < 4; s++) {
+                            if (!((need >> s) & 1u)) continue;
+                            slot(al, s) = rd.al[s];
+                            sgn[s] = rd.pass[s] ? ~0u : 0u;
+                            slot(E, s) = 6.2e-8f;  // rounding of a64 to float
+                        }
+                        n_redecide += __popc(need);
                     }
-                    n_redecide += __popc(need);
+                    verdicts();
                 }
             }
-            uint32_t my = ~0u;  // all-ones if this thread's group leader passed (ref / w = 1: no leader test)
-            if (W == 2 || W == 4) {
-                // the leader's alpha counts even if the leader pixel is done (rasterize.py:281)
-                const bool glive = W == 4 ? (lb & gmask) != 0u : qlive;
-                const bool lp = leader_thread && glive && sgn[0] != 0u;
-                const unsigned pb = __ballot_sync(0xffffffffu, lp);
+            if (W == 2 || W == 4) count_any(c_alpha, pb, bm);
 #ifdef SEELE_RASTER_PROFILE
-                pr_nolead += pb == 0u;
-#endif
-                count_any(c_alpha, pb, bm);
-                // w = 2: the group is the thread's own quad, its leader verdict is lp itself
-                my = W == 2 ? (glive ? sgn[0] : 0u) : 0u - ((pb >> leader_lane) & 1u);
-            }
-            // blend factors: pass mask & liveness (1.0f / 0) & the leader's verdict, one LOP3 per pixel
-            float2 m[2];
-#pragma unroll
-            for (int r = 0; r < 2; r++)
-                m[r] = make_float2(__uint_as_float(sgn[2 * r] & fbits(Lf[r].x) & my),
-                                   __uint_as_float(sgn[2 * r + 1] & fbits(Lf[r].y) & my));
-            const unsigned bb =
-                __ballot_sync(0xffffffffu, (fbits(m[0].x) | fbits(m[0].y) | fbits(m[1].x) | fbits(m[1].y)) != 0u);
-#ifdef SEELE_RASTER_PROFILE
+            pr_nolead += pb == 0u;
             pr_noblend += bb == 0u;
 #endif
-            if (bb == 0u) continue;
+            if (bb == 0u) continue;  // (no pixel of the warp blends: 5 % of C3's steps)
             count_any(c_blend, bb, bm);
             if (W == 1) count_any(c_alpha, bb, bm);  // each pixel is its own leader
             float2 y[2];
@@ -461,7 +467,7 @@ __global__ void __launch_bounds__(32 * kRWarps, SEELE_RASTER_MINB) k_raster_quad
                 D[r] = d1;
                 // sign set <=> T32 - D < gamma (rounded so that a clear sign proves T >= gamma); done pixels carry
                 // T = 1e30 (their transmittance is parked in s_T) and never test positive
-                const float2 dg = __fadd2_ru(d1, f2(gm));
+                const float2 dg = __fadd2_ru(d1, f2(cfg.gamma_up));  // (>= gamma: a clear sign proves T >= gamma)
                 y[r] = __fadd2_rn(t1, make_float2(-dg.x, -dg.y));
                 cnt[r] = __fadd2_rn(cnt[r], m[r]);
             }
@@ -473,7 +479,7 @@ __global__ void __launch_bounds__(32 * kRWarps, SEELE_RASTER_MINB) k_raster_quad
 #pragma unroll
                 for (int s = 0; s < 4; s++) {
                     if ((int)fbits(slot(y, s)) >= 0) continue;
-                    if (__fadd_ru(slot(T, s), slot(D, s)) < gm) {  // surely below: done
+                    if (__fadd_ru(slot(T, s), slot(D, s)) < cfg.gamma_dn) {  // surely below gamma: done
                         slot(Lf, s) = 0.0f;
                         s_T[lid][s] = slot(T, s);
                         slot(T, s) = 1e30f;
