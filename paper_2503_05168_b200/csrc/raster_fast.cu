@@ -299,8 +299,16 @@ __global__ void __launch_bounds__(32 * kRWarps, SEELE_RASTER_MINB) k_raster_quad
         cnt[r] = f2(0.0f);
     }
     // CR group leader pixel (rasterize.py:235-246): top-left pixel of the w x w group
-    const int lead_x = W == 4 ? ox + 4 * (bx >> 1) : x0, lead_y = W == 4 ? oy + 4 * (by >> 1) : y0;
-    uint32_t c_alpha = 0, c_blend = 0, n_redecide = 0, n_tamb = 0, n_skip = 0;
+    // (the rare paths and the epilogue take the quad origin back from the pixel centres, so the loop keeps the
+    // centres, not the integer origin, in registers)
+    auto qx0 = [&]() { return (int)lxp.x; };
+    auto qy0 = [&]() { return (int)lyp.x; };
+    const int lead_xo = W == 4 ? 4 * (bx >> 1) - 2 * bx : 0, lead_yo = W == 4 ? 4 * (by >> 1) - 2 * by : 0;
+    uint32_t c_alpha = 0, c_blend = 0, n_skip = 0;
+    // rare-path counters (alpha re-decisions, exact transmittance walks) in shared memory, off the registers
+    __shared__ uint32_t s_rare[32 * kRWarps][2];
+    s_rare[lid][0] = 0u;
+    s_rare[lid][1] = 0u;
 #ifdef SEELE_RASTER_PROFILE
     uint32_t pr_rel = 0, pr_nolead = 0, pr_noblend = 0, pr_amb = 0, pr_death = 0;
 #endif
@@ -426,7 +434,7 @@ __global__ void __launch_bounds__(32 * kRWarps, SEELE_RASTER_MINB) k_raster_quad
                 }
                 if (__any_sync(0xffffffffu, need != 0u)) {
                     if (need) {
-                        const Redecided rd = redecide(ws, sg.p, x0, y0, need, th64);
+                        const Redecided rd = redecide(ws, sg.p, qx0(), qy0(), need, th64);
 #pragma unroll
                         for (int s = 0; s < 4; s++) {
                             if (!((need >> s) & 1u)) continue;
@@ -434,7 +442,7 @@ __global__ void __launch_bounds__(32 * kRWarps, SEELE_RASTER_MINB) k_raster_quad
                             sgn[s] = rd.pass[s] ? ~0u : 0u;
                             slot(E, s) = 6.2e-8f;  // rounding of a64 to float
                         }
-                        n_redecide += __popc(need);
+                        s_rare[lid][0] += __popc(need);
                     }
                     verdicts();
                 }
@@ -506,12 +514,13 @@ __global__ void __launch_bounds__(32 * kRWarps, SEELE_RASTER_MINB) k_raster_quad
                     const int src = __ffs(ambw) - 1;
                     const uint32_t am = __shfl_sync(0xffffffffu, ambT, src);
                     const int s = __ffs(am) - 1;
-                    const int px = __shfl_sync(0xffffffffu, x0, src) + (s & 1);
-                    const int py = __shfl_sync(0xffffffffu, y0, src) + (s >> 1);
-                    const int gx = __shfl_sync(0xffffffffu, lead_x, src), gy = __shfl_sync(0xffffffffu, lead_y, src);
+                    const int sx0 = __shfl_sync(0xffffffffu, qx0(), src), sy0 = __shfl_sync(0xffffffffu, qy0(), src);
+                    const int px = sx0 + (s & 1), py = sy0 + (s >> 1);
+                    const int gx = sx0 + __shfl_sync(0xffffffffu, lead_xo, src);
+                    const int gy = sy0 + __shfl_sync(0xffffffffu, lead_yo, src);
                     const double Tx = exact_transmittance<W>(ws, pair_pos, rg.x, b0 + (uint32_t)j, px, py, gx, gy, th64);
                     if (lane == src) {
-                        n_tamb++;
+                        s_rare[lid][1]++;
 #pragma unroll
                         for (int ss = 0; ss < 4; ss++) {
                             if (ss != s) continue;
@@ -550,8 +559,8 @@ __global__ void __launch_bounds__(32 * kRWarps, SEELE_RASTER_MINB) k_raster_quad
     for (int o = 1; o < 8; o <<= 1) mw_steps = max(mw_steps, __shfl_xor_sync(0xffffffffu, mw_steps, o));
     uint32_t c_leader = 0;
     if (W == 0) c_alpha = mw_steps; else c_leader = mw_steps;
-    const uint32_t w_red = __reduce_add_sync(0xffffffffu, n_redecide);
-    const uint32_t w_tamb = __reduce_add_sync(0xffffffffu, n_tamb);
+    const uint32_t w_red = __reduce_add_sync(0xffffffffu, s_rare[lid][0]);
+    const uint32_t w_tamb = __reduce_add_sync(0xffffffffu, s_rare[lid][1]);
     const uint32_t w_live = __reduce_add_sync(0xffffffffu, n_live);
     const uint32_t w_blend = __reduce_add_sync(0xffffffffu, n_blend);
     const uint32_t w_skip = __reduce_add_sync(0xffffffffu, n_skip);
@@ -579,8 +588,9 @@ __global__ void __launch_bounds__(32 * kRWarps, SEELE_RASTER_MINB) k_raster_quad
     }
 #pragma unroll
     for (int s = 0; s < 4; s++) {
-        if (x0 + (s & 1) >= cam.width || y0 + (s >> 1) >= cam.height) continue;
-        const long long pix = (long long)(y0 + (s >> 1)) * cam.width + x0 + (s & 1);
+        const int ex0 = qx0(), ey0 = qy0();
+        if (ex0 + (s & 1) >= cam.width || ey0 + (s >> 1) >= cam.height) continue;
+        const long long pix = (long long)(ey0 + (s >> 1)) * cam.width + ex0 + (s & 1);
         const int r = s >> 1, c = s & 1;
         const float Ts = slot(Lf, s) != 0.0f ? slot(T, s) : s_T[lid][s];
         image[3 * pix + 0] = fmaf(Ts, (float)cfg.bg[0], lane_of(C[r][0], c));  // background (rasterize.py:228-231)
