@@ -290,11 +290,11 @@ __global__ void __launch_bounds__(32 * kRWarps, SEELE_RASTER_MINB) k_raster_quad
     const unsigned gmask = 0x33u << ((lane & ~7) + g_off);
     const bool leader_thread = W != 4 || (i == g_off);
     const double th64 = cfg.alpha_theta;
-    float2 T[2], D[2], C[2][3], cnt[2];
+    float2 T[2], L[2], C[2][3], cnt[2];  // L = T32 - D: a lower bound of the exact transmittance
 #pragma unroll
     for (int r = 0; r < 2; r++) {
         T[r] = f2(1.0f);
-        D[r] = f2(0.0f);
+        L[r] = f2(1.0f);
         C[r][0] = C[r][1] = C[r][2] = f2(0.0f);
         cnt[r] = f2(0.0f);
     }
@@ -470,13 +470,16 @@ __global__ void __launch_bounds__(32 * kRWarps, SEELE_RASTER_MINB) k_raster_quad
                 // the exact T (1 - alpha32) after the rounding of T alpha, together <= 2^-24 T: the 1e-7 T term
                 const float2 efm = __fmul2_rn(__ffma2_rn(al[r], E[r], f2(1.0e-7f)), m[r]);
                 const float2 t1 = __fadd2_rn(t0, make_float2(-wgt.x, -wgt.y));
-                const float2 d1 = __ffma2_ru(D[r], omm, __fmul2_ru(t0, efm));
+                // the bound kept as L = T32 - D: L' = L omm - T efm rounded down is T32' - D' for the D
+                // recurrence D' = D omm + T efm rounded up, so T32' - (T32' - L') bounds T from below and
+                // T32' + (T32' - L') from above
+                const float2 te = __fmul2_ru(t0, efm);
+                const float2 l1 = __ffma2_rd(L[r], omm, make_float2(-te.x, -te.y));
                 T[r] = t1;
-                D[r] = d1;
-                // sign set <=> T32 - D < gamma (rounded so that a clear sign proves T >= gamma); done pixels carry
-                // T = 1e30 (their transmittance is parked in s_T) and never test positive
-                const float2 dg = __fadd2_ru(d1, f2(cfg.gamma_up));  // (>= gamma: a clear sign proves T >= gamma)
-                y[r] = __fadd2_rn(t1, make_float2(-dg.x, -dg.y));
+                L[r] = l1;
+                // sign set <=> L < gamma_up (a clear sign proves T >= gamma); done pixels carry T = L = 1e30
+                // (their transmittance is parked in s_T) and never test positive
+                y[r] = __fadd2_rn(l1, f2(-cfg.gamma_up));
                 cnt[r] = __fadd2_rn(cnt[r], m[r]);
             }
             if (__any_sync(0xffffffffu, (int)(fbits(y[0].x) | fbits(y[0].y) | fbits(y[1].x) | fbits(y[1].y)) < 0)) {
@@ -487,10 +490,11 @@ __global__ void __launch_bounds__(32 * kRWarps, SEELE_RASTER_MINB) k_raster_quad
 #pragma unroll
                 for (int s = 0; s < 4; s++) {
                     if ((int)fbits(slot(y, s)) >= 0) continue;
-                    if (__fadd_ru(slot(T, s), slot(D, s)) < cfg.gamma_dn) {  // surely below gamma: done
+                    if (__fmaf_ru(slot(T, s), 2.0f, -slot(L, s)) < cfg.gamma_dn) {  // T32 + D < gamma: done
                         slot(Lf, s) = 0.0f;
                         s_T[lid][s] = slot(T, s);
                         slot(T, s) = 1e30f;
+                        slot(L, s) = 1e30f;
                         di[s] = b0 + (uint32_t)j - rg.x + 1u;  // its death step: tile splats processed
                         nlive--;
                         n_skip -= (uint32_t)__popc(skipped >> j >> 1);
@@ -498,7 +502,7 @@ __global__ void __launch_bounds__(32 * kRWarps, SEELE_RASTER_MINB) k_raster_quad
                         ambT |= 1u << s;
 #ifdef SEELE_AMB_PROFILE
                         {  // (debug build: histogram of the relative bound D / T at T-ambiguous events)
-                            const float rel = slot(D, s) / fmaxf(slot(T, s), 1e-30f);
+                            const float rel = (slot(T, s) - slot(L, s)) / fmaxf(slot(T, s), 1e-30f);
                             const int bk = rel < 1e-5f ? 0 : rel < 1e-4f ? 1 : rel < 1e-3f ? 2 : rel < 1e-2f ? 3 : 4;
                             atomicAdd((unsigned long long *)stats + 11 + bk, 1ull);
                         }
@@ -525,11 +529,12 @@ __global__ void __launch_bounds__(32 * kRWarps, SEELE_RASTER_MINB) k_raster_quad
                         for (int ss = 0; ss < 4; ss++) {
                             if (ss != s) continue;
                             slot(T, ss) = (float)Tx;
-                            slot(D, ss) = 6.0e-8f * (float)Tx;
+                            slot(L, ss) = __fmul_rd(slot(T, ss), 0.99999994f);  // D = 2^-24 T: the rounding of Tx
                             if (Tx < cfg.gamma) {
                                 slot(Lf, ss) = 0.0f;
                                 s_T[lid][ss] = slot(T, ss);
                                 slot(T, ss) = 1e30f;
+                                slot(L, ss) = 1e30f;
                                 di[ss] = b0 + (uint32_t)j - rg.x + 1u;
                                 nlive--;
                                 n_skip -= (uint32_t)__popc(skipped >> j >> 1);
