@@ -61,6 +61,8 @@ def parse():
                     help="raster on a high-priority stream, the plan stages of the frames in flight below it")
     ap.add_argument("--plan-first", action="store_true",
                     help="plan stages on a high-priority stream, the raster of the frames in flight below it")
+    ap.add_argument("--partition", type=int, default=0,
+                    help="SMs for the plan stages (green-context partition; rasters on the rest); 0 = shared")
     ap.add_argument("--gather", action="store_true",
                     help="also time the run with an NCCL all-gather of every frame (uint8) + stats inside the timed "
                          "region (value_gather)")
@@ -300,7 +302,8 @@ def run_ours(args):
 
     serial_ms = timed_serial()
     pipe = FramePipeline(rr, args.width, args.height, depth=args.depth, pair_capacity=cap,
-                         split=args.raster_first or args.plan_first, raster_priority=args.raster_first)
+                         split=args.raster_first or args.plan_first, raster_priority=args.raster_first,
+                         partition=args.partition or None)
     clocks = ClockSampler(device) if rank == 0 else None
     if clocks:
         clocks.start()

@@ -158,6 +158,19 @@ int seele_render_split(const seele_scene *scene, const int64_t *ranges_dev, int3
                        size_t workspace_bytes, int64_t n_max, int64_t pair_capacity, float *image_dev,
                        int32_t *contrib_dev, int64_t *stats_dev, void *stream, void *raster_stream);
 
+/* SM partition for pipelined trajectories (no reference counterpart: a
+ * B200-side scheduling aid).  Splits the device's SMs into two green
+ * contexts -- plan_sms SMs for the plan stages, the rest for the raster --
+ * and creates n_streams non-blocking streams in each (cudaStream_t handles in
+ * plan_streams[i] / raster_streams[i], valid for the process lifetime).
+ * Passing a plan stream as `stream` and a raster stream as `raster_stream`
+ * to seele_render_split runs one frame's plan beside another frame's raster;
+ * persistent grids are sized by the partition's SM count.  The granted SM
+ * counts (rounded to the hardware's granularity, 8 on sm_100) are returned.
+ * SEELE_ERR_CUDA when the driver has no green contexts. */
+int seele_partition_create(int32_t plan_sms, int32_t n_streams, void **plan_streams, void **raster_streams,
+                           int32_t *plan_sms_out, int32_t *raster_sms_out);
+
 /* Image metrics on the device (metrics.py:44-112) of two (H, W, 3) fp64
  * images a_dev, b_dev: PSNR in dB (+inf when equal) and mean SSIM over the
  * BT.601 luminance (11x11 Gaussian window, sigma 1.5, valid positions).  The

@@ -47,6 +47,7 @@ EXPORTED_SYMBOLS = (
     "seele_workspace_bytes",
     "seele_render",
     "seele_render_split",
+    "seele_partition_create",
     "seele_select_clusters",
     "seele_plan_export",
     "seele_skip_bound",
@@ -129,6 +130,8 @@ def load(required: bool = True):
     lib.seele_render.argtypes = [P, P, I32, P, P, P, ctypes.c_size_t, I64, I64, P, P, P, P]
     lib.seele_render.restype = ctypes.c_int
     lib.seele_render_split.argtypes = [P, P, I32, P, P, P, ctypes.c_size_t, I64, I64, P, P, P, P, P]
+    lib.seele_partition_create.restype = I32
+    lib.seele_partition_create.argtypes = [I32, I32, P, P, P, P]
     lib.seele_render_split.restype = ctypes.c_int
     lib.seele_select_clusters.argtypes = [P, P, I32, I32, ctypes.c_double, P, ctypes.c_double, P, P, P, P]
     lib.seele_select_clusters.restype = ctypes.c_int

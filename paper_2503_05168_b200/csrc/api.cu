@@ -285,7 +285,7 @@ int seele_render_split(const seele_scene *scene, const int64_t *ranges_dev, int3
     sk.plane_stride = scene->plane_stride;
 
     cudaError_t e;
-    const int sms = sm_count();
+    const int sms = stream_sms(st);  // (the plan partition's SMs on a partition stream)
     long long pre_blocks = (n_max + 255) / 256;
 #ifndef SEELE_PRE_GRID_PER_SM
 #define SEELE_PRE_GRID_PER_SM 3  // persistent: the resident CTAs of k_preprocess (launch bounds 256, 3)
@@ -451,6 +451,20 @@ int seele_skip_bound(void *workspace, int64_t n_max, int64_t pair_capacity, cons
     launch_skip_bound(cfg->group_w, ws, ws.pfinal, ck, cf, bound_dev, static_cast<cudaStream_t>(stream));
     cudaError_t e;
     if ((e = cudaGetLastError()) != cudaSuccess) return cuda_fail(e, "seele_skip_bound");
+    return SEELE_OK;
+}
+
+int seele_partition_create(int32_t plan_sms, int32_t n_streams, void **plan_streams, void **raster_streams,
+                           int32_t *plan_sms_out, int32_t *raster_sms_out) {
+    g_err[0] = 0;
+    if (plan_sms < 1 || n_streams < 1 || n_streams > 64 || !plan_streams || !raster_streams || !plan_sms_out ||
+        !raster_sms_out)
+        return fail(SEELE_ERR_INVALID_ARGUMENT, "partition: bad arguments");
+    int po = 0, ro = 0;
+    const int rc = partition_create(plan_sms, n_streams, plan_streams, raster_streams, &po, &ro);
+    if (rc != 0) return fail(SEELE_ERR_CUDA, "partition: green contexts unavailable or split refused (%d)", rc);
+    *plan_sms_out = po;
+    *raster_sms_out = ro;
     return SEELE_OK;
 }
 

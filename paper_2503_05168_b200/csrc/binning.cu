@@ -725,17 +725,6 @@ __global__ void k_fill_pair_tiles(const uint2 *ranges, int n_tiles, int32_t *pai
     }
 }
 
-int sm_count_bin() {
-    static int sms = 0;
-    if (!sms) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        if (sms <= 0) sms = 148;
-    }
-    return sms;
-}
-
 long long ceil_div(long long a, long long b) { return (a + b - 1) / b; }
 
 template <typename K>
@@ -770,7 +759,7 @@ void launch_binning(const Workspace &ws, long long n_max, long long cap, const C
                     cudaStream_t st) {
     (void)stats;
     const BinGeom g = bin_geometry(n_max, cam.width, cam.height);
-    const int sms = sm_count_bin();
+    const int sms = stream_sms(st);
     const size_t n_sd = (size_t)(g.stx + 1) * (g.sty + 1);
     const size_t diff_bytes = sizeof(int32_t) * (g.tiles_x + 1) * (g.tiles_y + 1);
     const size_t sd_bytes = sizeof(int32_t) * n_sd;

@@ -83,6 +83,11 @@ struct BinGeom {
     int count_group;  // chunks per k_bin_count CTA
 };
 BinGeom bin_geometry(long long n_max, int width, int height);
+// SMs of the device, and of the SM partition a stream belongs to (partition.cu; the device's when the
+// stream is not a partition stream): persistent grids are sized by the latter
+int stream_sms(cudaStream_t st);
+int partition_create(int plan_sms, int n_streams, void **plan_streams, void **raster_streams, int *plan_out,
+                     int *raster_out);
 
 // Depth order (depth.cu): buckets of the order-preserving fp64 bit pattern of
 // z above the near plane, 2^(52 - kDepthShift) = 65,536 per binade over 16

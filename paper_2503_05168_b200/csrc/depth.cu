@@ -307,21 +307,10 @@ __global__ void __launch_bounds__(kSortThreads) k_bucket_sort(Workspace ws, CamK
     }
 }
 
-int sm_count_depth() {
-    static int sms = 0;
-    if (!sms) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        if (sms <= 0) sms = 148;
-    }
-    return sms;
-}
-
 }  // namespace
 
 void launch_depth_sort(const Workspace &ws, const CamK &cam, long long n_max, int64_t *stats, cudaStream_t st) {
-    const int sms = sm_count_depth();
+    const int sms = stream_sms(st);
     k_bucket_scan<<<kDepthBuckets / kDepthScanItems, kScanThreads, 0, st>>>(ws, stats);
 #ifndef SEELE_SCATTER_PER_SM
 #define SEELE_SCATTER_PER_SM 4

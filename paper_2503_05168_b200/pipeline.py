@@ -12,6 +12,7 @@ buffers; a slot's outputs stay valid until the slot is used again
 """
 from __future__ import annotations
 
+import ctypes
 from dataclasses import dataclass
 
 import torch
@@ -20,6 +21,30 @@ from . import _native
 from .model import CameraPose
 from .render import EngineConfig, FrameOutput, FrameRenderer
 from .residency import ResidentRenderer, _select_on_device
+
+
+_PARTITIONS: dict = {}
+
+
+def partition_streams(device: torch.device, plan_sms: int, n: int):
+    """``n`` plan streams on a partition of ``plan_sms`` SMs and ``n`` raster
+    streams on the device's other SMs (seele_partition_create: green
+    contexts, which live for the process; one partition per (device,
+    plan_sms), its streams shared by every pipeline that asks).  Returns
+    (plan streams, raster streams, plan SMs, raster SMs)."""
+    key = (torch.device(device).index or 0, int(plan_sms))
+    part = _PARTITIONS.get(key)
+    if part is None or len(part[0]) < n:
+        lib = _native.load()
+        k = max(int(n), 4)
+        ps, rs = (ctypes.c_void_p * k)(), (ctypes.c_void_p * k)()
+        po, ro = ctypes.c_int32(), ctypes.c_int32()
+        with torch.cuda.device(device):
+            _native.check(lib.seele_partition_create(int(plan_sms), k, ps, rs, ctypes.byref(po), ctypes.byref(ro)))
+        part = ([torch.cuda.ExternalStream(ps[i], device=device) for i in range(k)],
+                [torch.cuda.ExternalStream(rs[i], device=device) for i in range(k)], po.value, ro.value)
+        _PARTITIONS[key] = part
+    return part[0][:n], part[1][:n], part[2], part[3]
 
 
 @dataclass
@@ -43,22 +68,30 @@ class FramePipeline:
 
     def __init__(self, rr: ResidentRenderer, width: int, height: int, *, depth: int = 2,
                  pair_capacity: int | None = None, contrib: bool = True, split: bool = False,
-                 raster_priority: bool = False, out_buffers: int = 1):
+                 raster_priority: bool = False, out_buffers: int = 1, partition: int | None = None):
         if depth < 1:
             raise ValueError("depth must be >= 1")
         self.rr = rr
         self.device = rr.device
         self.size = (int(width), int(height))
         self.slots: list[_Slot] = []
-        for _ in range(depth):
+        # partition = N: plan stages on N SMs, rasters on the rest (green contexts), so one frame's plan
+        # runs beside another frame's raster instead of waiting for its CTAs to drain
+        self.partition = None
+        if partition:
+            split = True
+            pstreams, rstreams, psms, rsms = partition_streams(self.device, partition, depth)
+            self.partition = (psms, rsms)
+        for k in range(depth):
             r = FrameRenderer(self.device)
             r.reserve(rr.n_max, width, height, pair_capacity=pair_capacity)
             least, greatest = torch.cuda.Stream.priority_range()  # lower number = higher priority
             plan_pri, raster_pri = (least, greatest) if raster_priority else (greatest, least)
             self.slots.append(_Slot(
                 renderer=r,
-                stream=torch.cuda.Stream(self.device, priority=plan_pri if split else 0),
-                raster_stream=torch.cuda.Stream(self.device, priority=raster_pri if split else 0),
+                stream=pstreams[k] if partition else torch.cuda.Stream(self.device, priority=plan_pri if split else 0),
+                raster_stream=rstreams[k] if partition else torch.cuda.Stream(self.device,
+                                                                              priority=raster_pri if split else 0),
                 free=torch.cuda.Event(),
                 sel_ids=torch.empty(rr.m + 1, dtype=torch.int32, device=self.device),
                 ranges=torch.empty((rr.m + 2, 2), dtype=torch.int64, device=self.device),

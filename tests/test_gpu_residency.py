@@ -105,3 +105,30 @@ def test_trajectory_pipeline_matches_serial(synthetic_container, depth):
         assert [int(st[k]) for k in range(len(STAT_KEYS))] == w_st
         got += 1
     assert got == len(frames)
+
+
+def test_partitioned_pipeline_matches_serial(synthetic_container):
+    """FramePipeline on an SM partition (plan stages and rasters on disjoint
+    green-context SM sets, seele_partition_create) gives exactly the per-frame
+    results of the serial path."""
+    import torch
+
+    from paper_2503_05168_b200.pipeline import FramePipeline
+
+    d, poses = synthetic_container
+    rr = ResidentRenderer(str(d))
+    cfg = EngineConfig(engine="cr", group_w=2)
+    frames = [5, 29, 30, 64, 118]
+    w, h = poses[0].width, poses[0].height
+    pipe = FramePipeline(rr, w, h, depth=2, pair_capacity=4_000_000, partition=32)
+    assert pipe.partition is not None and pipe.partition[0] >= 32 and sum(pipe.partition) <= 148 * 2
+    for f in frames:
+        want = rr.render_frame(poses[f], cfg, output="numpy32")
+        k = pipe.slot_of_next()
+        out = pipe.submit(poses[f], cfg)
+        pipe.output_stream(k).synchronize()
+        np.testing.assert_array_equal(out.image.cpu().numpy(), want.image)
+        np.testing.assert_array_equal(out.contrib.cpu().numpy(), want.contrib_count)
+        got = out.stats.cpu().numpy()
+        assert [int(got[i]) for i in range(len(STAT_KEYS))] == [getattr(want.stats, s) for s in STAT_KEYS]
+    torch.cuda.synchronize()
