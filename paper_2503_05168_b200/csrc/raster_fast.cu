@@ -258,7 +258,10 @@ __global__ void __launch_bounds__(32 * kRWarps, SEELE_RASTER_MINB) k_raster_quad
     const int tid = kRWarps == 2 ? lid : (int)((blockIdx.x & 1u) << 5) + lid;  // thread within the tile
     const int lane = tid & 31, warp = tid >> 5;
     const int mw = tid >> 3, i = tid & 7;
-    const unsigned bm = 0xffu << (lane & 24);  // this model-warp's byte of a warp ballot
+    // this model-warp's byte of a warp ballot (through an opaque move: the compiler would otherwise
+    // rematerialise it from %tid inside the step loop, an S2R whose latency lands on every step)
+    unsigned bm;
+    asm volatile("mov.b32 %0, %1;" : "=r"(bm) : "r"(0xffu << (lane & 24)));
     int bx, by;
     if (W == 4) {
         bx = 4 * (mw & 1) + (i & 3);
