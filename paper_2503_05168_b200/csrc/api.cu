@@ -140,8 +140,7 @@ Workspace carve_workspace(void *base, long long n_max, long long cap, int width,
     w.status = c.take<uint8_t>(n);
     w.depth = c.take<double>(n);
     w.rect = c.take<short4>(n);
-    w.mean = c.take<double2>(n);
-    w.conic_op = c.take<double4>(n);
+    w.xrec = c.take<ExactRec>(n);
     w.rec = c.take<RasterRec>(n);
     w.bbox = c.take<float4>(n);
     w.bhist = c.take<uint32_t>(kDepthBuckets + 1);
@@ -188,11 +187,11 @@ __global__ void k_export_splats(Workspace ws, long long n, int8_t *status, doubl
             rect[4 * p + 3] = r.w;
         }
         if (mean) {
-            const double2 m = ok ? ws.mean[p] : make_double2(0, 0);
+            const double2 m = ok ? ws.xrec[p].m : make_double2(0, 0);
             mean[2 * p] = m.x;
             mean[2 * p + 1] = m.y;
         }
-        const double4 co = ok ? ws.conic_op[p] : make_double4(0, 0, 0, 0);
+        const double4 co = ok ? ws.xrec[p].co : make_double4(0, 0, 0, 0);
         if (conic) {
             conic[3 * p] = co.x;
             conic[3 * p + 1] = co.y;

@@ -123,14 +123,23 @@ struct __align__(16) RasterRec {
     uint32_t p;                // assembled position (fp64 re-decisions)
 };
 
+// fp64 record of one binned splat for the exact paths (re-decisions, transmittance walks, the EXACT
+// engine, plan export): everything a walk reads per splat in one 64-byte line (two 32-byte sectors)
+// instead of three lines of three arrays.
+struct __align__(64) ExactRec {
+    double2 m;       // mean (pixel coordinates)
+    double4 co;      // conic (a, b, c), opacity
+    float q_lo, w_up;  // the FAST record's alpha bracket (RasterRec)
+    uint32_t pad[2];
+};
+
 // Workspace carve-up; identical on every call for the same (n_max, cap, w, h).
 struct Workspace {
     // per assembled splat (preprocess)
     uint8_t *status;
     double *depth;
     short4 *rect;
-    double2 *mean;
-    double4 *conic_op;   // (a, b, c, opacity)
+    ExactRec *xrec;      // fp64 mean, conic + opacity, alpha bracket: the exact paths' record, one line
     RasterRec *rec;      // FAST raster records (also the colour of the exact engine)
     float4 *bbox;        // (x_min, x_max, y_min, y_max) of {q' < q_up} in pixel coordinates
     // depth order (depth.cu): bucket counts (K1) -> exclusive offsets, bhist[kDepthBuckets] = binned; each

@@ -221,6 +221,11 @@ __device__ __forceinline__ void write_raster_record(const Workspace &ws, long lo
     const float q_up = nextafterf(rq.y, INFINITY);
     const float w_up = rq.x == -INFINITY ? 0.0f : __double2float_ru(__dsub_ru((double)q_up, (double)rq.x));
     rec[2] = make_float4(rq.x, w_up, rq.z * (1.0f + 1.0f / 1024.0f), rq.w * (1.0f + 1.0f / 1024.0f));
+    // the exact record, whole: two 32-byte stores (full sectors, no partial-sector merging in L2)
+    double *xr = reinterpret_cast<double *>(ws.xrec + p);
+    const double qw = __hiloint2double((int)__float_as_uint(w_up), (int)__float_as_uint(rq.x));  // (q_lo, w_up)
+    asm volatile("st.global.v4.b64 [%0], {%1, %2, %3, %4};" ::"l"(xr), "d"(m0), "d"(m1), "d"(ca), "d"(cb) : "memory");
+    asm volatile("st.global.v4.b64 [%0], {%1, %2, %3, %4};" ::"l"(xr + 4), "d"(cc), "d"(o), "d"(qw), "d"(0.0) : "memory");
     ws.bbox[p] = bb;
 }
 
@@ -396,8 +401,6 @@ __global__ void __launch_bounds__(kPre, SEELE_PRE_MINB) k_preprocess(SceneK sc, 
                         // depth-order bucket (depth.cu) of a binned splat: count it and keep its index in the bucket
                         if (n_tiles > 0)
                             ws.bidx[p] = atomicAdd(&ws.bhist[depth_bucket_of_key(depth_order_key(z), zbase)], 1u);
-                        ws.mean[p] = make_double2(m0, m1);
-                        ws.conic_op[p] = make_double4(ca, cb, cc, g.o);
                         write_raster_record(ws, p, m0, m1, ca, cb, cc, g.o, qth, qth_err);
                         // view direction for SH (preprocess.py:129-130), fp32 like the colour
                         const float rn = rsqrtf((float)(d[0] * d[0] + d[1] * d[1] + d[2] * d[2]));

@@ -51,8 +51,8 @@ __global__ void __launch_bounds__(256) k_raster_exact(Workspace ws, const uint32
         const uint32_t i = b0 + tid;
         if (i < rg.y) {
             const uint32_t p = pair_pos[i];
-            const double2 m = ws.mean[p];
-            const double4 co = ws.conic_op[p];
+            const double2 m = ws.xrec[p].m;
+            const double4 co = ws.xrec[p].co;
             s_mx[tid] = m.x;
             s_my[tid] = m.y;
             s_a[tid] = co.x;
@@ -107,8 +107,8 @@ __global__ void __launch_bounds__(256) k_skip_bound(Workspace ws, const uint32_t
         const uint32_t i = b0 + tid;
         if (i < rg.y) {
             const uint32_t p = pair_pos[i];
-            const double2 m = ws.mean[p];
-            const double4 co = ws.conic_op[p];
+            const double2 m = ws.xrec[p].m;
+            const double4 co = ws.xrec[p].co;
             s_mx[tid] = m.x;
             s_my[tid] = m.y;
             s_a[tid] = co.x;
@@ -177,8 +177,8 @@ __global__ void __launch_bounds__(256) k_harvest(Workspace ws, const uint32_t *_
         const uint32_t i = b0 + tid;
         if (i < rg.y) {
             const uint32_t p = pair_pos[i];
-            const double2 m = ws.mean[p];
-            const double4 co = ws.conic_op[p];
+            const double2 m = ws.xrec[p].m;
+            const double4 co = ws.xrec[p].co;
             s_mx[tid] = m.x;
             s_my[tid] = m.y;
             s_a[tid] = co.x;
@@ -283,8 +283,8 @@ __global__ void __launch_bounds__(256) k_contrib(Workspace ws, const uint32_t *_
         const uint32_t i = b0 + tid;
         if (i < rg.y) {
             const uint32_t p = pair_pos[i];
-            const double2 m = ws.mean[p];
-            const double4 co = ws.conic_op[p];
+            const double2 m = ws.xrec[p].m;
+            const double4 co = ws.xrec[p].co;
             s_mx[tid] = m.x;
             s_my[tid] = m.y;
             s_a[tid] = co.x;

@@ -179,9 +179,9 @@ __device__ __forceinline__ double exact_transmittance(const Workspace &ws, const
         float2 f[kU];
 #pragma unroll
         for (int u = 0; u < kU; u++) {
-            m[u] = ws.mean[p[u]];
-            co[u] = ws.conic_op[p[u]];
-            f[u] = reinterpret_cast<const float2 *>(ws.rec + p[u])[4];  // (q_lo, w_up)
+            m[u] = ws.xrec[p[u]].m;
+            co[u] = ws.xrec[p[u]].co;
+            f[u] = *reinterpret_cast<const float2 *>(&ws.xrec[p[u]].q_lo);  // (q_lo, w_up)
         }
 #pragma unroll
         for (int u = 0; u < kU; u++) {
@@ -193,9 +193,9 @@ __device__ __forceinline__ double exact_transmittance(const Workspace &ws, const
     }
     for (; k <= k1; k += 32) {
         const uint32_t p = pair_pos[k];
-        const double2 m = ws.mean[p];
-        const double4 co = ws.conic_op[p];
-        const float2 f = reinterpret_cast<const float2 *>(ws.rec + p)[4];  // (q_lo, w_up)
+        const double2 m = ws.xrec[p].m;
+        const double4 co = ws.xrec[p].co;
+        const float2 f = *reinterpret_cast<const float2 *>(&ws.xrec[p].q_lo);  // (q_lo, w_up)
         double a;
         if (W >= 2 && !exact_test<false>(lx + 0.5, ly + 0.5, m, co, f.x, f.y, th, a)) continue;
         if (!exact_test<true>(px + 0.5, py + 0.5, m, co, f.x, f.y, th, a)) continue;
@@ -214,8 +214,8 @@ struct Redecided {
 };
 __device__ __noinline__ Redecided redecide(const Workspace &ws, uint32_t p, int x0, int y0, uint32_t need, double th) {
     Redecided r;
-    const double2 m = ws.mean[p];
-    const double4 co = ws.conic_op[p];
+    const double2 m = ws.xrec[p].m;
+    const double4 co = ws.xrec[p].co;
 #pragma unroll
     for (int s = 0; s < 4; s++) {
         r.al[s] = 0.0f;
