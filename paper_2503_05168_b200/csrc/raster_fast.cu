@@ -246,7 +246,9 @@ __global__ void __launch_bounds__(32 * kRWarps, SEELE_RASTER_MINB) k_raster_quad
                                                         CfgK cfg, float *image, int32_t *contrib, int64_t *stats) {
     // per warp, double-buffered: each warp stages and walks the list on its own; batch b + 1 is in flight
     // (cp.async) while batch b is rasterized
-    __shared__ Staged s_stage[kRWarps][2][kBatch];
+    // records staged field-chunk major ([chunk][lane], 16 B each): a warp's cp.async writes and the cull's
+    // per-lane reads are conflict-free (a 64-byte lane stride put 16 lanes on one bank group)
+    __shared__ float4 s_stage[kRWarps][2][4][kBatch];
     __shared__ float4 s_box[kRWarps][2][kBatch];
     // per pixel: tile splats it was live for (written at its death)
     __shared__ uint32_t s_di[32 * kRWarps][4];
@@ -322,9 +324,8 @@ __global__ void __launch_bounds__(32 * kRWarps, SEELE_RASTER_MINB) k_raster_quad
     auto stage = [&](uint32_t idx, uint32_t p, int buf) {
         if (idx < rg.y) {
             const float4 *src = reinterpret_cast<const float4 *>(ws.rec + p);
-            float4 *dst = reinterpret_cast<float4 *>(&s_stage[wslot][buf][lane]);
 #pragma unroll
-            for (int k = 0; k < 4; k++) cp_async16(dst + k, src + k);
+            for (int k = 0; k < 4; k++) cp_async16(&s_stage[wslot][buf][k][lane], src + k);
             cp_async16(&s_box[wslot][buf][lane], ws.bbox + p);
         }
         cp_async_commit();
@@ -340,10 +341,18 @@ __global__ void __launch_bounds__(32 * kRWarps, SEELE_RASTER_MINB) k_raster_quad
         p_next = i2 < rg.y ? pair_pos[i2] : 0u;
         cp_async_wait<1>();  // this lane's part of batch b has landed
         __syncwarp();
-        const Staged *s_g = s_stage[wslot][buf];
+        const float4(*s_g)[kBatch] = s_stage[wslot][buf];
+        // record of staged splat i (chunks read as 16-byte vectors)
+        auto staged = [&](int i) {
+            Staged r;
+            float4 *d = reinterpret_cast<float4 *>(&r);
+#pragma unroll
+            for (int k = 0; k < 4; k++) d[k] = s_g[k][i];
+            return r;
+        };
         bool rel = false;
         if (b0 + lane < rg.y) {
-            const Staged &sv = s_g[lane];
+            const Staged sv = staged(lane);
             const float4 bb = s_box[wslot][buf][lane];
             rel = bb.y >= ox + 0.5f && bb.x <= ox + 15.5f && bb.w >= oy + ry0 && bb.z <= oy + ry1;
             if (rel) {
@@ -371,7 +380,7 @@ __global__ void __launch_bounds__(32 * kRWarps, SEELE_RASTER_MINB) k_raster_quad
         while (mlo) {
             const int j = __ffs(mlo) - 1;  // next relevant splat
             mlo &= mlo - 1u;
-            const Staged &sg = s_g[j];
+            const Staged sg = staged(j);
 #ifdef SEELE_RASTER_PROFILE
             pr_rel++;
 #endif
