@@ -77,6 +77,24 @@ def test_random_scenes_vs_oracle(seed, layout):
         _check_frame(res, want["contrib"], [want["stats"][k] for k in STAT_KEYS], want["image"])
 
 
+@pytest.mark.parametrize("layout", ["f64", "planes"])
+def test_high_opacity_clamp_vs_oracle(layout):
+    """Opacities up to 1: alpha = min(o exp(-q/2), 0.99) clamps near the centres
+    (rasterize.py:146-151), the FAST raster's rare path for o > 0.99."""
+    rng = np.random.default_rng(77)
+    cam = make_camera(160, 96)
+    scene = random_scene(rng, 2500, sh_degree=3, camera=cam, scale_range=(0.01, 0.2), opacity_range=(0.97, 1.0))
+    assert (scene.opacities > 0.99).sum() > 500
+    dscene = DeviceScene.from_arrays(scene, layout=layout)
+    host = dscene.host_arrays()
+    for eng in ("ref", "cr2", "cr4"):
+        kw = {"engine": "ref"} if eng == "ref" else {"engine": "cr", "group_w": int(eng[2])}
+        cfg = EngineConfig(background=(0.1, 0.2, 0.3), **kw)
+        want = O.render(host, cam, cfg)
+        res = render_frame(dscene, cam, cfg)
+        _check_frame(res, want["contrib"], [want["stats"][k] for k in STAT_KEYS], want["image"])
+
+
 def test_fast_equals_exact_discrete():
     cam = make_camera(256, 256)
     scene = random_scene(np.random.default_rng(9), 20000, sh_degree=3, camera=cam, opacity_range=(0.3, 0.99))
