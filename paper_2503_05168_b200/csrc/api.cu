@@ -138,13 +138,11 @@ Workspace carve_workspace(void *base, long long n_max, long long cap, int width,
     w.epoch = c.take<uint32_t>(1);
     w.look = c.take<unsigned long long>(kDepthBuckets / kDepthScanItems);
     w.status = c.take<uint8_t>(n);
-    w.depth = c.take<double>(n);
-    w.rect = c.take<short4>(n);
+    w.srec = c.take<uint4>(n);
     w.xrec = c.take<ExactRec>(n);
     w.rec = c.take<RasterRec>(n);
     w.bbox = c.take<float4>(n);
     w.bhist = c.take<uint32_t>(kDepthBuckets + 1);
-    w.bidx = c.take<uint32_t>(n);
     w.brec[0] = c.take<uint4>(n);
     w.brec[1] = c.take<uint4>(n);
     w.gfirst = c.take<uint32_t>(n / kDepthGroup + 2);
@@ -178,13 +176,13 @@ __global__ void k_export_splats(Workspace ws, long long n, int8_t *status, doubl
     for (long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x; p < n; p += (long long)gridDim.x * blockDim.x) {
         if (status) status[p] = (int8_t)ws.status[p];
         const bool ok = ws.status[p] == 0;
-        if (depth) depth[p] = ok ? ws.depth[p] : 0.0;
+        const uint4 sr = ws.srec[p];
+        if (depth) depth[p] = ok ? __hiloint2double((int)sr.w, (int)sr.z) : 0.0;
         if (rect) {
-            const short4 r = ws.rect[p];
-            rect[4 * p] = r.x;
-            rect[4 * p + 1] = r.y;
-            rect[4 * p + 2] = r.z;
-            rect[4 * p + 3] = r.w;
+            rect[4 * p] = (int32_t)(sr.x & 0xffu);
+            rect[4 * p + 1] = (int32_t)((sr.x >> 8) & 0xffu);
+            rect[4 * p + 2] = (int32_t)((sr.x >> 16) & 0xffu);
+            rect[4 * p + 3] = (int32_t)(sr.x >> 24);
         }
         if (mean) {
             const double2 m = ok ? ws.xrec[p].m : make_double2(0, 0);

@@ -109,6 +109,11 @@ __device__ __forceinline__ uint32_t depth_bucket_of_key(unsigned long long key, 
     return q < (unsigned long long)(kDepthBuckets - 1) ? (uint32_t)q : (uint32_t)(kDepthBuckets - 1);
 }
 
+__device__ __forceinline__ uint32_t pack_rect(short4 r) {
+    return (uint32_t)(r.x & 0xff) | ((uint32_t)(r.y & 0xff) << 8) | ((uint32_t)(r.z & 0xff) << 16) |
+           ((uint32_t)(r.w & 0xff) << 24);
+}
+
 // FAST raster record of one splat (raster_fast.cu), written by preprocess.
 // q' = q log2(e) / 2, so alpha = o 2^-q'; one 64-byte line, staged into
 // shared memory by four 16-byte cp.async per splat.
@@ -137,8 +142,9 @@ struct __align__(64) ExactRec {
 struct Workspace {
     // per assembled splat (preprocess)
     uint8_t *status;
-    double *depth;
-    short4 *rect;
+    // per assembled splat: tile rect packed in bytes (x0 | x1 << 8 | y0 << 16 | y1 << 24; x0 > x1: not binned),
+    // its index in its depth bucket, the fp64 view depth (bits): one 16-byte record, what the depth scatter reads
+    uint4 *srec;
     ExactRec *xrec;      // fp64 mean, conic + opacity, alpha bracket: the exact paths' record, one line
     RasterRec *rec;      // FAST raster records (also the colour of the exact engine)
     float4 *bbox;        // (x_min, x_max, y_min, y_max) of {q' < q_up} in pixel coordinates
@@ -147,7 +153,6 @@ struct Workspace {
     // packed tile rect x0 | x1 << 8 | y0 << 16 | y1 << 24) in brec[0] (brec[1]: merge buffer of large groups);
     // first bucket of each sort group; the sorted order in dval[0] / drect[0] (dval[1] / drect[1]: unused)
     uint32_t *bhist;     // [kDepthBuckets + 1]
-    uint32_t *bidx;      // [n_max]
     uint4 *brec[2];      // [n_max]
     uint32_t *gfirst;    // [n_max / kDepthGroup + 2]
     uint32_t *dval[2];

@@ -44,10 +44,6 @@ static_assert(kPerThread % 4 == 0 && kDepthBuckets % kDepthScanItems == 0, "scan
 constexpr int kSortThreads = 256;
 constexpr int kRankMaxBucket = 128;  // buckets up to this size are ranked by counting
 
-__device__ __forceinline__ uint32_t pack_rect(short4 r) {
-    return (uint32_t)(r.x & 0xff) | ((uint32_t)(r.y & 0xff) << 8) | ((uint32_t)(r.z & 0xff) << 16) |
-           ((uint32_t)(r.w & 0xff) << 24);
-}
 
 // (depth, position) strictly before
 __device__ __forceinline__ bool before(unsigned long long ka, uint32_t pa, unsigned long long kb, uint32_t pb) {
@@ -130,12 +126,11 @@ __global__ void __launch_bounds__(kScanThreads) k_bucket_scan(Workspace ws, cons
 __global__ void __launch_bounds__(SEELE_SCATTER_THREADS) k_bucket_scatter(Workspace ws, CamK cam) {
     const uint32_t p = blockIdx.x * blockDim.x + threadIdx.x;
     if (p >= ws.counters[CNT_WS]) return;
-    const short4 r = ws.rect[p];
-    if (r.x > r.y) return;  // not binned
-    const unsigned long long key = depth_order_key(ws.depth[p]);
-    const uint32_t idx = ws.bidx[p];
-    const uint32_t slot = ws.bhist[depth_bucket_of_key(key, depth_order_key(cam.near_clip))] + idx;
-    ws.brec[0][slot] = make_uint4((uint32_t)key, (uint32_t)(key >> 32), p, pack_rect(r));
+    const uint4 sr = ws.srec[p];  // (packed rect, bucket index, depth): one load, then the bucket offset
+    if ((sr.x & 0xffu) > ((sr.x >> 8) & 0xffu)) return;  // not binned
+    const unsigned long long key = depth_order_key(__hiloint2double((int)sr.w, (int)sr.z));
+    const uint32_t slot = ws.bhist[depth_bucket_of_key(key, depth_order_key(cam.near_clip))] + sr.y;
+    ws.brec[0][slot] = make_uint4((uint32_t)key, (uint32_t)(key >> 32), p, sr.x);
 }
 
 union SortSmem {

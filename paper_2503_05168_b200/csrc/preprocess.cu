@@ -294,6 +294,8 @@ __global__ void __launch_bounds__(kPre, SEELE_PRE_MINB) k_preprocess(SceneK sc, 
     for (long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x; p < n_ws; p += stride) {
         int status = 3;
         uint32_t n_tiles = 0;
+        uint32_t bi = 0u;  // index in the depth bucket (binned splats)
+        double sz = 0.0;   // view depth (binned, or every projected splat with keep_unbinned)
         {
             int r = 0;
             while (r + 1 < n_ranges && s_prefix[r + 1] <= p) r++;
@@ -397,10 +399,9 @@ __global__ void __launch_bounds__(kPre, SEELE_PRE_MINB) k_preprocess(SceneK sc, 
                             }
                             cp_async_commit();
                         }
-                        ws.depth[p] = z;
+                        sz = z;
                         // depth-order bucket (depth.cu) of a binned splat: count it and keep its index in the bucket
-                        if (n_tiles > 0)
-                            ws.bidx[p] = atomicAdd(&ws.bhist[depth_bucket_of_key(depth_order_key(z), zbase)], 1u);
+                        if (n_tiles > 0) bi = atomicAdd(&ws.bhist[depth_bucket_of_key(depth_order_key(z), zbase)], 1u);
                         write_raster_record(ws, p, m0, m1, ca, cb, cc, g.o, qth, qth_err);
                         // view direction for SH (preprocess.py:129-130), fp32 like the colour
                         const float rn = rsqrtf((float)(d[0] * d[0] + d[1] * d[1] + d[2] * d[2]));
@@ -435,7 +436,7 @@ __global__ void __launch_bounds__(kPre, SEELE_PRE_MINB) k_preprocess(SceneK sc, 
                 }
             }
             ws.status[p] = (uint8_t)status;
-            ws.rect[p] = rect;
+            ws.srec[p] = make_uint4(pack_rect(rect), bi, (uint32_t)__double2loint(sz), (uint32_t)__double2hiint(sz));
         }
         cnt[0] += status == 1;
         cnt[1] += status == 2;
