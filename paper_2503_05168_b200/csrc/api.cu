@@ -141,7 +141,6 @@ Workspace carve_workspace(void *base, long long n_max, long long cap, int width,
     w.srec = c.take<uint4>(n);
     w.xrec = c.take<ExactRec>(n);
     w.rec = c.take<RasterRec>(n);
-    w.bbox = c.take<float4>(n);
     w.bhist = c.take<uint32_t>(kDepthBuckets + 1);
     w.brec[0] = c.take<uint4>(n);
     w.brec[1] = c.take<uint4>(n);

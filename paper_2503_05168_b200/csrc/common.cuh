@@ -147,7 +147,6 @@ struct Workspace {
     uint4 *srec;
     ExactRec *xrec;      // fp64 mean, conic + opacity, alpha bracket: the exact paths' record, one line
     RasterRec *rec;      // FAST raster records (also the colour of the exact engine)
-    float4 *bbox;        // (x_min, x_max, y_min, y_max) of {q' < q_up} in pixel coordinates
     // depth order (depth.cu): bucket counts (K1) -> exclusive offsets, bhist[kDepthBuckets] = binned; each
     // binned splat's index inside its bucket (K1's atomic); bucket-order records (order key lo / hi, position,
     // packed tile rect x0 | x1 << 8 | y0 << 16 | y1 << 24) in brec[0] (brec[1]: merge buffer of large groups);

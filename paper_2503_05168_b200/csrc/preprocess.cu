@@ -159,14 +159,13 @@ __device__ __forceinline__ void load_splat(const SceneK &sc, long long i, int sh
 // the fp64-vs-numpy evaluation difference (1e-15 kappa) and two roundings.
 // The alpha relative error model adds ex2.approx (2^-21.5), the rounding of o
 // and of o e, and ln 2 times the q' error: e0 = 4.7e-7 + ln2 e0q, e1 = ln2 e1q.
-// bbox = axis-aligned box of {q' <= q_hi'}; the raster refines it with the
-// exact minimum of q' over each warp's pixel rectangle.
+// The raster culls a splat per warp with the exact minimum of q' over the
+// warp's pixel rectangle against q_hi' (no box is stored).
 __device__ __forceinline__ void write_raster_record(const Workspace &ws, long long p, double m0, double m1, double ca,
                                                     double cb, double cc, double o, double qth, float qth_err) {
     const double K = 0.72134752044448170368;  // log2(e) / 2
     const double det = ca * cc - cb * cb;
     float4 rq = make_float4(-INFINITY, -INFINITY, 0.f, 0.f);
-    float4 bb = make_float4(INFINITY, -INFINITY, INFINITY, -INFINITY);
     if (qth >= 0.0) {
         // The error-model terms are upper bounds, so they are evaluated in fp32 and widened by 1.001
         // (several fp32 roundings); lmin = det / lmax has no cancellation.  Any s > 0 is a valid
@@ -188,18 +187,6 @@ __device__ __forceinline__ void write_raster_record(const Workspace &ws, long lo
         rq.y = delta < 1e6f ? __double2float_ru(qt + (double)delta) : INFINITY;
         rq.z = W * (4.7e-7f + 0.6931471805599453f * e0q);
         rq.w = W * 0.6931471805599453f * e1q;
-        // bounding box of {q <= q_hi' / k}: half extents sqrt(Q Sigma_xx), sqrt(Q Sigma_yy), Sigma = conic^-1
-        // (fp32, widened by 1e-6 relative + 1e-4 px, rounded outward)
-        const float Q = rq.y / (float)K * W;
-        if (isfinite(Q) && det > 0.0) {
-            const float rdet = 1.0f / (float)det;
-            const double hx = (double)(sqrtf(Q * (ccf * rdet)) * (1.0f + 1e-6f) + 1e-4f);
-            const double hy = (double)(sqrtf(Q * (caf * rdet)) * (1.0f + 1e-6f) + 1e-4f);
-            bb = make_float4(__double2float_rd(m0 - hx), __double2float_ru(m0 + hx), __double2float_rd(m1 - hy),
-                             __double2float_ru(m1 + hy));
-        } else {
-            bb = make_float4(-INFINITY, INFINITY, -INFINITY, INFINITY);
-        }
     }
     const double l11 = sqrt(K * ca);
     const double l21 = K * cb / l11;
@@ -226,7 +213,6 @@ __device__ __forceinline__ void write_raster_record(const Workspace &ws, long lo
     const double qw = __hiloint2double((int)__float_as_uint(w_up), (int)__float_as_uint(rq.x));  // (q_lo, w_up)
     asm volatile("st.global.v4.b64 [%0], {%1, %2, %3, %4};" ::"l"(xr), "d"(m0), "d"(m1), "d"(ca), "d"(cb) : "memory");
     asm volatile("st.global.v4.b64 [%0], {%1, %2, %3, %4};" ::"l"(xr + 4), "d"(cc), "d"(o), "d"(qw), "d"(0.0) : "memory");
-    ws.bbox[p] = bb;
 }
 
 // Block-level reduction of the per-thread frame counters: one atomic per

@@ -19,10 +19,11 @@
 // has run (5 % of C3's relevant warp-steps, SEELE_RASTER_PROFILE), so a
 // leader-first branch would not pay for itself.
 //
-// Work skipping (exact): every staged splat carries the box of pixel centres
-// that can pass its alpha test (preprocess write_raster_record).  A warp
-// whose region misses the box cannot blend or pass a leader test with that
-// splat, so it skips it; the reference still charges one lockstep step to
+// Work skipping (exact): each lane tests one staged splat -- the minimum of
+// q' over the warp's 16x8 pixel-centre rectangle (closed form in Cholesky
+// coordinates, rect_reaches) against the top of its alpha bracket with the
+// evaluation margins.  A warp whose region it misses cannot blend or pass a
+// leader test with that splat, so it skips it; the reference still charges one lockstep step to
 // every live model-warp (alpha_eval for ref, leader_eval for cr), which the
 // warp adds per skipped splat from its (unchanged) live mask.
 //
@@ -249,7 +250,6 @@ __global__ void __launch_bounds__(32 * kRWarps, SEELE_RASTER_MINB) k_raster_quad
     // records staged field-chunk major ([chunk][lane], 16 B each): a warp's cp.async writes and the cull's
     // per-lane reads are conflict-free (a 64-byte lane stride put 16 lanes on one bank group)
     __shared__ float4 s_stage[kRWarps][2][4][kBatch];
-    __shared__ float4 s_box[kRWarps][2][kBatch];
     // per pixel: tile splats it was live for (written at its death)
     __shared__ uint32_t s_di[32 * kRWarps][4];
     __shared__ float s_T[32 * kRWarps][4];  // per pixel: transmittance at its death
@@ -326,7 +326,6 @@ __global__ void __launch_bounds__(32 * kRWarps, SEELE_RASTER_MINB) k_raster_quad
             const float4 *src = reinterpret_cast<const float4 *>(ws.rec + p);
 #pragma unroll
             for (int k = 0; k < 4; k++) cp_async16(&s_stage[wslot][buf][k][lane], src + k);
-            cp_async16(&s_box[wslot][buf][lane], ws.bbox + p);
         }
         cp_async_commit();
     };
@@ -351,11 +350,9 @@ __global__ void __launch_bounds__(32 * kRWarps, SEELE_RASTER_MINB) k_raster_quad
             return r;
         };
         bool rel = false;
-        if (b0 + lane < rg.y) {
+        if (b0 + lane < rg.y) {  // (the box test of round 1 dropped: the exact refinement alone is cheaper)
             const Staged sv = staged(lane);
-            const float4 bb = s_box[wslot][buf][lane];
-            rel = bb.y >= ox + 0.5f && bb.x <= ox + 15.5f && bb.w >= oy + ry0 && bb.z <= oy + ry1;
-            if (rel) {
+            {
                 // exact refinement in tile-relative floats; the margin covers the fp32 evaluation (twice the
                 // bracket width) and the float mean, |error| <= ep = 2^-23 (|d| + 32) px, times
                 // |grad q'| <= 2 P sqrt(q')
@@ -367,7 +364,8 @@ __global__ void __launch_bounds__(32 * kRWarps, SEELE_RASTER_MINB) k_raster_quad
                 const float qh = __fadd_ru(sv.q_lo, sv.w_up), pe = P * ep;  // top of the alpha bracket
                 const float qm = qh + 2.0f * (qh - sv.q_lo) + 1e-6f * qh + 2.2f * pe * (1.0001f * sqrt_approx(fmaxf(qh, 0.f))) +
                                  1.1f * pe * pe + 1e-6f;
-                rel = rect_reaches(mx, my, sv.l11, sv.l21, sv.l22, qm, 0.5f, 15.5f, ry0, ry1);
+                // (an empty bracket, o < theta: w_up = 0, nothing can pass)
+                rel = sv.w_up > 0.0f && rect_reaches(mx, my, sv.l11, sv.l21, sv.l22, qm, 0.5f, 15.5f, ry0, ry1);
             }
         }
         uint32_t mlo = __ballot_sync(0xffffffffu, rel);
