@@ -585,13 +585,19 @@ __global__ void __launch_bounds__(kExpandThreads, SEELE_EXPAND_MINB) k_bin_expan
         seg_span(ws, seg, s, e0, e1);
         uint32_t m[kSegBatches], p[kSegBatches];
         load_segment(ws, e0, e1, m, p);
+        // per (batch, warp) pair counts of the 16 tiles: the entries' tile bits spread into bytes (four tiles
+        // per word; a count <= 32 fits a byte) and summed over the warp by four hardware reductions
 #pragma unroll
-        for (int b = 0; b < kSegBatches; b++)
+        for (int b = 0; b < kSegBatches; b++) {
+            uint32_t c[4];
 #pragma unroll
-            for (int j = 0; j < 16; j++) {
-                const uint32_t bb = __ballot_sync(0xffffffffu, (m[b] >> j) & 1u);
-                if (lane == j) s_cnt[j][b * NW + warp] = __popc(bb);
+            for (int k = 0; k < 4; k++)
+                c[k] = __reduce_add_sync(0xffffffffu, (((m[b] >> (4 * k)) & 0xfu) * 0x00204081u) & 0x01010101u);
+            if (lane < 16) {
+                const uint32_t w = (lane & 8) ? ((lane & 4) ? c[3] : c[2]) : ((lane & 4) ? c[1] : c[0]);
+                s_cnt[lane][b * NW + warp] = (w >> (8 * (lane & 3))) & 0xffu;
             }
+        }
         __syncthreads();
         // exclusive scan of every tile's 64 unit counts (warp w: tiles 2w, 2w + 1; lane: units 2l, 2l + 1)
 #pragma unroll
