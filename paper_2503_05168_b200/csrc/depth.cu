@@ -318,7 +318,7 @@ void launch_depth_sort(const Workspace &ws, const CamK &cam, long long n_max, in
         attr = true;
     }
 #ifndef SEELE_BSORT_PER_SM
-#define SEELE_BSORT_PER_SM 5
+#define SEELE_BSORT_PER_SM 8  // (vs 5: depth 0.076 -> 0.072 ms serial, C3)
 #endif
     const long long groups = n_max / kDepthGroup + 1;
     const int so_grid = (int)std::min<long long>(groups, SEELE_BSORT_PER_SM * sms);
