@@ -161,8 +161,16 @@ __device__ __forceinline__ void load_splat(const SceneK &sc, long long i, int sh
 // and of o e, and ln 2 times the q' error: e0 = 4.7e-7 + ln2 e0q, e1 = ln2 e1q.
 // The raster culls a splat per warp with the exact minimum of q' over the
 // warp's pixel rectangle against q_hi' (no box is stored).
+// 32 bytes (two float4) by one 256-bit store
+__device__ __forceinline__ void st256(float4 *dst, const float4 &a, const float4 &b) {
+    asm volatile("st.global.v8.f32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"l"(dst), "f"(a.x), "f"(a.y), "f"(a.z),
+                 "f"(a.w), "f"(b.x), "f"(b.y), "f"(b.z), "f"(b.w)
+                 : "memory");
+}
+
 __device__ __forceinline__ void write_raster_record(const Workspace &ws, long long p, double m0, double m1, double ca,
-                                                    double cb, double cc, double o, double qth, float qth_err) {
+                                                    double cb, double cc, double o, double qth, float qth_err,
+                                                    float4 &rec2) {
     const double K = 0.72134752044448170368;  // log2(e) / 2
     const double det = ca * cc - cb * cb;
     float4 rq = make_float4(-INFINITY, -INFINITY, 0.f, 0.f);
@@ -201,13 +209,14 @@ __device__ __forceinline__ void write_raster_record(const Workspace &ws, long lo
     // carry no rounding of x - mxh - mxl (one fewer than the hi + lo form the error model was derived for)
     const float l11f = (float)l11, l21f = (float)l21, l22f = (float)l22;
     const double mxl = m0 - (double)mxh, myl = m1 - (double)myh;
-    rec[0] = make_float4(mxh, (float)((double)l11f * mxl + (double)l21f * myl), myh, (float)((double)l22f * myl));
-    rec[1] = make_float4(l11f, l21f, l22f, (float)o);
+    // (the record's first and second halves are written by one 256-bit store each: full sectors)
+    st256(rec, make_float4(mxh, (float)((double)l11f * mxl + (double)l21f * myl), myh, (float)((double)l22f * myl)),
+          make_float4(l11f, l21f, l22f, (float)o));
     // (q_lo, w_up): the bracket [q_lo, q_up) as its width rounded upward, so the raster tests it on
     // d = q' - q_lo alone (0 <= d <= w_up, compared as bit patterns); an empty bracket (o < theta) has w_up = 0
     const float q_up = nextafterf(rq.y, INFINITY);
     const float w_up = rq.x == -INFINITY ? 0.0f : __double2float_ru(__dsub_ru((double)q_up, (double)rq.x));
-    rec[2] = make_float4(rq.x, w_up, rq.z * (1.0f + 1.0f / 1024.0f), rq.w * (1.0f + 1.0f / 1024.0f));
+    rec2 = make_float4(rq.x, w_up, rq.z * (1.0f + 1.0f / 1024.0f), rq.w * (1.0f + 1.0f / 1024.0f));  // (stored with the colour)
     // the exact record, whole: two 32-byte stores (full sectors, no partial-sector merging in L2)
     double *xr = reinterpret_cast<double *>(ws.xrec + p);
     const double qw = __hiloint2double((int)__float_as_uint(w_up), (int)__float_as_uint(rq.x));  // (q_lo, w_up)
@@ -388,7 +397,8 @@ __global__ void __launch_bounds__(kPre, SEELE_PRE_MINB) k_preprocess(SceneK sc, 
                         sz = z;
                         // depth-order bucket (depth.cu) of a binned splat: count it and keep its index in the bucket
                         if (n_tiles > 0) bi = atomicAdd(&ws.bhist[depth_bucket_of_key(depth_order_key(z), zbase)], 1u);
-                        write_raster_record(ws, p, m0, m1, ca, cb, cc, g.o, qth, qth_err);
+                        float4 rec2;
+                        write_raster_record(ws, p, m0, m1, ca, cb, cc, g.o, qth, qth_err, rec2);
                         // view direction for SH (preprocess.py:129-130), fp32 like the colour
                         const float rn = rsqrtf((float)(d[0] * d[0] + d[1] * d[1] + d[2] * d[2]));
                         const float vx = (float)d[0] * rn, vy = (float)d[1] * rn, vz = (float)d[2] * rn;
@@ -417,7 +427,8 @@ __global__ void __launch_bounds__(kPre, SEELE_PRE_MINB) k_preprocess(SceneK sc, 
                             col.y = sh_channel([&](int k) { return (float)shp[16 + k]; }, vx, vy, vz, cfg.sh_degree);
                             col.z = sh_channel([&](int k) { return (float)shp[32 + k]; }, vx, vy, vz, cfg.sh_degree);
                         }
-                        reinterpret_cast<float4 *>(ws.rec + p)[3] = make_float4(col.x, col.y, col.z, __uint_as_float((uint32_t)p));
+                        st256(reinterpret_cast<float4 *>(ws.rec + p) + 2, rec2,
+                              make_float4(col.x, col.y, col.z, __uint_as_float((uint32_t)p)));
                     }
                 }
             }
