@@ -146,14 +146,23 @@ __device__ __forceinline__ void load_splat(const SceneK &sc, long long i, int sh
 // rounding of each coordinate); the folded form has every rounding it has
 // except that one (cu, cw are ~2^-24 |m| |l|, their own rounding ~2^-48), so
 // the bound covers it.
-// With u = 2^-24, P = sqrt(trace(k C)) and |d| the pixel-to-mean distance:
-// |eta_dx|, |eta_dy| <= 3u (|d| + 1) and the coefficient / product roundings
-// give |q'32 - q'| <= 2u (5|d| + 3) P sqrt(q') + 4u q'.  With |d|^2 <=
-// q' / lmin' this is <= u q' (4 + 10 sqrt(tr / lmin)) + 6u P sqrt(q'),
-// linearised around the threshold (sqrt(x) <= (s + x / s) / 2, s^2 = q_th')
-// and taken with a 1.25 safety factor: |q'32 - q'| <= e0q + e1q q'.  No
-// cancellation in the sum of squares: the error grows like sqrt(kappa), not
-// kappa (the direct a dx^2 + 2b dx dy + c dy^2 form).
+// With u = 2^-24, U = l11 dx + l21 dy and W = l22 dy (exact, so q' = U^2 +
+// W^2): the coefficient roundings (u each), the rounding of dx, dy (exact
+// unless the mean is > 2^11 px away, else u each) and of t and u1 give
+// |dU| <= 2u (|l11 dx| + |l21 dy|) + u |t| + u |U| <= 3u |U| + 5u |l21 dy|
+// (|l11 dx| <= |U| + |l21 dy|), and |dW| <= 3u |W|; with the roundings of w^2
+// and of q', |q'32 - q'| <= 8u q' + 10u |U| |l21 dy|.  |U| <= sqrt(q') and
+// |l21 dy| = |l21 / l22| |W| <= (|b| / sqrt(det)) sqrt(q') (l21 / l22 =
+// b / sqrt(det) for the conic (a, b, c)), so the cancellation term is
+// 10u q' |b| / sqrt(det): it vanishes for axis-aligned ellipses, and is at most
+// 10u q' sqrt(kappa / 2) (round 1 bounded it by 10u q' sqrt(kappa) through |d|:
+// the C4 scene's transmittance walks fall from 623K to 227K per frame with the
+// tighter form).  Round 1's additive terms 6u P sqrt(q') (mean and pixel
+// representation) are kept.  Linearised around the threshold (sqrt(x) <=
+// (s + x / s) / 2, s^2 = q_th') and taken with a 1.25 safety factor:
+// |q'32 - q'| <= e0q + e1q q'.  No cancellation in the sum of squares: the
+// error grows like sqrt(kappa), not kappa (the direct a dx^2 + 2b dx dy + c dy^2
+// form).
 // The alpha-test bracket [q_lo', q_hi'] widens q_th' = k 2 ln(o / theta)
 // (rasterize.py:146-151, 209: alpha >= theta <=> q <= q_th) by that bound,
 // the fp64-vs-numpy evaluation difference (1e-15 kappa) and two roundings.
@@ -189,7 +198,9 @@ __device__ __forceinline__ void write_raster_record(const Workspace &ws, long lo
         const float P = W * sqrtf((float)K * trf);
         const float sq = fmaxf(sqrtf(qtf), 1e-3f);
         const float e0q = W * 1.25f * 3.0f * u * P * sq;
-        const float e1q = W * 1.25f * (u * (4.0f + 10.0f * sqrtf(kap)) + 3.0f * u * P / sq);
+        // the cancellation term: |l21 dy| <= |l21 / l22| |l22 dy| <= (|b| / sqrt(det)) sqrt(q') (derivation above)
+        const float bsd = (float)(fabs(cb) / sqrt(fmax(det, 1e-300)));
+        const float e1q = W * 1.25f * (u * (8.0f + 10.0f * bsd) + 3.0f * u * P / sq);
         const float delta = W * (e0q + e1q * qtf + qtf * (1e-15f * 2.0f * kap + 2.0f * u) + (float)K * qth_err) + 1e-30f;
         rq.x = __double2float_rd(qt - (double)delta);
         rq.y = delta < 1e6f ? __double2float_ru(qt + (double)delta) : INFINITY;
