@@ -131,3 +131,67 @@ def test_cancellation_term_vanishes_for_axis_aligned():
     P = np.sqrt(K * 0.52)
     sq = np.sqrt(K * qth[0])
     assert np.isclose(b[0], 3 * U * P * sq + U * 8.0 + 3 * U * P / sq)
+
+
+def _round_dir(x, up):
+    """x (long double) rounded to float32 toward +inf (up) or -inf."""
+    r = _r32(x)
+    rl = r.astype(ld)
+    if up:
+        return np.where(rl < x, np.nextafter(r, f32(np.inf)), r)
+    return np.where(rl > x, np.nextafter(r, f32(-np.inf)), r)
+
+
+def test_transmittance_bound_holds_under_adversarial_alpha_errors():
+    """raster_fast.cu blend step: T32 and the lower bound L = T32 - D of the exact transmittance.
+
+    Every step's q'32 sits at the edge of the certified q' error (both signs) and ex2.approx at the edge of
+    its 2^-21.5 relative error; the reference alpha is min(o 2^-q', 0.99) in fp64 and T the fp64 product
+    (rasterize.py:146-177).  After every blend L <= T <= 2 T32 - L (the kernel's live / done tests) must hold.
+    """
+    rng = np.random.default_rng(5168)
+    n_pix, n_steps = 4096, 600
+    W = 1.001
+    T32 = np.ones(n_pix, f32)
+    L = np.ones(n_pix, f32)
+    T = np.ones(n_pix, f64)
+    mode = np.arange(n_pix) % 3  # 0: errors push alpha up, 1: down, 2: random signs per step
+    worst = 0.0
+    for step in range(n_steps):
+        ca, cb, cc, _, _, qth = _splats(rng, n_pix)
+        o = rng.uniform(1.0 / 255.0, 1.0, n_pix)
+        o[rng.uniform(0, 1, n_pix) < 0.05] = rng.uniform(0.99, 1.0)  # the alpha clamp
+        qth = 2.0 * np.log(o * 255.0)
+        qt = K * qth
+        det, tr = ca * cc - cb * cb, ca + cc
+        P = W * np.sqrt(K * tr)
+        sq = np.maximum(np.sqrt(qt), 1e-3)
+        bsd = np.abs(cb) / np.sqrt(det)
+        e0q = W * 1.25 * 3.0 * U * P * sq
+        e1q = W * 1.25 * (U * (8.0 + 10.0 * bsd) + 3.0 * U * P / sq)
+        e0r = _r32(W * (4.7e-7 + np.log(2.0) * e0q) * (1.0 + 1.0 / 1024.0))
+        e1r = _r32(W * np.log(2.0) * e1q * (1.0 + 1.0 / 1024.0))
+        qp = rng.uniform(0.0, 1.0, n_pix) ** 2 * qt  # exact q' of a passing pixel (alpha >= theta)
+        sgn = np.where(mode == 0, -1.0, np.where(mode == 1, 1.0, rng.choice([-1.0, 1.0], n_pix)))
+        dq = (e0q + e1q * qp) / (1.25 * W) * 0.999  # the derived bound's edge (test_fp32_q_bound_...)
+        q32 = np.maximum(_r32(qp + sgn * dq), f32(0))
+        ex = _r32(np.exp2(-q32.astype(f64)) * (1.0 - sgn * 2.0 ** -21.5 * 0.999))
+        al = fmul(_r32(o), ex)
+        al = np.where(_r32(o) > f32(0.99), np.minimum(al, f32(0.99)), al)
+        E = fma(e1r, q32, e0r)
+        wgt = fmul(T32, al)
+        omm = fadd(np.ones_like(al), -al)
+        efm = fma(al, E, np.full_like(al, f32(1e-7)))
+        t1 = fadd(T32, -wgt)
+        te = _round_dir(T32.astype(ld) * efm.astype(ld), up=True)
+        l1 = _round_dir(L.astype(ld) * omm.astype(ld) - te.astype(ld), up=False)
+        T = T * (1.0 - np.minimum(o * np.exp2(-qp), 0.99))
+        T32, L = t1, l1
+        upper = _round_dir(2.0 * T32.astype(ld) - L.astype(ld), up=True).astype(f64)
+        assert np.all(L.astype(f64) <= T), step
+        assert np.all(T <= upper), step
+        live = T > 1e-30
+        if live.any():
+            worst = max(worst, float(np.max(np.abs(T32.astype(f64) - T)[live] / (T32 - L).astype(f64)[live])))
+    print("worst |T32 - T| / D:", worst)
+    assert worst > 0.01  # the adversarial errors reach a visible part of D
