@@ -151,13 +151,15 @@ __device__ __forceinline__ void load_splat(const SceneK &sc, long long i, int sh
 // unless the mean is > 2^11 px away, else u each) and of t and u1 give
 // |dU| <= 2u (|l11 dx| + |l21 dy|) + u |t| + u |U| <= 3u |U| + 5u |l21 dy|
 // (|l11 dx| <= |U| + |l21 dy|), and |dW| <= 3u |W|; with the roundings of w^2
-// and of q', |q'32 - q'| <= 8u q' + 10u |U| |l21 dy|.  |U| <= sqrt(q') and
-// |l21 dy| = |l21 / l22| |W| <= (|b| / sqrt(det)) sqrt(q') (l21 / l22 =
-// b / sqrt(det) for the conic (a, b, c)), so the cancellation term is
-// 10u q' |b| / sqrt(det): it vanishes for axis-aligned ellipses, and is at most
-// 10u q' sqrt(kappa / 2) (round 1 bounded it by 10u q' sqrt(kappa) through |d|:
-// the C4 scene's transmittance walks fall from 623K to 227K per frame with the
-// tighter form).  Round 1's additive terms 6u P sqrt(q') (mean and pixel
+// and of q', |q'32 - q'| <= 8u q' + 10u |U| |l21 dy|.  |l21 dy| = |l21 / l22|
+// |W| (l21 / l22 = b / sqrt(det) for the conic (a, b, c)) and |U| |W| <=
+// (U^2 + W^2) / 2 = q' / 2, so the cancellation term is 5u q' |b| / sqrt(det):
+// it vanishes for axis-aligned ellipses, and is at most 5u q' sqrt(kappa / 2)
+// (round 1 bounded it by 10u q' sqrt(kappa) through |d|: the C4 scene's
+// transmittance walks fall from 623K to 227K per frame with |U|, |W| <=
+// sqrt(q') taken apart, and further with their product bounded together;
+// tests/test_qbound.py replays the fp32 sequence against the bound).  Round 1's
+// additive terms 6u P sqrt(q') (mean and pixel
 // representation) are kept.  Linearised around the threshold (sqrt(x) <=
 // (s + x / s) / 2, s^2 = q_th') and taken with a 1.25 safety factor:
 // |q'32 - q'| <= e0q + e1q q'.  No cancellation in the sum of squares: the
@@ -198,9 +200,10 @@ __device__ __forceinline__ void write_raster_record(const Workspace &ws, long lo
         const float P = W * sqrtf((float)K * trf);
         const float sq = fmaxf(sqrtf(qtf), 1e-3f);
         const float e0q = W * 1.25f * 3.0f * u * P * sq;
-        // the cancellation term: |l21 dy| <= |l21 / l22| |l22 dy| <= (|b| / sqrt(det)) sqrt(q') (derivation above)
+        // the cancellation term: 10u |U| |l21 dy| = 10u (|b| / sqrt(det)) |U| |W| <= 5u (|b| / sqrt(det)) q'
+        // (derivation above)
         const float bsd = (float)(fabs(cb) / sqrt(fmax(det, 1e-300)));
-        const float e1q = W * 1.25f * (u * (8.0f + 10.0f * bsd) + 3.0f * u * P / sq);
+        const float e1q = W * 1.25f * (u * (8.0f + 5.0f * bsd) + 3.0f * u * P / sq);
         const float delta = W * (e0q + e1q * qtf + qtf * (1e-15f * 2.0f * kap + 2.0f * u) + (float)K * qth_err) + 1e-30f;
         rq.x = __double2float_rd(qt - (double)delta);
         rq.y = delta < 1e6f ? __double2float_ru(qt + (double)delta) : INFINITY;

@@ -89,7 +89,7 @@ def _derived_bound(ca, cb, cc, qth, q):
     sq = np.maximum(np.sqrt(qt), 1e-3)
     bsd = np.abs(cb) / np.sqrt(np.maximum(det, 1e-300))
     e0q = 3.0 * U * P * sq
-    e1q = U * (8.0 + 10.0 * bsd) + 3.0 * U * P / sq
+    e1q = U * (8.0 + 5.0 * bsd) + 3.0 * U * P / sq
     return e0q + e1q * q
 
 
@@ -168,7 +168,7 @@ def test_transmittance_bound_holds_under_adversarial_alpha_errors():
         sq = np.maximum(np.sqrt(qt), 1e-3)
         bsd = np.abs(cb) / np.sqrt(det)
         e0q = W * 1.25 * 3.0 * U * P * sq
-        e1q = W * 1.25 * (U * (8.0 + 10.0 * bsd) + 3.0 * U * P / sq)
+        e1q = W * 1.25 * (U * (8.0 + 5.0 * bsd) + 3.0 * U * P / sq)
         e0r = _r32(W * (4.7e-7 + np.log(2.0) * e0q) * (1.0 + 1.0 / 1024.0))
         e1r = _r32(W * np.log(2.0) * e1q * (1.0 + 1.0 / 1024.0))
         qp = rng.uniform(0.0, 1.0, n_pix) ** 2 * qt  # exact q' of a passing pixel (alpha >= theta)
