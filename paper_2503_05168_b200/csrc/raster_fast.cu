@@ -37,9 +37,10 @@
 //  * transmittance: alpha32 = min(o 2^-q'32, 0.99) has relative error
 //    <= e0 + e1 q'; 1 - alpha32 is exact for alpha >= 0.5 and within 2^-25
 //    otherwise.  Each pixel carries T in fp32 and a bound D >= |T32 - T|,
-//    D' = D (1 - alpha) + T (alpha (e0 + e1 q') + 1e-7), products rounded
-//    upward.  A clear sign of T32 - (D + gamma) (rounded up) proves T >=
-//    gamma; otherwise T + D < gamma proves the pixel done, and in between
+//    D' = D (1 - alpha) + T alpha (e0 + e1 q') + 1e-7 T, products rounded
+//    upward (the 1e-7 T term on every live step, blending or not).  A clear
+//    sign of T32 - (D + gamma) (rounded up) proves T >= gamma; otherwise
+//    T + D < gamma proves the pixel done, and in between
 //    its transmittance is recomputed exactly in fp64 over the tile list so
 //    far (exact_transmittance, warp-cooperative) and the decision is the
 //    reference's.
@@ -477,13 +478,16 @@ __global__ void __launch_bounds__(32 * kRWarps, SEELE_RASTER_MINB) k_raster_quad
                 const float2 nam = make_float2(-am.x, -am.y);  // (a negated operand, no instruction)
                 const float2 omm = __fadd2_rn(f2(1.0f), nam);  // 1 - alpha, or 1
                 // |omm - (1 - alpha_ref)| <= alpha (e0 + e1 q'); the new T = T - T alpha has one rounding of
-                // the exact T (1 - alpha32) after the rounding of T alpha, together <= 2^-24 T: the 1e-7 T term
-                const float2 efm = __fmul2_rn(__ffma2_rn(al[r], E[r], f2(1.0e-7f)), m[r]);
+                // the exact T (1 - alpha32) after the rounding of T alpha, together <= 2^-24 T: the 1e-7 T term,
+                // charged on every live step (a step that does not blend only loosens D by it: two
+                // instructions fewer than masking it)
+                const float2 c7 = __fmul2_ru(t0, f2(1.0e-7f));
                 const float2 t1 = __fadd2_rn(t0, make_float2(-wgt.x, -wgt.y));
-                // the bound kept as L = T32 - D: L' = L omm - T efm rounded down is T32' - D' for the D
-                // recurrence D' = D omm + T efm rounded up, so T32' - (T32' - L') bounds T from below and
+                // the bound kept as L = T32 - D: L' = L omm - te rounded down, te = T alpha E + 1e-7 T rounded
+                // up (the 2^-10 widening of e0, e1 covers the rounding of T alpha in wgt), is T32' - D' for
+                // the D recurrence D' = D omm + te, so T32' - (T32' - L') bounds T from below and
                 // T32' + (T32' - L') from above
-                const float2 te = __fmul2_ru(t0, efm);
+                const float2 te = __ffma2_ru(wgt, E[r], c7);
                 const float2 l1 = __ffma2_rd(L[r], omm, make_float2(-te.x, -te.y));
                 T[r] = t1;
                 L[r] = l1;
