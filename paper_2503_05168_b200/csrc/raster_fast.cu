@@ -289,7 +289,11 @@ __global__ void __launch_bounds__(32 * kRWarps, SEELE_RASTER_MINB) k_raster_quad
     bool qlive = nlive != 0;
     unsigned lb = __ballot_sync(0xffffffffu, qlive);
     const float lx0 = (float)x0 + 0.5f, ly0 = (float)y0 + 0.5f;  // centre of pixel 0 (exact in fp32)
-    const float2 lxp = make_float2(lx0, lx0 + 1.0f), lyp = make_float2(ly0, ly0 + 1.0f);
+    float2 lxp = make_float2(lx0, lx0 + 1.0f), lyp = make_float2(ly0, ly0 + 1.0f);
+    // the pixel-centre pairs through an opaque move: the compiler otherwise rebuilds the pair registers
+    // (lx0 + 1) every step for the packed subtractions
+    asm volatile("mov.b64 %0, %0;" : "+l"(*reinterpret_cast<unsigned long long *>(&lxp)));
+    asm volatile("mov.b64 %0, %0;" : "+l"(*reinterpret_cast<unsigned long long *>(&lyp)));
     // w = 4: the group is the 2x2 of quads whose top-left quad holds the leader pixel
     const int g_off = (i & 2);
     const int leader_lane = (lane & ~7) + g_off;
