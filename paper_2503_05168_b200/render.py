@@ -60,6 +60,24 @@ class EngineConfig:
 
 
 @dataclass
+class WarpCost:
+    """Lockstep step counters, summed over warps (rasterize.py:36-48).  The
+    GPU raster produces them per frame (FrameStats); this mirrors the
+    reference's accumulator for callers that sum costs themselves."""
+
+    alpha_eval_steps: int = 0
+    blend_steps: int = 0
+    leader_eval_steps: int = 0
+    warp_steps: int = 0
+
+    def add(self, other: "WarpCost") -> None:
+        self.alpha_eval_steps += other.alpha_eval_steps
+        self.blend_steps += other.blend_steps
+        self.leader_eval_steps += other.leader_eval_steps
+        self.warp_steps += other.warp_steps
+
+
+@dataclass
 class FrameStats:
     """Per-frame counters (rasterize.py:51-86)."""
 
@@ -74,6 +92,13 @@ class FrameStats:
     stalls: int = 0
     prefetch_hits: int = 0
     wall_ms: float = 0.0
+
+    def add_cost(self, cost: WarpCost) -> None:
+        """rasterize.py:66-70."""
+        self.alpha_eval_steps += cost.alpha_eval_steps
+        self.blend_steps += cost.blend_steps
+        self.leader_eval_steps += cost.leader_eval_steps
+        self.warp_steps += cost.warp_steps
 
     def as_dict(self) -> dict:
         return {k: getattr(self, k) for k in (
@@ -135,6 +160,20 @@ class SortedTileRange:
 
 
 INTERSECTION_DTYPE = np.dtype([("tile_id", "<i8"), ("gaussian_ref", "<i8"), ("depth", "<f8")])
+
+
+@dataclass(frozen=True)
+class TileIntersection:
+    """One (tile, splat) pair surviving the binning test (preprocess.py:59-65);
+    ``FramePlan.sorted_pairs`` holds them as INTERSECTION_DTYPE records."""
+
+    tile_id: int
+    gaussian_ref: int
+    depth: float
+
+    @classmethod
+    def from_record(cls, rec) -> "TileIntersection":
+        return cls(int(rec["tile_id"]), int(rec["gaussian_ref"]), float(rec["depth"]))
 
 
 @dataclass

@@ -156,3 +156,30 @@ def test_select_rejects_m_ge_n():
     mean = (ctypes.c_double * 3)(0, 0, 0)
     rc = lib.seele_select_clusters(ctypes.byref(camc), dummy, 4, 4, 1.0, mean, 1.0, dummy, dummy, dummy, None)
     assert rc == 1 and b"m must be" in lib.seele_last_error()
+
+
+def test_warp_cost_and_tile_intersection_mirror_the_reference():
+    """rasterize.py:36-70 (WarpCost, FrameStats.add_cost), preprocess.py:59-65 (TileIntersection),
+    rasterize.py:154-156 (_check_sorted)."""
+    import numpy as np
+    import pytest
+
+    from paper_2503_05168_b200 import FrameStats, TileIntersection, WarpCost
+    from paper_2503_05168_b200.errors import ContractViolationError
+    from paper_2503_05168_b200.render import INTERSECTION_DTYPE, check_sorted_depths
+
+    total = WarpCost()
+    total.add(WarpCost(alpha_eval_steps=3, blend_steps=2, leader_eval_steps=1, warp_steps=4))
+    total.add(WarpCost(alpha_eval_steps=1, blend_steps=1, leader_eval_steps=0, warp_steps=2))
+    st = FrameStats(tile_pairs=7)
+    st.add_cost(total)
+    assert (st.alpha_eval_steps, st.blend_steps, st.leader_eval_steps, st.warp_steps, st.tile_pairs) == (4, 3, 1, 6, 7)
+    rec = np.zeros(1, dtype=INTERSECTION_DTYPE)
+    rec[0] = (5, 11, 2.5)
+    ti = TileIntersection.from_record(rec[0])
+    assert ti == TileIntersection(tile_id=5, gaussian_ref=11, depth=2.5)
+    with pytest.raises(Exception):
+        ti.depth = 1.0  # frozen like the reference's
+    check_sorted_depths(np.array([1.0, 1.0, 2.0]))
+    with pytest.raises(ContractViolationError):
+        check_sorted_depths(np.array([2.0, 1.0]))
